@@ -1,0 +1,208 @@
+/*
+ * sfx.h -- C ABI of the B200-native execution path for the Specx/seqflow
+ * sequential-task-flow runtime (reference: /root/reference/pkg/src/seqflow).
+ *
+ * Plain pointers, sizes and integers only; no torch or CUDA types.  Every
+ * entry point returns an int status (SFX_OK = 0, negative = error) and the
+ * message of the last error on this runtime is available from
+ * sfx_last_error().  Calls come from ONE inserter thread per runtime
+ * (reference graph.py:85-90); executors, event-completion threads and
+ * copies are internal.
+ *
+ * Reference interface each entry point replaces (file:line relative to
+ * pkg/src/seqflow/):
+ *   sfx_create / sfx_destroy ...... create_engine engine.py:280, ComputeEngine
+ *                                   __init__ engine.py:180-198, stop() 247-258,
+ *                                   WorkerTeam.of_host_and_device_workers 58-68
+ *   sfx_graph_create .............. TaskGraph.__init__ graph.py:34 +
+ *                                   compute_on graph.py:57-64
+ *   sfx_register / sfx_unregister . HandleRegistry.ensure/unregister
+ *                                   handles.py:159-182 (+ the movable protocol
+ *                                   device.py:136-194: a host pointer and a 2-D
+ *                                   descriptor replace move_to/from_device)
+ *   sfx_submit .................... TaskGraph.task / _insert_raw graph.py:77-166
+ *                                   (+ append_access handles.py:209-236,
+ *                                   dispatch_ready graph.py:176-182)
+ *   sfx_wait_all .................. TaskGraph.wait_all graph.py:199-217
+ *   sfx_wait_task ................. TaskViewer.wait task.py:233-239
+ *   sfx_flush ..................... TaskGraph.flush_to_host graph.py:258-260
+ *   sfx_stats ..................... Mover meters device.py:22-46
+ *   sfx_trace ..................... TraceRecorder.export_events trace.py:78-84
+ *   sfx_edges ..................... successor_edges / render_dot trace.py:94-135
+ *   sfx_pause / sfx_resume ........ the gate task of the reference's gated
+ *                                   insertion protocol (tests/conftest.py:184-203)
+ */
+#ifndef SFX_H
+#define SFX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFX_ABI_VERSION 1
+
+/* ---- status codes (map 1:1 onto the reference exception classes) ---- */
+#define SFX_OK 0
+#define SFX_TIMEOUT 1              /* wait_all: timeout expired (returns False)     */
+#define SFX_ERR_CONFIG (-2)        /* ConfigurationError (errors.py:12-13)          */
+#define SFX_ERR_STAGING (-3)       /* StagingError (errors.py:36-37)                */
+#define SFX_ERR_ENGINE_FAILED (-4) /* EngineFailedError (errors.py:32-33); cause via
+                                      sfx_failure()                                 */
+#define SFX_ERR_CUDA (-5)          /* CUDA runtime error (cause of an engine failure) */
+#define SFX_ERR_INTERNAL (-6)      /* InternalConsistencyError (errors.py:20-21)    */
+#define SFX_ERR_DUPLICATE (-7)     /* DuplicateAccessError (errors.py:16-17)        */
+#define SFX_ERR_REGISTRATION (-8)  /* RegistrationError (errors.py:8-9)             */
+#define SFX_ERR_UNSUPPORTED (-9)   /* op needs a CUDA device (sim backend)          */
+
+/* ---- access modes (access.py:16-21) ---- */
+#define SFX_READ 0
+#define SFX_WRITE 1
+#define SFX_ATOMIC_WRITE 2
+#define SFX_COMMUTATIVE_WRITE 3
+#define SFX_MAYBE_WRITE 4
+
+/* ---- runtime flags ---- */
+#define SFX_FLAG_SIM 1u    /* host-memory simulated devices: bookkeeping tests only;
+                              tile ops are refused with SFX_ERR_UNSUPPORTED       */
+#define SFX_FLAG_TRACE 2u  /* record Push/Pop/Start/End (CUDA-event timestamps)     */
+#define SFX_FLAG_PAUSED 4u /* start with executors held (gated insertion)           */
+
+/* ---- schedulers (scheduler.py:66-126) ---- */
+#define SFX_SCHED_FIFO 0
+#define SFX_SCHED_PRIO 1
+
+/* ---- dtypes ---- */
+#define SFX_DTYPE_BYTES 0
+#define SFX_DTYPE_F64 1
+#define SFX_DTYPE_I64 2
+
+/* ---- ops (operands are the task's accesses in declaration order) ---- */
+#define SFX_OP_NOOP 0          /* any accesses; no data movement beyond staging     */
+#define SFX_OP_SPIN 1          /* busy-wait iparam[0] ns on the device (overhead bench) */
+#define SFX_OP_CELL 2          /* int64 cell arithmetic of the reference random programs
+                                  (tests/conftest.py:87-124): iparam = {kind, a, b}   */
+#define SFX_OP_BYTES_ADD 3     /* bytes[off:off+len] += delta (mod 256): iparam={off,len,delta} */
+#define SFX_OP_FLUSH 4         /* runtime-internal host flush (write or read mode)    */
+#define SFX_OP_DGEMM 10        /* C = beta*C + alpha*A*op(B); fparam={alpha,beta}, iparam[0]=trans_b */
+#define SFX_OP_DSYRK 11        /* C = beta*C + alpha*A*A^T, lower; fparam={alpha,beta} */
+#define SFX_OP_DTRSM 12        /* B = B * L^-T  (right, lower, transposed, non-unit)   */
+#define SFX_OP_DPOTRF 13       /* A = L*L^T in place, lower                            */
+#define SFX_OP_P2P_PAIR 20     /* particles: P_i, P_j (read), F_i, F_j (commutative)   */
+#define SFX_OP_P2P_SELF 21     /* particles: P_i (read), F_i (commutative)             */
+#define SFX_OP_FILL_UNIFORM 30 /* A = splitmix64 uniform[0,1): iparam={seed,row0,col0,ncols_total} */
+#define SFX_OP_FILL_SPD 31     /* A = (R+R^T)/2 + n*I tile: iparam={seed,row0,col0,n}    */
+#define SFX_OP_FILL_PARTICLES 32 /* P (4 x n SoA x,y,z,q): iparam={seed,first_particle}  */
+#define SFX_OP_ZERO 33         /* A = 0                                                  */
+
+/* ---- trace event kinds (trace.py:14-21) ---- */
+#define SFX_EV_PUSH 0
+#define SFX_EV_POP 1
+#define SFX_EV_START 2
+#define SFX_EV_END 3
+#define SFX_EV_STAGE_BEGIN 4
+#define SFX_EV_STAGE_END 5
+
+/* ---- task states (task.py:11-16) ---- */
+#define SFX_STATE_INSERTED 0
+#define SFX_STATE_READY 1
+#define SFX_STATE_EXECUTING 2
+#define SFX_STATE_FINISHED 3
+
+typedef struct sfx_runtime sfx_runtime;
+
+typedef struct sfx_task_desc {
+  uint64_t tid;       /* caller-assigned, process-global (task.py:63-69)         */
+  uint32_t graph;     /* from sfx_graph_create                                    */
+  uint32_t op;        /* SFX_OP_*                                                 */
+  int32_t priority;   /* PriorityScheduler key (-priority, seq) scheduler.py:111  */
+  int32_t device;     /* placement hint, -1 = locality-aware scheduler decides    */
+  uint32_t n_access;  /* this task's accesses, consecutive in the access array    */
+  uint32_t flags;     /* reserved, 0                                               */
+  double fparam[4];
+  int64_t iparam[4];
+} sfx_task_desc;
+
+typedef struct sfx_access {
+  uint64_t hid;  /* registered handle id */
+  uint32_t mode; /* SFX_READ ...          */
+  uint32_t reserved;
+} sfx_access;
+
+typedef struct sfx_dev_stats {
+  /* Mover meters (device.py:26-30) */
+  uint64_t bytes_to_device, copies_to_device;     /* host -> device */
+  uint64_t bytes_from_device, copies_from_device; /* device -> host */
+  uint64_t bytes_p2p_in, copies_p2p_in;           /* peer -> this device (NVLink) */
+  /* tile cache */
+  uint64_t hits, misses, evictions, writebacks;
+  uint64_t blocks, bytes_in_use, capacity;
+  /* executor */
+  uint64_t tasks_executed, kernel_launches, stream_waits;
+} sfx_dev_stats;
+
+typedef struct sfx_event {
+  int64_t t_ns;   /* CLOCK_MONOTONIC ns (same clock as Python perf_counter_ns) */
+  uint64_t tid;
+  int32_t kind;   /* SFX_EV_* */
+  int32_t worker; /* device * streams_per_dev + stream; -1 inserter            */
+  int64_t extra;  /* hid for stage events                                       */
+} sfx_event;
+
+int sfx_abi_version(void);
+/* number of CUDA devices visible (0 without a driver/GPU) */
+int sfx_device_count(int* n);
+
+/* ndev devices (ordinals[i]; NULL = 0..ndev-1), streams_per_dev streams each
+ * (WorkerTeam workers_per_device), arena_bytes[i] per device (NULL or 0 =
+ * default: free HBM minus a reserve on CUDA, 16 MiB in sim).  window = max
+ * in-flight tasks per device (0 = 4 * streams_per_dev). */
+int sfx_create(int ndev, const int* ordinals, int streams_per_dev, const uint64_t* arena_bytes,
+               uint32_t sched, uint32_t flags, uint32_t window, sfx_runtime** out);
+int sfx_destroy(sfx_runtime* rt);
+const char* sfx_last_error(sfx_runtime* rt);
+/* first failure that poisoned the engine: its status code and message */
+int sfx_failure(sfx_runtime* rt, int* code, char* msg, uint64_t cap);
+
+int sfx_graph_create(sfx_runtime* rt, uint32_t* gid);
+int sfx_register(sfx_runtime* rt, uint32_t gid, uint64_t hid, void* host, uint64_t bytes, int64_t rows,
+                 int64_t cols, int64_t ld, int32_t dtype);
+/* owner hint for the locality-aware scheduler (2-D block-cyclic distribution) */
+int sfx_set_home(sfx_runtime* rt, uint64_t hid, int32_t device);
+int sfx_unregister(sfx_runtime* rt, uint64_t hid);
+
+int sfx_submit(sfx_runtime* rt, uint32_t n, const sfx_task_desc* tasks, const sfx_access* accesses);
+int sfx_pause(sfx_runtime* rt);
+int sfx_resume(sfx_runtime* rt);
+/* SFX_OK when every task of the graph completed, SFX_TIMEOUT, or an error */
+int sfx_wait_all(sfx_runtime* rt, uint32_t gid, double timeout_s);
+int sfx_wait_task(sfx_runtime* rt, uint64_t tid, double timeout_s);
+int sfx_task_state(sfx_runtime* rt, uint64_t tid, int32_t* state);
+/* insert a flush of hid to its host buffer: write_mode=1 is the reference's
+ * flush_to_host (host write: device copies dropped), 0 keeps device copies */
+int sfx_flush(sfx_runtime* rt, uint32_t gid, uint64_t tid, uint64_t hid, int32_t write_mode);
+
+int sfx_stats(sfx_runtime* rt, int dev, sfx_dev_stats* out);
+/* resident block handle ids of a device arena (LRU parity tests) */
+int sfx_resident(sfx_runtime* rt, int dev, uint64_t* hids, uint64_t cap, uint64_t* n);
+/* per-device coherency state of hid: bit0 valid, bit1 dirty; *host_valid */
+int sfx_block_state(sfx_runtime* rt, uint64_t hid, int32_t dev, int32_t* state, int32_t* host_valid);
+int sfx_trace(sfx_runtime* rt, uint32_t gid, sfx_event* buf, uint64_t cap, uint64_t* n);
+/* successor edges of a graph: (src tid, dst tid, hid) triples, one per handle pair */
+int sfx_edges(sfx_runtime* rt, uint32_t gid, uint64_t* src, uint64_t* dst, uint64_t* hid, uint64_t cap,
+              uint64_t* n);
+/* conflict instrumentation (handles.py:88-107): violations observed */
+int sfx_violations(sfx_runtime* rt, uint64_t* n);
+
+/* pinned host memory (cudaHostAlloc; aligned malloc in sim) for tiles */
+int sfx_host_alloc(uint64_t bytes, int sim, void** out);
+int sfx_host_free(void* p, int sim);
+
+/* FP64 DMMA throughput microbenchmark on a device (roofline denominator) */
+int sfx_fp64_peak(int ordinal, double* tflops, double* sm_mhz);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFX_H */

@@ -1,0 +1,97 @@
+"""In-tree build of libsfx.so (the C-ABI runtime + sm_100a kernels).
+
+``python -m paper_2308_15964_b200.build`` compiles every source under
+``csrc/`` with nvcc for ``-gencode arch=compute_100a,code=sm_100a`` and links
+``paper_2308_15964_b200/libsfx.so`` (static cudart, so the library loads on a
+machine without a GPU; it only needs the driver when a CUDA runtime is
+created).  Objects are cached in ``build/`` and rebuilt when a source or any
+header is newer.
+"""
+
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OUT = os.path.join(PKG, "libsfx.so")
+OBJDIR = os.path.join(ROOT, "build", "sfx")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+
+
+def _nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found: cannot build libsfx.so")
+
+
+def _sources():
+    out = []
+    for dirpath, _, files in os.walk(CSRC):
+        for f in sorted(files):
+            if f.endswith((".cu", ".cpp")):
+                out.append(os.path.join(dirpath, f))
+    return sorted(out)
+
+
+def _headers():
+    hs = [os.path.join(ROOT, "include", "sfx.h")]
+    for dirpath, _, files in os.walk(CSRC):
+        hs += [os.path.join(dirpath, f) for f in files if f.endswith((".h", ".cuh"))]
+    return hs
+
+
+def _compile(nvcc, src, obj):
+    cmd = [nvcc] + ARCH + COMMON + ["-c", src, "-o", obj]
+    if src.endswith(".cpp"):
+        cmd = [nvcc, "-x", "cu"] + ARCH + COMMON + ["-c", src, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"compile failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return obj
+
+
+def build(verbose: bool = False, force: bool = False) -> str:
+    nvcc = _nvcc()
+    os.makedirs(OBJDIR, exist_ok=True)
+    newest_header = max(os.path.getmtime(h) for h in _headers() if os.path.exists(h))
+    jobs = []
+    objs = []
+    for src in _sources():
+        rel = os.path.relpath(src, CSRC).replace(os.sep, "_")
+        obj = os.path.join(OBJDIR, rel + ".o")
+        objs.append(obj)
+        stale = (force or not os.path.exists(obj)
+                 or os.path.getmtime(obj) < max(os.path.getmtime(src), newest_header))
+        if stale:
+            jobs.append((src, obj))
+    if jobs:
+        with cf.ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
+            futs = [ex.submit(_compile, nvcc, s, o) for s, o in jobs]
+            for f in futs:
+                o = f.result()
+                if verbose:
+                    print("compiled", os.path.relpath(o, ROOT))
+    if jobs or not os.path.exists(OUT):
+        tmp = OUT + ".tmp"
+        cmd = [nvcc] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs + ["-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+        os.replace(tmp, OUT)
+        if verbose:
+            print("linked", os.path.relpath(OUT, ROOT))
+    return OUT
+
+
+if __name__ == "__main__":
+    build(verbose=True, force="--force" in sys.argv)

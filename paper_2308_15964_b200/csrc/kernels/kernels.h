@@ -1,0 +1,35 @@
+// Internal launch interface of the sm_100a tile kernels (not part of the C ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sfx {
+
+bool make_tmap_f64_2d(CUtensorMap* tm, const double* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                      uint32_t box_inner, uint32_t box_outer, bool swizzle128);
+
+// C = beta*C + alpha*A*op(B); op(B) = B^T ([N x K] storage) if trans_b else B ([K x N]).
+// lower: only row >= col of C is computed/stored (square C).
+cudaError_t launch_dgemm(const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc,
+                         int M, int N, int K, double alpha, double beta, bool trans_b, bool lower,
+                         cudaStream_t stream);
+
+cudaError_t launch_dtrsm(const double* L, long long ldl, double* B, long long ldb, int M, int n, cudaStream_t s);
+cudaError_t launch_dpotrf(double* A, long long lda, int n, int* info, cudaStream_t s);
+cudaError_t launch_p2p(const double* Pi, long long ldpi, int ni, const double* Pj, long long ldpj, int nj, double* Fi,
+                       long long ldfi, double* Fj, long long ldfj, bool self, double eps2, cudaStream_t s);
+
+cudaError_t launch_fill_uniform(double* a, long long rows, long long cols, long long ld, long long seed,
+                                long long row0, long long col0, long long ncols_total, cudaStream_t s);
+cudaError_t launch_fill_spd(double* a, long long rows, long long cols, long long ld, long long seed, long long row0,
+                            long long col0, long long n, cudaStream_t s);
+cudaError_t launch_fill_particles(double* p, long long n, long long ld, long long seed, long long first,
+                                  cudaStream_t s);
+cudaError_t launch_spin(long long ns, cudaStream_t s);
+cudaError_t launch_cell(long long* target, const long long* const* reads, int nreads, long long kind, long long a,
+                        long long b, cudaStream_t s);
+cudaError_t launch_bytes_add(unsigned char* p, long long off, long long len, long long delta, cudaStream_t s);
+cudaError_t fp64_dmma_peak(int iters, double* tflops);
+
+}  // namespace sfx

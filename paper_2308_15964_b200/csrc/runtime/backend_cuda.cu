@@ -1,0 +1,307 @@
+// CUDA backend: one arena (single cudaMalloc slab) per device, K streams per
+// device, pooled events, async H2D/D2H copies and cudaMemcpyPeerAsync over
+// NVLink, and the op dispatch to the sm_100a kernels.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "../kernels/kernels.h"
+#include "runtime.h"
+
+namespace sfx {
+namespace {
+
+inline int cuda_err(cudaError_t e, const char* what, std::string& err) {
+  if (e == cudaSuccess) return SFX_OK;
+  err = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return SFX_ERR_CUDA;
+}
+
+struct Ev {
+  cudaEvent_t e = nullptr;
+  bool timing = false;
+};
+inline cudaEvent_t ev_of(void* p) { return static_cast<Ev*>(p)->e; }
+
+class CudaBackend : public Backend {
+  struct Dev {
+    int ordinal = 0;
+    std::vector<cudaStream_t> streams;
+    char* arena = nullptr;
+    uint64_t cap = 0;
+    std::mutex pool_mu;
+    std::vector<Ev*> pool_timing, pool_plain;
+    cudaEvent_t base = nullptr;
+    int64_t base_ns = 0;
+    int* info = nullptr;
+    bool ready = false;
+  };
+
+ public:
+  CudaBackend(int ndev, const int* ordinals) : devs_(ndev) {
+    for (int d = 0; d < ndev; ++d) {
+      devs_[d] = new Dev();
+      devs_[d]->ordinal = ordinals ? ordinals[d] : d;
+    }
+  }
+  ~CudaBackend() override {
+    shutdown();
+    for (Dev* d : devs_) delete d;
+  }
+  bool is_sim() const override { return false; }
+
+  int init_device(int d, int, int nstreams, uint64_t bytes, std::string& err) override {
+    Dev& D = *devs_[d];
+    cudaError_t e = cudaSetDevice(D.ordinal);
+    if (e) return cuda_err(e, "cudaSetDevice", err);
+    cudaSetDeviceFlags(cudaDeviceScheduleYield);  // fails harmlessly if a context exists
+    cudaGetLastError();
+    e = cudaFree(nullptr);
+    if (e) return cuda_err(e, "context init", err);
+    if (!bytes) {
+      size_t fr = 0, tot = 0;
+      e = cudaMemGetInfo(&fr, &tot);
+      if (e) return cuda_err(e, "cudaMemGetInfo", err);
+      const uint64_t reserve = 6ull << 30;
+      bytes = fr > 2 * reserve ? fr - reserve : fr / 2;
+    }
+    bytes = (bytes + 255) / 256 * 256;
+    e = cudaMalloc(&D.arena, bytes);
+    if (e) return cuda_err(e, "arena cudaMalloc", err);
+    D.cap = bytes;
+    e = cudaMalloc(&D.info, sizeof(int));
+    if (e) return cuda_err(e, "cudaMalloc info", err);
+    cudaMemset(D.info, 0, sizeof(int));
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    D.streams.resize(nstreams);
+    for (int s = 0; s < nstreams; ++s) {
+      e = cudaStreamCreateWithPriority(&D.streams[s], cudaStreamNonBlocking, least);
+      if (e) return cuda_err(e, "cudaStreamCreate", err);
+    }
+    // peer access to every device initialised before this one (both ways)
+    for (int o = 0; o < d; ++o) {
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, D.ordinal, devs_[o]->ordinal);
+      if (can) {
+        cudaDeviceEnablePeerAccess(devs_[o]->ordinal, 0);
+        cudaSetDevice(devs_[o]->ordinal);
+        cudaDeviceEnablePeerAccess(D.ordinal, 0);
+        cudaSetDevice(D.ordinal);
+      }
+      cudaGetLastError();
+    }
+    // timestamp calibration: host CLOCK_MONOTONIC of the base event
+    e = cudaEventCreate(&D.base);
+    if (e) return cuda_err(e, "cudaEventCreate", err);
+    cudaEventRecord(D.base, D.streams[0]);
+    cudaEventSynchronize(D.base);
+    int64_t best = INT64_MAX;
+    cudaEvent_t probe;
+    cudaEventCreate(&probe);
+    for (int k = 0; k < 5; ++k) {
+      cudaEventRecord(probe, D.streams[0]);
+      cudaEventSynchronize(probe);
+      const int64_t host = now_ns();
+      float ms = 0;
+      cudaEventElapsedTime(&ms, D.base, probe);
+      const int64_t b = host - static_cast<int64_t>(static_cast<double>(ms) * 1e6);
+      if (b < best) best = b;
+    }
+    cudaEventDestroy(probe);
+    D.base_ns = best;
+    D.ready = true;
+    return cuda_err(cudaGetLastError(), "device init", err);
+  }
+
+  void bind_thread(int d) override { cudaSetDevice(devs_[d]->ordinal); }
+  uint64_t arena_capacity(int d) override { return devs_[d]->cap; }
+  void* arena_ptr(int d, uint64_t off) override { return devs_[d]->arena + off; }
+
+  void* event_create(int d, bool timing) override {
+    Dev& D = *devs_[d];
+    {
+      std::lock_guard<std::mutex> g(D.pool_mu);
+      auto& pool = timing ? D.pool_timing : D.pool_plain;
+      if (!pool.empty()) {
+        Ev* e = pool.back();
+        pool.pop_back();
+        return e;
+      }
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != D.ordinal) cudaSetDevice(D.ordinal);
+    Ev* e = new Ev();
+    e->timing = timing;
+    cudaEventCreateWithFlags(&e->e, timing ? cudaEventDefault : cudaEventDisableTiming);
+    if (cur != D.ordinal) cudaSetDevice(cur);
+    return e;
+  }
+  void event_release(int d, void* ev) override {
+    Dev& D = *devs_[d];
+    std::lock_guard<std::mutex> g(D.pool_mu);
+    Ev* e = static_cast<Ev*>(ev);
+    if (shut_) {
+      cudaEventDestroy(e->e);
+      delete e;
+      return;
+    }
+    (e->timing ? D.pool_timing : D.pool_plain).push_back(e);
+  }
+  int event_record(int d, int stream, void* ev, std::string& err) override {
+    return cuda_err(cudaEventRecord(ev_of(ev), devs_[d]->streams[stream]), "cudaEventRecord", err);
+  }
+  int stream_wait(int d, int stream, void* ev, std::string& err) override {
+    return cuda_err(cudaStreamWaitEvent(devs_[d]->streams[stream], ev_of(ev), 0),
+                    "cudaStreamWaitEvent", err);
+  }
+  int event_sync(int, void* ev, std::string& err) override {
+    return cuda_err(cudaEventSynchronize(ev_of(ev)), "kernel execution", err);
+  }
+  int64_t event_time_ns(int d, void* ev) override {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, devs_[d]->base, ev_of(ev)) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    return devs_[d]->base_ns + static_cast<int64_t>(static_cast<double>(ms) * 1e6);
+  }
+  int copy_h2d(int d, int stream, uint64_t dst, const void* src, uint64_t n, std::string& err) override {
+    return cuda_err(cudaMemcpyAsync(devs_[d]->arena + dst, src, n, cudaMemcpyHostToDevice, devs_[d]->streams[stream]),
+                    "H2D copy", err);
+  }
+  int copy_d2h(int d, int stream, void* dst, uint64_t src, uint64_t n, std::string& err) override {
+    return cuda_err(cudaMemcpyAsync(dst, devs_[d]->arena + src, n, cudaMemcpyDeviceToHost, devs_[d]->streams[stream]),
+                    "D2H copy", err);
+  }
+  int copy_p2p(int d, int stream, uint64_t dst, int sd, uint64_t src, uint64_t n, std::string& err) override {
+    return cuda_err(cudaMemcpyPeerAsync(devs_[d]->arena + dst, devs_[d]->ordinal, devs_[sd]->arena + src,
+                                        devs_[sd]->ordinal, n, devs_[d]->streams[stream]),
+                    "peer copy", err);
+  }
+  bool supports(uint32_t op) const override {
+    switch (op) {
+      case SFX_OP_NOOP:
+      case SFX_OP_SPIN:
+      case SFX_OP_CELL:
+      case SFX_OP_BYTES_ADD:
+      case SFX_OP_FLUSH:
+      case SFX_OP_ZERO:
+      case SFX_OP_DGEMM:
+      case SFX_OP_DSYRK:
+      case SFX_OP_DTRSM:
+      case SFX_OP_DPOTRF:
+      case SFX_OP_P2P_PAIR:
+      case SFX_OP_P2P_SELF:
+      case SFX_OP_FILL_UNIFORM:
+      case SFX_OP_FILL_SPD:
+      case SFX_OP_FILL_PARTICLES:
+        return true;
+      default:
+        return false;
+    }
+  }
+
+  int launch(int d, int stream, const OpLaunch& op, std::string& err) override {
+    cudaStream_t s = devs_[d]->streams[stream];
+    const Operand* o = op.o;
+    auto f64 = [](const Operand& x) { return static_cast<double*>(x.dptr); };
+    cudaError_t e = cudaSuccess;
+    switch (op.op) {
+      case SFX_OP_SPIN:
+        e = launch_spin(op.ip[0], s);
+        break;
+      case SFX_OP_ZERO:
+        e = cudaMemsetAsync(o[0].dptr, 0, o[0].bytes, s);
+        break;
+      case SFX_OP_BYTES_ADD:
+        e = launch_bytes_add(static_cast<unsigned char*>(o[0].dptr), op.ip[0], op.ip[1], op.ip[2], s);
+        break;
+      case SFX_OP_CELL: {
+        const long long* reads[7];
+        for (int k = 1; k < op.n; ++k) reads[k - 1] = static_cast<const long long*>(o[k].dptr);
+        e = launch_cell(static_cast<long long*>(o[0].dptr), reads, op.n - 1, op.ip[0], op.ip[1], op.ip[2], s);
+        break;
+      }
+      case SFX_OP_FILL_UNIFORM:
+        e = launch_fill_uniform(f64(o[0]), o[0].rows, o[0].cols, o[0].ld, op.ip[0], op.ip[1], op.ip[2], op.ip[3], s);
+        break;
+      case SFX_OP_FILL_SPD:
+        e = launch_fill_spd(f64(o[0]), o[0].rows, o[0].cols, o[0].ld, op.ip[0], op.ip[1], op.ip[2], op.ip[3], s);
+        break;
+      case SFX_OP_FILL_PARTICLES:
+        e = launch_fill_particles(f64(o[0]), o[0].cols, o[0].ld, op.ip[0], op.ip[1], s);
+        break;
+      case SFX_OP_DGEMM: {
+        const bool tb = op.ip[0] != 0;
+        e = launch_dgemm(f64(o[0]), o[0].ld, f64(o[1]), o[1].ld, f64(o[2]), o[2].ld, static_cast<int>(o[2].rows),
+                         static_cast<int>(o[2].cols), static_cast<int>(o[0].cols), op.fp[0], op.fp[1], tb, false, s);
+        break;
+      }
+      case SFX_OP_DSYRK:
+        e = launch_dgemm(f64(o[0]), o[0].ld, f64(o[0]), o[0].ld, f64(o[1]), o[1].ld, static_cast<int>(o[1].rows),
+                         static_cast<int>(o[1].rows), static_cast<int>(o[0].cols), op.fp[0], op.fp[1], true, true, s);
+        break;
+      case SFX_OP_DTRSM:
+        e = launch_dtrsm(f64(o[0]), o[0].ld, f64(o[1]), o[1].ld, static_cast<int>(o[1].rows),
+                         static_cast<int>(o[1].cols), s);
+        break;
+      case SFX_OP_DPOTRF:
+        e = launch_dpotrf(f64(o[0]), o[0].ld, static_cast<int>(o[0].rows), devs_[d]->info, s);
+        break;
+      case SFX_OP_P2P_PAIR:
+        e = launch_p2p(f64(o[0]), o[0].ld, static_cast<int>(o[0].cols), f64(o[1]), o[1].ld, static_cast<int>(o[1].cols),
+                       f64(o[2]), o[2].ld, f64(o[3]), o[3].ld, false, op.fp[0], s);
+        break;
+      case SFX_OP_P2P_SELF:
+        e = launch_p2p(f64(o[0]), o[0].ld, static_cast<int>(o[0].cols), nullptr, 0, 0, f64(o[1]), o[1].ld, nullptr, 0,
+                       true, op.fp[0], s);
+        break;
+      default:
+        err = "unsupported op";
+        return SFX_ERR_UNSUPPORTED;
+    }
+    return cuda_err(e, "kernel launch", err);
+  }
+
+  void shutdown() override {
+    if (shut_) return;
+    for (Dev* dp : devs_) {
+      Dev& D = *dp;
+      if (!D.ready) continue;
+      cudaSetDevice(D.ordinal);
+      cudaDeviceSynchronize();
+      std::lock_guard<std::mutex> g(D.pool_mu);
+      for (Ev* e : D.pool_timing) {
+        cudaEventDestroy(e->e);
+        delete e;
+      }
+      for (Ev* e : D.pool_plain) {
+        cudaEventDestroy(e->e);
+        delete e;
+      }
+      D.pool_timing.clear();
+      D.pool_plain.clear();
+      if (D.base) cudaEventDestroy(D.base);
+      for (auto st : D.streams) cudaStreamDestroy(st);
+      D.streams.clear();
+      if (D.arena) cudaFree(D.arena);
+      if (D.info) cudaFree(D.info);
+      D.arena = nullptr;
+      D.ready = false;
+    }
+    shut_ = true;
+  }
+
+ private:
+  std::vector<Dev*> devs_;
+  bool shut_ = false;
+};
+
+}  // namespace
+
+Backend* make_cuda_backend(int ndev, const int* ordinals, bool) { return new CudaBackend(ndev, ordinals); }
+
+}  // namespace sfx

@@ -1,0 +1,1227 @@
+// Native STF runtime (see runtime.h for the reference mapping).
+#include "runtime.h"
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <ctime>
+
+namespace sfx {
+
+int64_t now_ns() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return static_cast<int64_t>(ts.tv_sec) * 1000000000LL + ts.tv_nsec;
+}
+
+Sync::~Sync() {
+  if (be && event) be->event_release(dev, event);
+}
+
+static bool heap_less(const Task* a, const Task* b) {
+  // max-heap on (priority, -seq): higher priority first, FIFO among equals
+  if (a->prio != b->prio) return a->prio < b->prio;
+  return a->seq > b->seq;
+}
+
+void DevQueue::push(Task* t) {
+  if (!prio) {
+    fifo.push_back(t);
+  } else {
+    heap.push_back(t);
+    std::push_heap(heap.begin(), heap.end(), heap_less);
+  }
+}
+
+Task* DevQueue::pop() {
+  if (!prio) {
+    if (fifo.empty()) return nullptr;
+    Task* t = fifo.front();
+    fifo.pop_front();
+    return t;
+  }
+  if (heap.empty()) return nullptr;
+  std::pop_heap(heap.begin(), heap.end(), heap_less);
+  Task* t = heap.back();
+  heap.pop_back();
+  return t;
+}
+
+static std::string fmt(const char* f, ...) __attribute__((format(printf, 1, 2)));
+static std::string fmt(const char* f, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, f);
+  vsnprintf(buf, sizeof buf, f, ap);
+  va_end(ap);
+  return buf;
+}
+
+Runtime::Runtime(Backend* be, int ndev, int nstreams, uint32_t sched, uint32_t flags, uint32_t window,
+                 uint64_t align)
+    : be_(be),
+      ndev_(ndev),
+      nstreams_(nstreams),
+      sched_(sched),
+      flags_(flags),
+      window_(window ? window : 4u * static_cast<uint32_t>(nstreams)),
+      align_(align),
+      trace_((flags & SFX_FLAG_TRACE) != 0) {
+  paused_ = (flags & SFX_FLAG_PAUSED) != 0;
+}
+
+int Runtime::init(const uint64_t* arena_bytes, std::string& err) {
+  for (int d = 0; d < ndev_; ++d) {
+    auto dev = std::make_unique<Device>();
+    dev->index = d;
+    dev->queue.prio = sched_ == SFX_SCHED_PRIO;
+    dev->stream_inflight.assign(nstreams_, 0);
+    int rc = be_->init_device(d, d, nstreams_, arena_bytes ? arena_bytes[d] : 0, err);
+    if (rc) return rc;
+    dev->capacity = be_->arena_capacity(d);
+    dev->free_bytes = dev->capacity;
+    dev->free_list[0] = dev->capacity;
+    dev->stats.capacity = dev->capacity;
+    devs_.push_back(std::move(dev));
+  }
+  for (int d = 0; d < ndev_; ++d) {
+    devs_[d]->exec_thread = std::thread(&Runtime::exec_loop, this, d);
+    if (!be_->is_sim()) devs_[d]->comp_thread = std::thread(&Runtime::comp_loop, this, d);
+  }
+  started_ = true;
+  return SFX_OK;
+}
+
+Runtime::~Runtime() {
+  {
+    std::unique_lock<std::mutex> lk(mu_);
+    stopping_ = true;
+    for (auto& d : devs_) {
+      d->exec_cv.notify_all();
+      d->comp_cv.notify_all();
+    }
+    done_cv_.notify_all();
+  }
+  for (auto& d : devs_) {
+    if (d->exec_thread.joinable()) d->exec_thread.join();
+    if (d->comp_thread.joinable()) d->comp_thread.join();
+  }
+  // drop every sync/event reference before the backend goes away
+  for (auto& t : task_store_) {
+    t.waits.clear();
+    t.start.reset();
+    t.end.reset();
+    t.copy_syncs.clear();
+  }
+  for (auto& h : handle_store_) {
+    h->host_ready.reset();
+    h->commute_last.reset();
+    for (Block* b : h->blocks) {
+      if (b) {
+        b->ready.reset();
+        delete b;
+      }
+    }
+    h->blocks.clear();
+  }
+  be_->shutdown();
+  delete be_;
+}
+
+// ---------------------------------------------------------------- graphs
+
+int Runtime::graph_create(uint32_t* gid) {
+  std::unique_lock<std::mutex> lk(mu_);
+  auto g = std::make_unique<Graph>();
+  g->gid = next_gid_++;
+  *gid = g->gid;
+  graphs_[g->gid] = std::move(g);
+  return SFX_OK;
+}
+
+int Runtime::reg(uint32_t gid, uint64_t hid, void* host, uint64_t bytes, int64_t rows, int64_t cols, int64_t ld,
+                 int32_t dtype) {
+  std::unique_lock<std::mutex> lk(mu_);
+  auto git = graphs_.find(gid);
+  if (git == graphs_.end()) {
+    last_error = fmt("unknown graph %u", gid);
+    return SFX_ERR_CONFIG;
+  }
+  if (handles_.count(hid)) {
+    last_error = fmt("handle %llu is already registered", (unsigned long long)hid);
+    return SFX_ERR_REGISTRATION;
+  }
+  auto h = std::make_unique<Handle>();
+  h->hid = hid;
+  h->gid = gid;
+  h->host = host;
+  h->bytes = bytes;
+  h->rows = rows;
+  h->cols = cols;
+  h->ld = ld;
+  h->dtype = dtype;
+  h->blocks.assign(ndev_, nullptr);
+  handles_[hid] = h.get();
+  git->second->handles.push_back(h.get());
+  handle_store_.push_back(std::move(h));
+  return SFX_OK;
+}
+
+int Runtime::set_home(uint64_t hid, int dev) {
+  std::unique_lock<std::mutex> lk(mu_);
+  auto it = handles_.find(hid);
+  if (it == handles_.end()) {
+    last_error = "set_home: unknown handle";
+    return SFX_ERR_REGISTRATION;
+  }
+  it->second->home = (dev >= 0 && ndev_ > 0) ? dev % ndev_ : -1;
+  return SFX_OK;
+}
+
+int Runtime::unreg(uint64_t hid) {
+  std::unique_lock<std::mutex> lk(mu_);
+  auto it = handles_.find(hid);
+  if (it == handles_.end()) {
+    last_error = "object is not registered";
+    return SFX_ERR_REGISTRATION;
+  }
+  Handle* h = it->second;
+  if (h->active < h->slots.size()) {
+    // handles.py:179-182
+    last_error = "cannot unregister an object with pending accesses";
+    return SFX_ERR_REGISTRATION;
+  }
+  for (int d = 0; d < ndev_; ++d) {
+    Block* b = h->blocks[d];
+    if (!b) continue;
+    if (b->pins > 0) {
+      last_error = "cannot unregister an object still in use on a device";
+      return SFX_ERR_REGISTRATION;
+    }
+    if (b->dirty) {
+      // synchronous write-back: the host object is the only copy left afterwards
+      std::string err;
+      be_->bind_thread(d);
+      if (b->ready && !b->ready->complete) be_->event_sync(d, b->ready->event, err);
+      void* ev = be_->event_create(d, false);
+      int rc = be_->copy_d2h(d, 0, h->host, b->off, h->bytes, err);
+      if (!rc) rc = be_->event_record(d, 0, ev, err);
+      if (!rc) rc = be_->event_sync(d, ev, err);
+      be_->event_release(d, ev);
+      if (rc) {
+        last_error = err;
+        return SFX_ERR_CUDA;
+      }
+      devs_[d]->stats.bytes_from_device += h->bytes;
+      devs_[d]->stats.copies_from_device += 1;
+      h->host_valid = true;
+      h->dirty_dev = -1;
+    }
+    drop_block(b, false, nullptr, 0);
+  }
+  handles_.erase(it);
+  return SFX_OK;
+}
+
+// ------------------------------------------------------------- insertion
+
+static int expect_f64(const Handle* h, const char* what, std::string& err) {
+  if (h->dtype != SFX_DTYPE_F64 || h->rows <= 0 || h->cols <= 0 || h->ld < h->cols ||
+      h->bytes < static_cast<uint64_t>((h->rows - 1) * h->ld + h->cols) * 8) {
+    err = fmt("%s must be a 2-D float64 tile (got dtype %d, %lldx%lld ld %lld)", what, h->dtype,
+              (long long)h->rows, (long long)h->cols, (long long)h->ld);
+    return SFX_ERR_CONFIG;
+  }
+  return 0;
+}
+
+int Runtime::validate(const sfx_task_desc& d, const sfx_access* acc, std::string& err) {
+  if (!graphs_.count(d.graph)) {
+    err = fmt("unknown graph %u", d.graph);
+    return SFX_ERR_CONFIG;
+  }
+  if (!be_->supports(d.op)) {
+    err = fmt("op %u needs a CUDA device: the simulated backend only runs the runtime's test ops", d.op);
+    return SFX_ERR_UNSUPPORTED;
+  }
+  std::vector<Handle*> hs(d.n_access);
+  for (uint32_t k = 0; k < d.n_access; ++k) {
+    auto it = handles_.find(acc[k].hid);
+    if (it == handles_.end()) {
+      err = fmt("access %u names unregistered handle %llu", k, (unsigned long long)acc[k].hid);
+      return SFX_ERR_REGISTRATION;
+    }
+    if (acc[k].mode > SFX_MAYBE_WRITE) {
+      err = fmt("bad access mode %u", acc[k].mode);
+      return SFX_ERR_CONFIG;
+    }
+    hs[k] = it->second;
+    for (uint32_t j = 0; j < k; ++j)
+      if (hs[j] == hs[k]) {
+        err = "task declares the same object twice";  // graph.py:134-137
+        return SFX_ERR_DUPLICATE;
+      }
+  }
+  auto need = [&](uint32_t n) {
+    if (d.n_access != n) {
+      err = fmt("op %u takes %u accesses, got %u", d.op, n, d.n_access);
+      return false;
+    }
+    return true;
+  };
+  auto writes = [&](uint32_t k) {
+    if (!mode_writes(acc[k].mode)) {
+      err = fmt("op %u writes operand %u but it is declared read-only", d.op, k);
+      return false;
+    }
+    return true;
+  };
+  int rc;
+  switch (d.op) {
+    case SFX_OP_NOOP:
+    case SFX_OP_SPIN:
+      return 0;
+    case SFX_OP_CELL:
+      if (d.n_access < 1 || d.n_access > 8) {
+        err = "cell op takes a target plus up to 7 read cells";
+        return SFX_ERR_CONFIG;
+      }
+      for (uint32_t k = 0; k < d.n_access; ++k)
+        if (hs[k]->bytes < 8) {
+          err = "cell op operands must be 8-byte int64 cells";
+          return SFX_ERR_CONFIG;
+        }
+      return 0;
+    case SFX_OP_BYTES_ADD:
+      if (!need(1) || !writes(0)) return SFX_ERR_CONFIG;
+      if (d.iparam[0] < 0 || d.iparam[1] < 0 || static_cast<uint64_t>(d.iparam[0] + d.iparam[1]) > hs[0]->bytes) {
+        err = "bytes_add range outside the buffer";
+        return SFX_ERR_CONFIG;
+      }
+      return 0;
+    case SFX_OP_ZERO:
+      if (!need(1) || !writes(0)) return SFX_ERR_CONFIG;
+      return 0;
+    case SFX_OP_FILL_UNIFORM:
+    case SFX_OP_FILL_SPD:
+    case SFX_OP_FILL_PARTICLES:
+      if (!need(1) || !writes(0)) return SFX_ERR_CONFIG;
+      return expect_f64(hs[0], "fill target", err);
+    case SFX_OP_DGEMM: {
+      if (!need(3) || !writes(2)) return SFX_ERR_CONFIG;
+      if ((rc = expect_f64(hs[0], "A", err)) || (rc = expect_f64(hs[1], "B", err)) || (rc = expect_f64(hs[2], "C", err)))
+        return rc;
+      const bool tb = d.iparam[0] != 0;
+      const int64_t M = hs[0]->rows, K = hs[0]->cols;
+      const int64_t bk = tb ? hs[1]->cols : hs[1]->rows, N = tb ? hs[1]->rows : hs[1]->cols;
+      if (bk != K || hs[2]->rows != M || hs[2]->cols != N) {
+        err = fmt("dgemm shapes do not conform: A %lldx%lld, B %lldx%lld%s, C %lldx%lld", (long long)M, (long long)K,
+                  (long long)hs[1]->rows, (long long)hs[1]->cols, tb ? "^T" : "", (long long)hs[2]->rows,
+                  (long long)hs[2]->cols);
+        return SFX_ERR_CONFIG;
+      }
+      return 0;
+    }
+    case SFX_OP_DSYRK:
+      if (!need(2) || !writes(1)) return SFX_ERR_CONFIG;
+      if ((rc = expect_f64(hs[0], "A", err)) || (rc = expect_f64(hs[1], "C", err))) return rc;
+      if (hs[1]->rows != hs[1]->cols || hs[1]->rows != hs[0]->rows) {
+        err = "dsyrk: C must be square with A's row count";
+        return SFX_ERR_CONFIG;
+      }
+      return 0;
+    case SFX_OP_DTRSM:
+      if (!need(2) || !writes(1)) return SFX_ERR_CONFIG;
+      if ((rc = expect_f64(hs[0], "L", err)) || (rc = expect_f64(hs[1], "B", err))) return rc;
+      if (hs[0]->rows != hs[0]->cols || hs[1]->cols != hs[0]->rows) {
+        err = "dtrsm: L must be square with B's column count";
+        return SFX_ERR_CONFIG;
+      }
+      return 0;
+    case SFX_OP_DPOTRF:
+      if (!need(1) || !writes(0)) return SFX_ERR_CONFIG;
+      if ((rc = expect_f64(hs[0], "A", err))) return rc;
+      if (hs[0]->rows != hs[0]->cols) {
+        err = "dpotrf: A must be square";
+        return SFX_ERR_CONFIG;
+      }
+      return 0;
+    case SFX_OP_P2P_PAIR:
+      if (!need(4) || !writes(2) || !writes(3)) return SFX_ERR_CONFIG;
+      for (int k = 0; k < 4; ++k)
+        if ((rc = expect_f64(hs[k], "particle block", err))) return rc;
+      if (hs[0]->rows != 4 || hs[1]->rows != 4 || hs[2]->rows != 4 || hs[3]->rows != 4 || hs[0]->cols != hs[2]->cols ||
+          hs[1]->cols != hs[3]->cols) {
+        err = "p2p: positions/accumulators are 4 x n SoA blocks (x,y,z,q / fx,fy,fz,pot)";
+        return SFX_ERR_CONFIG;
+      }
+      return 0;
+    case SFX_OP_P2P_SELF:
+      if (!need(2) || !writes(1)) return SFX_ERR_CONFIG;
+      for (int k = 0; k < 2; ++k)
+        if ((rc = expect_f64(hs[k], "particle block", err))) return rc;
+      if (hs[0]->rows != 4 || hs[1]->rows != 4 || hs[0]->cols != hs[1]->cols) {
+        err = "p2p: positions/accumulators are 4 x n SoA blocks";
+        return SFX_ERR_CONFIG;
+      }
+      return 0;
+    case SFX_OP_FLUSH:
+      if (!need(1)) return SFX_ERR_CONFIG;
+      return 0;
+    default:
+      err = fmt("unknown op %u", d.op);
+      return SFX_ERR_CONFIG;
+  }
+}
+
+void Runtime::bind(Task* t, Handle* h, uint32_t mode) {
+  // handles.py:209-236: join the last slot only if the category groups, matches,
+  // and the slot has not been passed yet; otherwise open a new slot.
+  const Cat cat = category_of(mode);
+  const bool grouping = cat != CAT_X;
+  auto& slots = h->slots;
+  uint32_t idx;
+  if (grouping && !slots.empty() && slots.back().cat == cat && h->active + 1 <= slots.size()) {
+    idx = static_cast<uint32_t>(slots.size() - 1);
+  } else {
+    slots.push_back(Slot{cat, {}, 0});
+    idx = static_cast<uint32_t>(slots.size() - 1);
+  }
+  slots[idx].tasks.push_back(t);
+  t->acc.push_back(Access{h, mode, idx});
+  if (idx != h->active) {
+    t->pending += 1;
+  } else if (idx > 0) {
+    // The slot is already active: the previous slot's members were released at
+    // launch and may still be running on a device -- wait on their end events.
+    for (Task* p : slots[idx - 1].tasks)
+      if (p->end && !p->end->complete) t->waits.push_back(p->end);
+  }
+}
+
+int Runtime::submit(uint32_t n, const sfx_task_desc* descs, const sfx_access* acc) {
+  std::unique_lock<std::mutex> lk(mu_);
+  size_t ai = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    const sfx_task_desc& d = descs[i];
+    std::string err;
+    int rc = validate(d, acc + ai, err);
+    if (rc) {
+      last_error = err;
+      return rc;
+    }
+    if (tasks_by_tid_.count(d.tid)) {
+      last_error = fmt("task id %llu reused", (unsigned long long)d.tid);
+      return SFX_ERR_INTERNAL;
+    }
+    task_store_.emplace_back();
+    Task* t = &task_store_.back();
+    t->tid = d.tid;
+    t->gid = d.graph;
+    t->op = d.op;
+    t->prio = d.priority;
+    t->hint = d.device;
+    for (int k = 0; k < 4; ++k) {
+      t->fp[k] = d.fparam[k];
+      t->ip[k] = d.iparam[k];
+    }
+    t->acc.reserve(d.n_access);
+    for (uint32_t k = 0; k < d.n_access; ++k) bind(t, handles_[acc[ai + k].hid], acc[ai + k].mode);
+    ai += d.n_access;
+    Graph* g = graphs_[d.graph].get();
+    g->tasks.push_back(t);
+    g->inserted += 1;
+    tasks_by_tid_[t->tid] = t;
+    if (--t->pending == 0) {  // drop the insertion guard (graph.py:161-163)
+      t->state = SFX_STATE_READY;
+      push_ready(t, -1);
+    }
+  }
+  return SFX_OK;
+}
+
+int Runtime::flush(uint32_t gid, uint64_t tid, uint64_t hid, int write_mode) {
+  sfx_task_desc d;
+  memset(&d, 0, sizeof d);
+  d.tid = tid;
+  d.graph = gid;
+  d.op = SFX_OP_FLUSH;
+  d.device = -1;
+  d.n_access = 1;
+  d.iparam[0] = write_mode;
+  sfx_access a;
+  a.hid = hid;
+  a.mode = write_mode ? SFX_WRITE : SFX_READ;
+  a.reserved = 0;
+  return submit(1, &d, &a);
+}
+
+// ------------------------------------------------------------ scheduling
+
+int Runtime::place(Task* t) {
+  if (ndev_ == 1) return 0;
+  if (t->hint >= 0) return t->hint % ndev_;
+  if (t->op == SFX_OP_FLUSH) {
+    Handle* h = t->acc[0].h;
+    if (h->dirty_dev >= 0) return h->dirty_dev;
+    for (int e = 0; e < ndev_; ++e)
+      if (h->blocks[e] && h->blocks[e]->valid) return e;
+    return 0;
+  }
+  // concurrent atomic/commutative members share the device of their group
+  for (auto& a : t->acc)
+    if ((a.mode == SFX_ATOMIC_WRITE || a.mode == SFX_COMMUTATIVE_WRITE) && a.h->group_dev >= 0) return a.h->group_dev;
+  int chosen = -1;
+  // owner computes: the device holding the freshest copy of a written tile
+  for (auto& a : t->acc)
+    if (mode_writes(a.mode) && a.h->dirty_dev >= 0) {
+      chosen = a.h->dirty_dev;
+      break;
+    }
+  if (chosen < 0)
+    for (auto& a : t->acc)
+      if (mode_writes(a.mode) && a.h->home >= 0) {
+        chosen = a.h->home;
+        break;
+      }
+  if (chosen < 0) {
+    // most operand bytes already valid on the device; ties -> least loaded
+    uint64_t best_bytes = 0;
+    size_t best_load = SIZE_MAX;
+    for (int e = 0; e < ndev_; ++e) {
+      uint64_t bytes = 0;
+      for (auto& a : t->acc)
+        if (a.h->blocks[e] && a.h->blocks[e]->valid) bytes += a.h->bytes;
+      size_t load = devs_[e]->queue.size() + devs_[e]->ninflight;
+      if (chosen < 0 || bytes > best_bytes || (bytes == best_bytes && load < best_load)) {
+        chosen = e;
+        best_bytes = bytes;
+        best_load = load;
+      }
+    }
+  }
+  for (auto& a : t->acc)
+    if (a.mode == SFX_ATOMIC_WRITE || a.mode == SFX_COMMUTATIVE_WRITE) a.h->group_dev = chosen;
+  return chosen;
+}
+
+void Runtime::record(Graph* g, int kind, int64_t t, int wid, uint64_t tid, int64_t extra) {
+  if (!trace_ || !g) return;
+  sfx_event e;
+  e.t_ns = t;
+  e.tid = tid;
+  e.kind = kind;
+  e.worker = wid;
+  e.extra = extra;
+  g->events.push_back(e);
+}
+
+void Runtime::push_ready(Task* t, int wid) {
+  // engine.py:212-223: record Push before the task becomes poppable
+  const int d = place(t);
+  t->dev = d;
+  t->seq = push_seq_++;
+  t->t_push = now_ns();
+  record(graphs_[t->gid].get(), SFX_EV_PUSH, t->t_push, wid, t->tid);
+  devs_[d]->queue.push(t);
+  devs_[d]->exec_cv.notify_one();
+}
+
+void Runtime::advance(Handle* h) {
+  // handles.py:331-343; members of the next slot inherit the finished slot's
+  // end events as stream waits
+  const uint32_t prev = h->active;
+  h->active += 1;
+  h->group_dev = -1;
+  if (h->active >= h->slots.size()) return;
+  Slot& nx = h->slots[h->active];
+  const Slot& pv = h->slots[prev];
+  for (Task* m : nx.tasks) {
+    for (Task* p : pv.tasks)
+      if (p->end && !p->end->complete) m->waits.push_back(p->end);
+    if (--m->pending == 0) {
+      m->state = SFX_STATE_READY;
+      push_ready(m, -1);
+    }
+  }
+}
+
+void Runtime::release(Task* t) {
+  // handles.py:274-312 (no commutative re-offer: members are chained on events)
+  if (t->released) {
+    poison(SFX_ERR_INTERNAL, fmt("double release of task %llu", (unsigned long long)t->tid));
+    return;
+  }
+  t->released = true;
+  for (auto& a : t->acc) {
+    Handle* h = a.h;
+    Slot& s = h->slots[a.slot];
+    s.done += 1;
+    if (a.slot == h->active && s.done >= s.tasks.size()) advance(h);
+  }
+}
+
+// --------------------------------------------------------------- arenas
+
+bool Runtime::alloc_space(int d, uint64_t size, uint64_t* off) {
+  Device& D = *devs_[d];
+  for (auto it = D.free_list.begin(); it != D.free_list.end(); ++it) {
+    if (it->second >= size) {
+      *off = it->first;
+      const uint64_t rest = it->second - size;
+      const uint64_t noff = it->first + size;
+      D.free_list.erase(it);
+      if (rest) D.free_list[noff] = rest;
+      D.free_bytes -= size;
+      D.stats.bytes_in_use += size;
+      return true;
+    }
+  }
+  return false;
+}
+
+void Runtime::free_space(int d, uint64_t off, uint64_t size) {
+  Device& D = *devs_[d];
+  auto it = D.free_list.emplace(off, size).first;
+  if (it != D.free_list.begin()) {
+    auto pv = std::prev(it);
+    if (pv->first + pv->second == it->first) {
+      pv->second += it->second;
+      D.free_list.erase(it);
+      it = pv;
+    }
+  }
+  auto nx = std::next(it);
+  if (nx != D.free_list.end() && it->first + it->second == nx->first) {
+    it->second += nx->second;
+    D.free_list.erase(nx);
+  }
+  D.free_bytes += size;
+  D.stats.bytes_in_use -= size;
+}
+
+SyncP Runtime::new_sync(int d, int s, bool timing) {
+  auto p = std::make_shared<Sync>();
+  p->be = be_;
+  p->dev = d;
+  p->stream = s;
+  p->timing = timing;
+  p->event = be_->event_create(d, timing);
+  return p;
+}
+
+void Runtime::drop_block(Block* b, bool write_back, std::vector<Action>* acts, int s) {
+  // device.py:226-232 (+ the write-back leg of evict_victims)
+  Handle* h = b->h;
+  Device& D = *devs_[b->dev];
+  if (b->dirty && write_back && acts) {
+    if (b->ready && !b->ready->complete) acts->push_back(Action{Action::WAIT, b->ready});
+    Action cp{Action::D2H, nullptr};
+    cp.host = h->host;
+    cp.src_off = b->off;
+    cp.n = h->bytes;
+    acts->push_back(cp);
+    SyncP hs = new_sync(b->dev, s, false);
+    acts->push_back(Action{Action::RECORD, hs});
+    h->host_ready = hs;
+    h->host_valid = true;
+    D.stats.bytes_from_device += h->bytes;
+    D.stats.copies_from_device += 1;
+    D.stats.writebacks += 1;
+  }
+  if (h->dirty_dev == b->dev) h->dirty_dev = -1;
+  b->valid = false;
+  b->dirty = false;
+  h->blocks[b->dev] = nullptr;
+  D.blocks.erase(h->hid);
+  D.stats.blocks -= 1;
+  if (b->pins > 0) {
+    b->zombie = true;  // freed when its last in-flight user completes
+  } else {
+    free_space(b->dev, b->off, b->size);
+    b->ready.reset();
+    delete b;
+  }
+}
+
+int Runtime::evict_one(int d, int s, std::vector<Action>& acts, std::string& err) {
+  // device.py:208-224: victim = least (stamp, hid) among unpinned blocks
+  Device& D = *devs_[d];
+  Block* victim = nullptr;
+  for (auto& kv : D.blocks) {
+    Block* b = kv.second;
+    if (b->pins) continue;
+    if (!victim || b->stamp < victim->stamp || (b->stamp == victim->stamp && b->h->hid < victim->h->hid)) victim = b;
+  }
+  if (!victim) return 1;
+  D.stats.evictions += 1;
+  drop_block(victim, true, &acts, s);
+  return 0;
+}
+
+int Runtime::ensure_block(int d, int s, Handle* h, std::vector<Action>& acts, std::vector<Block*>& tmp_pins,
+                          Block** out, std::string& err) {
+  // device.py:234-264
+  Device& D = *devs_[d];
+  const uint64_t size = std::max<uint64_t>((h->bytes + align_ - 1) / align_ * align_, align_);
+  if (size > D.capacity) {
+    err = fmt("device %d: object of %llu bytes exceeds the %llu-byte arena", d, (unsigned long long)h->bytes,
+              (unsigned long long)D.capacity);
+    return SFX_ERR_STAGING;
+  }
+  Block* b = h->blocks[d];
+  if (!b) {
+    auto pinned_by_others = [&]() {
+      size_t mine = 0, all = 0;
+      for (auto& kv : D.blocks) all += kv.second->pins;
+      for (Block* p : tmp_pins)
+        if (p->dev == d) mine += 1;
+      return all > mine || D.ninflight > 0;
+    };
+    while (D.free_bytes < size) {
+      if (evict_one(d, s, acts, err)) {
+        if (pinned_by_others()) return 1;
+        err = fmt("device %d: need %llu bytes but every block is pinned by a running task", d,
+                  (unsigned long long)size);
+        return SFX_ERR_STAGING;
+      }
+    }
+    uint64_t off;
+    while (!alloc_space(d, size, &off)) {
+      if (evict_one(d, s, acts, err)) {
+        if (pinned_by_others()) return 1;
+        err = fmt("device %d: fragmentation and pinned blocks prevent a %llu-byte allocation", d,
+                  (unsigned long long)size);
+        return SFX_ERR_STAGING;
+      }
+    }
+    b = new Block();
+    b->h = h;
+    b->dev = d;
+    b->off = off;
+    b->size = size;
+    h->blocks[d] = b;
+    D.blocks[h->hid] = b;
+    D.stats.blocks += 1;
+  }
+  b->pins += 1;
+  tmp_pins.push_back(b);
+  *out = b;
+  return 0;
+}
+
+// ------------------------------------------------------------- execution
+
+int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op, std::string& err) {
+  Device& D = *devs_[d];
+  auto wait_on = [&](const SyncP& p) {
+    if (!p || p->complete) return;
+    if (p->dev == d && p->stream == s) return;  // same stream: ordered
+    acts.push_back(Action{Action::WAIT, p});
+  };
+  // pass 1: blocks for every operand (may evict; victims are written back)
+  std::vector<Block*> pins;
+  std::vector<Block*> blocks(t->acc.size(), nullptr);
+  if (t->op != SFX_OP_FLUSH) {
+    for (size_t k = 0; k < t->acc.size(); ++k) {
+      int rc = ensure_block(d, s, t->acc[k].h, acts, pins, &blocks[k], err);
+      if (rc) {
+        for (Block* b : pins) {
+          if (--b->pins == 0 && b->zombie) {
+            free_space(b->dev, b->off, b->size);
+            delete b;
+          }
+        }
+        return rc;
+      }
+    }
+  }
+  if (!t->end) {
+    t->end = new_sync(d, s, trace_);
+    if (trace_) t->start = new_sync(d, s, true);
+  }
+  for (const SyncP& w : t->waits) wait_on(w);
+  for (auto& a : t->acc)
+    if (a.mode == SFX_COMMUTATIVE_WRITE) wait_on(a.h->commute_last);
+  if (t->start) acts.push_back(Action{Action::RECORD, t->start});
+
+  if (t->op == SFX_OP_FLUSH) {
+    // graph.py:258-260 + device.py:318-326: fetch the dirty copy home; a
+    // write-mode flush then drops every device copy
+    Handle* h = t->acc[0].h;
+    if (h->dirty_dev >= 0) {
+      Block* b = h->blocks[h->dirty_dev];
+      if (h->dirty_dev != d) {
+        err = "flush placed away from the dirty copy";
+        return SFX_ERR_INTERNAL;
+      }
+      wait_on(b->ready);
+      Action cp{Action::D2H, nullptr};
+      cp.host = h->host;
+      cp.src_off = b->off;
+      cp.n = h->bytes;
+      acts.push_back(cp);
+      b->dirty = false;
+      b->pins += 1;
+      t->pinned.push_back(b);
+      h->dirty_dev = -1;
+      h->host_valid = true;
+      h->host_ready = t->end;
+      D.stats.bytes_from_device += h->bytes;
+      D.stats.copies_from_device += 1;
+    }
+    if (t->ip[0]) {
+      for (int e = 0; e < ndev_; ++e)
+        if (h->blocks[e]) drop_block(h->blocks[e], false, nullptr, s);
+    }
+    op.op = SFX_OP_FLUSH;
+    op.n = 0;
+    return 0;
+  }
+
+  // pass 2: make every operand valid on d (device.py:340-369)
+  for (size_t k = 0; k < t->acc.size(); ++k) {
+    Handle* h = t->acc[k].h;
+    Block* b = blocks[k];
+    if (b->valid) {
+      D.stats.hits += 1;
+      wait_on(b->ready);
+    } else {
+      D.stats.misses += 1;
+      int src = -1;
+      if (h->dirty_dev >= 0 && h->dirty_dev != d) {
+        src = h->dirty_dev;
+      } else {
+        for (int e = 0; e < ndev_; ++e)
+          if (e != d && h->blocks[e] && h->blocks[e]->valid) {
+            src = e;
+            break;
+          }
+      }
+      if (src >= 0) {
+        Block* sb = h->blocks[src];
+        wait_on(sb->ready);
+        Action cp{Action::P2P, nullptr};
+        cp.src_dev = src;
+        cp.src_off = sb->off;
+        cp.dst_off = b->off;
+        cp.n = h->bytes;
+        acts.push_back(cp);
+        sb->pins += 1;
+        t->pinned.push_back(sb);
+        D.stats.bytes_p2p_in += h->bytes;
+        D.stats.copies_p2p_in += 1;
+      } else {
+        if (!h->host_valid) {
+          err = fmt("handle %llu has no valid copy anywhere", (unsigned long long)h->hid);
+          return SFX_ERR_INTERNAL;
+        }
+        wait_on(h->host_ready);
+        Action cp{Action::H2D, nullptr};
+        cp.host = h->host;
+        cp.dst_off = b->off;
+        cp.n = h->bytes;
+        acts.push_back(cp);
+        D.stats.bytes_to_device += h->bytes;
+        D.stats.copies_to_device += 1;
+      }
+      SyncP cs = new_sync(d, s, false);
+      acts.push_back(Action{Action::RECORD, cs});
+      t->copy_syncs.push_back(cs);
+      b->valid = true;
+      b->ready = cs;
+    }
+    b->stamp = ++D.clock;
+    t->pinned.push_back(b);  // the pass-1 pin is released at completion
+  }
+
+  // pass 3: coherency of written operands
+  for (size_t k = 0; k < t->acc.size(); ++k) {
+    const uint32_t m = t->acc[k].mode;
+    if (!mode_writes(m)) continue;
+    Handle* h = t->acc[k].h;
+    Block* b = blocks[k];
+    for (int e = 0; e < ndev_; ++e)
+      if (e != d && h->blocks[e]) drop_block(h->blocks[e], false, nullptr, s);  // device.py:298-314
+    b->dirty = true;
+    h->dirty_dev = d;
+    h->host_valid = false;
+    if (m == SFX_COMMUTATIVE_WRITE) h->commute_last = t->end;
+    if (m == SFX_WRITE || m == SFX_MAYBE_WRITE) b->ready = t->end;
+  }
+
+  op.op = t->op;
+  op.n = static_cast<int>(std::min<size_t>(t->acc.size(), 8));
+  for (int k = 0; k < op.n; ++k) {
+    Handle* h = t->acc[k].h;
+    op.o[k].dptr = be_->arena_ptr(d, blocks[k]->off);
+    op.o[k].bytes = h->bytes;
+    op.o[k].rows = h->rows;
+    op.o[k].cols = h->cols;
+    op.o[k].ld = h->ld;
+    op.o[k].dtype = h->dtype;
+  }
+  for (int k = 0; k < 4; ++k) {
+    op.fp[k] = t->fp[k];
+    op.ip[k] = t->ip[k];
+  }
+  return 0;
+}
+
+int Runtime::issue(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op, std::string& err) {
+  int rc = 0;
+  for (Action& a : acts) {
+    switch (a.kind) {
+      case Action::WAIT: {
+        while (!a.sync->recorded.load(std::memory_order_acquire)) std::this_thread::yield();
+        if (a.sync->dev == d && a.sync->stream == s) break;
+        rc = be_->stream_wait(d, s, a.sync->event, err);
+        devs_[d]->stats.stream_waits += 1;
+        break;
+      }
+      case Action::H2D:
+        rc = be_->copy_h2d(d, s, a.dst_off, a.host, a.n, err);
+        break;
+      case Action::D2H:
+        rc = be_->copy_d2h(d, s, a.host, a.src_off, a.n, err);
+        break;
+      case Action::P2P:
+        rc = be_->copy_p2p(d, s, a.dst_off, a.src_dev, a.src_off, a.n, err);
+        break;
+      case Action::RECORD:
+        rc = be_->event_record(d, s, a.sync->event, err);
+        a.sync->recorded.store(true, std::memory_order_release);
+        break;
+    }
+    if (rc) return rc;
+  }
+  if (!t) return 0;
+  if (op.op != SFX_OP_FLUSH && op.op != SFX_OP_NOOP) {
+    rc = be_->launch(d, s, op, err);
+    if (rc) return rc;
+    devs_[d]->stats.kernel_launches += 1;
+  }
+  rc = be_->event_record(d, s, t->end->event, err);
+  t->end->recorded.store(true, std::memory_order_release);
+  return rc;
+}
+
+void Runtime::complete(Task* t) {
+  Device& D = *devs_[t->dev];
+  if (t->end) t->end->complete = true;
+  if (t->start) t->start->complete = true;
+  for (auto& c : t->copy_syncs) c->complete = true;
+  for (Block* b : t->pinned) {
+    if (--b->pins == 0 && b->zombie) {
+      free_space(b->dev, b->off, b->size);
+      b->ready.reset();
+      delete b;
+    }
+  }
+  t->pinned.clear();
+  t->copy_syncs.clear();
+  t->waits.clear();
+  Graph* g = graphs_[t->gid].get();
+  if (trace_ && t->start && t->end) {
+    t->t_start = be_->event_time_ns(t->dev, t->start->event);
+    t->t_end = be_->event_time_ns(t->dev, t->end->event);
+    const int wid = t->dev * nstreams_ + t->stream;
+    record(g, SFX_EV_START, t->t_start, wid, t->tid);
+    record(g, SFX_EV_END, t->t_end, wid, t->tid);
+  }
+  t->start.reset();
+  t->end.reset();
+  t->state = SFX_STATE_FINISHED;
+  g->completed += 1;
+  D.ninflight -= 1;
+  D.stream_inflight[t->stream] -= 1;
+  D.stats.tasks_executed += 1;
+  D.exec_cv.notify_one();
+  done_cv_.notify_all();
+}
+
+void Runtime::poison(int code, const std::string& msg) {
+  // engine.py:227-243: first failure wins; everyone waiting learns of it
+  if (!fail_code_) {
+    fail_code_ = code;
+    fail_msg_ = msg;
+  }
+  for (auto& d : devs_) {
+    d->exec_cv.notify_all();
+    d->comp_cv.notify_all();
+  }
+  done_cv_.notify_all();
+}
+
+void Runtime::exec_loop(int d) {
+  be_->bind_thread(d);
+  Device& D = *devs_[d];
+  std::unique_lock<std::mutex> lk(mu_);
+  while (true) {
+    D.exec_cv.wait(lk, [&] {
+      return stopping_ || (!paused_ && !fail_code_ && D.queue.size() > 0 && D.ninflight < static_cast<int>(window_));
+    });
+    if (stopping_) return;
+    Task* t = D.queue.pop();
+    t->state = SFX_STATE_EXECUTING;
+    int s = 0;
+    for (int k = 1; k < nstreams_; ++k)
+      if (D.stream_inflight[k] < D.stream_inflight[s]) s = k;
+    t->stream = s;
+    t->t_pop = now_ns();
+    record(graphs_[t->gid].get(), SFX_EV_POP, t->t_pop, d * nstreams_ + s, t->tid);
+    std::vector<Action> acts;
+    OpLaunch op;
+    std::string err;
+    int rc;
+    while (true) {
+      acts.clear();
+      rc = plan(d, s, t, acts, op, err);
+      if (rc != 1) break;
+      // every evictable block is pinned by in-flight work: issue the write-backs
+      // planned so far, then wait for a completion anywhere and re-plan
+      if (!acts.empty()) {
+        lk.unlock();
+        std::string e2;
+        int r2 = issue(d, s, nullptr, acts, op, e2);
+        lk.lock();
+        if (r2) {
+          rc = SFX_ERR_CUDA;
+          err = e2;
+          break;
+        }
+      }
+      uint64_t total_before = 0;
+      for (auto& dv : devs_) total_before += dv->stats.tasks_executed;
+      done_cv_.wait(lk, [&] {
+        uint64_t tot = 0;
+        for (auto& dv : devs_) tot += dv->stats.tasks_executed;
+        return stopping_ || fail_code_ || tot != total_before;
+      });
+      if (stopping_ || fail_code_) {
+        rc = -100;
+        break;
+      }
+    }
+    if (rc == -100) continue;
+    if (rc < 0) {
+      poison(rc, err);
+      continue;
+    }
+    D.ninflight += 1;
+    D.stream_inflight[s] += 1;
+    lk.unlock();
+    rc = issue(d, s, t, acts, op, err);
+    lk.lock();
+    if (rc) {
+      poison(SFX_ERR_CUDA, err);
+      continue;
+    }
+    if (be_->is_sim()) {
+      complete(t);  // synchronous device: stage_out + task_end before release
+      release(t);
+    } else {
+      release(t);
+      D.inflight.push_back(t);
+      D.comp_cv.notify_one();
+    }
+  }
+}
+
+void Runtime::comp_loop(int d) {
+  be_->bind_thread(d);
+  Device& D = *devs_[d];
+  std::unique_lock<std::mutex> lk(mu_);
+  while (true) {
+    D.comp_cv.wait(lk, [&] { return stopping_ || !D.inflight.empty(); });
+    if (D.inflight.empty()) {
+      if (stopping_) return;
+      continue;
+    }
+    Task* t = D.inflight.front();
+    void* ev = t->end->event;
+    SyncP keep = t->end;
+    lk.unlock();
+    std::string err;
+    int rc = be_->event_sync(d, ev, err);
+    lk.lock();
+    D.inflight.pop_front();
+    if (rc) poison(SFX_ERR_CUDA, err);
+    complete(t);
+  }
+}
+
+// ----------------------------------------------------------- waiting/export
+
+int Runtime::pause(bool p) {
+  std::unique_lock<std::mutex> lk(mu_);
+  paused_ = p;
+  if (!p)
+    for (auto& d : devs_) d->exec_cv.notify_all();
+  return SFX_OK;
+}
+
+int Runtime::wait_all(uint32_t gid, double timeout_s) {
+  std::unique_lock<std::mutex> lk(mu_);
+  auto it = graphs_.find(gid);
+  if (it == graphs_.end()) {
+    last_error = fmt("unknown graph %u", gid);
+    return SFX_ERR_CONFIG;
+  }
+  Graph* g = it->second.get();
+  auto done = [&] { return fail_code_ != 0 || g->completed >= g->inserted; };
+  if (timeout_s < 0) {
+    done_cv_.wait(lk, done);
+  } else {
+    done_cv_.wait_for(lk, std::chrono::duration<double>(timeout_s), done);
+  }
+  if (fail_code_) {
+    last_error = fail_msg_;
+    return SFX_ERR_ENGINE_FAILED;
+  }
+  return g->completed >= g->inserted ? SFX_OK : SFX_TIMEOUT;
+}
+
+int Runtime::wait_task(uint64_t tid, double timeout_s) {
+  std::unique_lock<std::mutex> lk(mu_);
+  auto it = tasks_by_tid_.find(tid);
+  if (it == tasks_by_tid_.end()) {
+    last_error = "unknown task";
+    return SFX_ERR_CONFIG;
+  }
+  Task* t = it->second;
+  auto done = [&] { return t->state == SFX_STATE_FINISHED || fail_code_ != 0; };
+  if (timeout_s < 0)
+    done_cv_.wait(lk, done);
+  else
+    done_cv_.wait_for(lk, std::chrono::duration<double>(timeout_s), done);
+  if (t->state == SFX_STATE_FINISHED) return SFX_OK;
+  if (fail_code_) {
+    last_error = fail_msg_;
+    return SFX_ERR_ENGINE_FAILED;
+  }
+  return SFX_TIMEOUT;
+}
+
+int Runtime::task_state(uint64_t tid, int32_t* st) {
+  std::unique_lock<std::mutex> lk(mu_);
+  auto it = tasks_by_tid_.find(tid);
+  if (it == tasks_by_tid_.end()) {
+    last_error = "unknown task";
+    return SFX_ERR_CONFIG;
+  }
+  *st = it->second->state;
+  return SFX_OK;
+}
+
+int Runtime::stats(int dev, sfx_dev_stats* out) {
+  std::unique_lock<std::mutex> lk(mu_);
+  if (dev < 0 || dev >= ndev_) {
+    last_error = "bad device index";
+    return SFX_ERR_CONFIG;
+  }
+  *out = devs_[dev]->stats;
+  return SFX_OK;
+}
+
+int Runtime::resident(int dev, uint64_t* hids, uint64_t cap, uint64_t* n) {
+  std::unique_lock<std::mutex> lk(mu_);
+  if (dev < 0 || dev >= ndev_) {
+    last_error = "bad device index";
+    return SFX_ERR_CONFIG;
+  }
+  uint64_t k = 0;
+  for (auto& kv : devs_[dev]->blocks) {
+    if (hids && k < cap) hids[k] = kv.first;
+    ++k;
+  }
+  *n = k;
+  return SFX_OK;
+}
+
+int Runtime::block_state(uint64_t hid, int dev, int32_t* st, int32_t* host_valid) {
+  std::unique_lock<std::mutex> lk(mu_);
+  Handle* h = nullptr;
+  for (auto& hp : handle_store_)
+    if (hp->hid == hid) h = hp.get();
+  if (!h || dev < 0 || dev >= ndev_) {
+    last_error = "unknown handle or device";
+    return SFX_ERR_CONFIG;
+  }
+  Block* b = h->blocks[dev];
+  *st = b ? ((b->valid ? 1 : 0) | (b->dirty ? 2 : 0) | 4) : 0;
+  *host_valid = h->host_valid ? 1 : 0;
+  return SFX_OK;
+}
+
+int Runtime::trace(uint32_t gid, sfx_event* buf, uint64_t cap, uint64_t* n) {
+  std::unique_lock<std::mutex> lk(mu_);
+  auto it = graphs_.find(gid);
+  if (it == graphs_.end()) {
+    last_error = "unknown graph";
+    return SFX_ERR_CONFIG;
+  }
+  auto& ev = it->second->events;
+  std::stable_sort(ev.begin(), ev.end(), [](const sfx_event& a, const sfx_event& b) { return a.t_ns < b.t_ns; });
+  *n = ev.size();
+  if (buf) memcpy(buf, ev.data(), std::min<uint64_t>(cap, ev.size()) * sizeof(sfx_event));
+  return SFX_OK;
+}
+
+int Runtime::edges(uint32_t gid, uint64_t* src, uint64_t* dst, uint64_t* hid, uint64_t cap, uint64_t* n) {
+  // trace.py:94-102 / 122-127: every member of slot i -> every member of slot i+1
+  std::unique_lock<std::mutex> lk(mu_);
+  auto it = graphs_.find(gid);
+  if (it == graphs_.end()) {
+    last_error = "unknown graph";
+    return SFX_ERR_CONFIG;
+  }
+  uint64_t k = 0;
+  for (Handle* h : it->second->handles) {
+    for (size_t i = 0; i + 1 < h->slots.size(); ++i)
+      for (Task* a : h->slots[i].tasks)
+        for (Task* b : h->slots[i + 1].tasks) {
+          if (k < cap) {
+            if (src) src[k] = a->tid;
+            if (dst) dst[k] = b->tid;
+            if (hid) hid[k] = h->hid;
+          }
+          ++k;
+        }
+  }
+  *n = k;
+  return SFX_OK;
+}
+
+int Runtime::violations(uint64_t* n) {
+  // race detection on device timestamps: every edge must satisfy
+  // start(dst) >= end(src) (handles.py:88-107 restated for streams)
+  std::unique_lock<std::mutex> lk(mu_);
+  uint64_t bad = 0;
+  for (auto& hp : handle_store_) {
+    Handle* h = hp.get();
+    for (size_t i = 0; i + 1 < h->slots.size(); ++i)
+      for (Task* a : h->slots[i].tasks)
+        for (Task* b : h->slots[i + 1].tasks) {
+          if (a->state != SFX_STATE_FINISHED || b->state != SFX_STATE_FINISHED) continue;
+          if (!a->t_end || !b->t_start) continue;
+          const int64_t slack = (a->dev == b->dev) ? 0 : 20000;  // cross-device clock calibration
+          if (b->t_start + slack < a->t_end) ++bad;
+        }
+  }
+  *n = bad;
+  return SFX_OK;
+}
+
+int Runtime::failure(int* code, char* msg, uint64_t cap) {
+  std::unique_lock<std::mutex> lk(mu_);
+  *code = fail_code_;
+  if (msg && cap) {
+    strncpy(msg, fail_msg_.c_str(), cap - 1);
+    msg[cap - 1] = 0;
+  }
+  return SFX_OK;
+}
+
+}  // namespace sfx

@@ -1,0 +1,286 @@
+// Native STF runtime: dependency core, locality-aware per-device schedulers,
+// per-device tile arenas (LRU + valid/dirty coherency), stream executors with
+// CUDA-event release, and completion tracking.
+//
+// Semantics follow the reference seqflow runtime (paths relative to
+// /root/reference/pkg/src/seqflow):
+//   slot grouping ........ handles.py:209-236  (Runtime::bind)
+//   pending counter ...... task.py:76,105-124  (Task::pending, insertion guard)
+//   release / advance .... handles.py:274-343  (Runtime::release)
+//   FIFO / priority ...... scheduler.py:66-126 (DevQueue)
+//   staging / LRU ........ device.py:197-378   (Runtime::plan_access, evict)
+//   coherency ............ device.py:282-326   (dirty_dev / host_valid)
+//
+// B200-first differences:
+//   * a task is released when it is LAUNCHED, not when it finishes: its
+//     successors are enqueued behind a cudaStreamWaitEvent on its end event,
+//     so the host never sits on the critical path; completion is tracked by
+//     a per-device thread that only unpins blocks and does accounting;
+//   * cross-device reads pull the freshest copy peer-to-peer (NVLink) from
+//     the dirty owner instead of bouncing through the host;
+//   * commutative members are serialized per handle by chaining on the
+//     previous member's end event (any order, never concurrent).
+#pragma once
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "sfx.h"
+
+namespace sfx {
+
+enum Cat : uint8_t { CAT_R = 0, CAT_A = 1, CAT_C = 2, CAT_X = 3 };
+
+inline Cat category_of(uint32_t mode) {
+  switch (mode) {
+    case SFX_READ: return CAT_R;
+    case SFX_ATOMIC_WRITE: return CAT_A;
+    case SFX_COMMUTATIVE_WRITE: return CAT_C;
+    default: return CAT_X;  // WRITE and MAYBE_WRITE are exclusive (access.py:41-47)
+  }
+}
+inline bool mode_writes(uint32_t m) { return m != SFX_READ; }
+
+class Backend;
+
+// A point recorded on one device stream (a CUDA event), shared by everything
+// that must wait for it.  `recorded` flips once the executor that planned it
+// has issued the record, so a waiter planned meanwhile can spin briefly.
+struct Sync {
+  Backend* be = nullptr;
+  int dev = -1, stream = -1;
+  void* event = nullptr;
+  bool timing = false;
+  std::atomic<bool> recorded{false};
+  bool complete = false;  // guarded by the runtime mutex
+  ~Sync();
+};
+using SyncP = std::shared_ptr<Sync>;
+
+struct Task;
+struct Handle;
+
+struct Slot {
+  Cat cat;
+  std::vector<Task*> tasks;
+  uint32_t done = 0;
+};
+
+struct Block {
+  Handle* h = nullptr;
+  int dev = -1;
+  uint64_t off = 0, size = 0;
+  uint64_t stamp = 0;
+  int pins = 0;
+  bool valid = false, dirty = false, zombie = false;
+  SyncP ready;  // contents valid once this completes (null: valid now)
+};
+
+struct Handle {
+  uint64_t hid = 0;
+  uint32_t gid = 0;
+  void* host = nullptr;
+  uint64_t bytes = 0;
+  int64_t rows = 0, cols = 0, ld = 0;
+  int32_t dtype = 0;
+  std::vector<Slot> slots;
+  uint32_t active = 0;
+  std::vector<Block*> blocks;  // per device
+  int dirty_dev = -1;          // at most one dirty copy
+  bool host_valid = true;
+  SyncP host_ready;     // host buffer is current once this completes
+  SyncP commute_last;   // end of the last launched commutative member
+  int group_dev = -1;   // device of the active atomic/commutative group
+  int home = -1;        // owner hint (2-D block-cyclic distribution)
+};
+
+struct Access {
+  Handle* h;
+  uint32_t mode;
+  uint32_t slot;
+};
+
+struct Task {
+  uint64_t tid = 0;
+  uint32_t gid = 0, op = 0;
+  int32_t prio = 0, hint = -1;
+  double fp[4] = {0, 0, 0, 0};
+  int64_t ip[4] = {0, 0, 0, 0};
+  std::vector<Access> acc;
+  int32_t pending = 1;  // insertion guard (task.py:76)
+  int state = SFX_STATE_INSERTED;
+  bool released = false;
+  uint64_t seq = 0;  // scheduler push sequence
+  int dev = -1, stream = -1;
+  std::vector<SyncP> waits;       // predecessors' end points
+  SyncP start, end;
+  std::vector<Block*> pinned;     // unpinned at completion
+  std::vector<SyncP> copy_syncs;  // copies issued on this task's stream
+  int64_t t_push = 0, t_pop = 0, t_start = 0, t_end = 0;
+};
+
+struct Operand {
+  void* dptr = nullptr;
+  uint64_t bytes = 0;
+  int64_t rows = 0, cols = 0, ld = 0;
+  int32_t dtype = 0;
+};
+
+struct OpLaunch {
+  uint32_t op = 0;
+  int n = 0;
+  Operand o[8];
+  double fp[4];
+  int64_t ip[4];
+};
+
+// One step of a planned task, issued outside the runtime lock.
+struct Action {
+  enum Kind { WAIT, H2D, D2H, P2P, RECORD } kind;
+  SyncP sync;
+  uint64_t dst_off = 0, src_off = 0, n = 0;
+  void* host = nullptr;
+  int src_dev = -1;
+};
+
+// Device/stream abstraction: CUDA (B200) or host-memory simulation (tests).
+class Backend {
+ public:
+  virtual ~Backend() {}
+  virtual bool is_sim() const = 0;
+  virtual int init_device(int d, int ordinal, int nstreams, uint64_t arena_bytes, std::string& err) = 0;
+  virtual void bind_thread(int d) = 0;
+  virtual uint64_t arena_capacity(int d) = 0;
+  virtual void* arena_ptr(int d, uint64_t off) = 0;
+  virtual void* event_create(int d, bool timing) = 0;
+  virtual void event_release(int d, void* ev) = 0;
+  virtual int event_record(int d, int stream, void* ev, std::string& err) = 0;
+  virtual int stream_wait(int d, int stream, void* ev, std::string& err) = 0;
+  virtual int event_sync(int d, void* ev, std::string& err) = 0;
+  // CLOCK_MONOTONIC ns of a completed timing event
+  virtual int64_t event_time_ns(int d, void* ev) = 0;
+  virtual int copy_h2d(int d, int stream, uint64_t dst_off, const void* src, uint64_t n, std::string& err) = 0;
+  virtual int copy_d2h(int d, int stream, void* dst, uint64_t src_off, uint64_t n, std::string& err) = 0;
+  virtual int copy_p2p(int d, int stream, uint64_t dst_off, int src_dev, uint64_t src_off, uint64_t n,
+                       std::string& err) = 0;
+  virtual int launch(int d, int stream, const OpLaunch& op, std::string& err) = 0;
+  virtual bool supports(uint32_t op) const = 0;
+  virtual void shutdown() = 0;
+};
+
+Backend* make_sim_backend(int ndev);
+Backend* make_cuda_backend(int ndev, const int* ordinals, bool trace);
+int64_t now_ns();
+
+struct Graph {
+  uint32_t gid = 0;
+  uint64_t inserted = 0, completed = 0;
+  std::vector<Task*> tasks;
+  std::vector<Handle*> handles;
+  std::vector<sfx_event> events;
+};
+
+struct DevQueue {
+  // FIFO (scheduler.py:66-94) or max-priority with FIFO ties (scheduler.py:97-126)
+  bool prio = false;
+  std::deque<Task*> fifo;
+  std::vector<Task*> heap;
+  size_t size() const { return prio ? heap.size() : fifo.size(); }
+  void push(Task* t);
+  Task* pop();
+};
+
+struct Device {
+  int index = 0;
+  uint64_t capacity = 0, free_bytes = 0;
+  std::map<uint64_t, uint64_t> free_list;      // offset -> size, first fit
+  std::unordered_map<uint64_t, Block*> blocks;  // hid -> live block
+  uint64_t clock = 0;
+  DevQueue queue;
+  std::deque<Task*> inflight;
+  std::vector<int> stream_inflight;
+  int ninflight = 0;
+  std::condition_variable exec_cv, comp_cv;
+  std::thread exec_thread, comp_thread;
+  sfx_dev_stats stats{};
+};
+
+class Runtime {
+ public:
+  Runtime(Backend* be, int ndev, int nstreams, uint32_t sched, uint32_t flags, uint32_t window, uint64_t align);
+  ~Runtime();
+  int init(const uint64_t* arena_bytes, std::string& err);
+
+  int graph_create(uint32_t* gid);
+  int reg(uint32_t gid, uint64_t hid, void* host, uint64_t bytes, int64_t rows, int64_t cols, int64_t ld,
+          int32_t dtype);
+  int set_home(uint64_t hid, int dev);
+  int unreg(uint64_t hid);
+  int submit(uint32_t n, const sfx_task_desc* tasks, const sfx_access* acc);
+  int flush(uint32_t gid, uint64_t tid, uint64_t hid, int write_mode);
+  int pause(bool p);
+  int wait_all(uint32_t gid, double timeout_s);
+  int wait_task(uint64_t tid, double timeout_s);
+  int task_state(uint64_t tid, int32_t* st);
+  int stats(int dev, sfx_dev_stats* out);
+  int resident(int dev, uint64_t* hids, uint64_t cap, uint64_t* n);
+  int block_state(uint64_t hid, int dev, int32_t* st, int32_t* host_valid);
+  int trace(uint32_t gid, sfx_event* buf, uint64_t cap, uint64_t* n);
+  int edges(uint32_t gid, uint64_t* src, uint64_t* dst, uint64_t* hid, uint64_t cap, uint64_t* n);
+  int violations(uint64_t* n);
+  int failure(int* code, char* msg, uint64_t cap);
+
+  std::string last_error;
+
+ private:
+  int validate(const sfx_task_desc& d, const sfx_access* acc, std::string& err);
+  void bind(Task* t, Handle* h, uint32_t mode);
+  void push_ready(Task* t, int wid);
+  int place(Task* t);
+  void release(Task* t);
+  void advance(Handle* h);
+  int plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op, std::string& err);
+  int ensure_block(int d, int s, Handle* h, std::vector<Action>& acts, std::vector<Block*>& tmp_pins, Block** out,
+                   std::string& err);
+  int evict_one(int d, int s, std::vector<Action>& acts, std::string& err);
+  void drop_block(Block* b, bool write_back, std::vector<Action>* acts, int s);
+  void free_space(int d, uint64_t off, uint64_t size);
+  bool alloc_space(int d, uint64_t size, uint64_t* off);
+  SyncP new_sync(int d, int s, bool timing);
+  int issue(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op, std::string& err);
+  void complete(Task* t);
+  void poison(int code, const std::string& msg);
+  void record(Graph* g, int kind, int64_t t, int wid, uint64_t tid, int64_t extra = 0);
+  void exec_loop(int d);
+  void comp_loop(int d);
+
+  Backend* be_;
+  int ndev_, nstreams_;
+  uint32_t sched_, flags_, window_;
+  uint64_t align_;
+  bool trace_;
+  std::mutex mu_;
+  std::condition_variable done_cv_;
+  std::vector<std::unique_ptr<Device>> devs_;
+  std::unordered_map<uint64_t, Handle*> handles_;
+  std::vector<std::unique_ptr<Handle>> handle_store_;
+  std::unordered_map<uint32_t, std::unique_ptr<Graph>> graphs_;
+  std::unordered_map<uint64_t, Task*> tasks_by_tid_;
+  std::deque<Task> task_store_;
+  uint32_t next_gid_ = 1;
+  uint64_t push_seq_ = 0;
+  bool paused_ = false, stopping_ = false;
+  int fail_code_ = 0;
+  std::string fail_msg_;
+  bool started_ = false;
+};
+
+}  // namespace sfx

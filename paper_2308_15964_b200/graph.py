@@ -1,0 +1,439 @@
+"""Task graphs on the GPU engine (drop-in for reference src/graph.py:26-295).
+
+Insertion keeps the reference's contract: one inserter thread, accesses in
+declaration order, ``DuplicateAccessError`` for an object declared twice,
+process-global task ids (task.py:63-69) and handle ids (handles.py:123-126),
+``wait_all`` returning False on timeout and raising ``EngineFailedError``
+(with the original error as ``__cause__``) after a failure.  Everything past
+the access list -- slot binding, readiness, placement, staging, launch and
+release -- happens in libsfx.so; Python never runs on the execution path.
+"""
+
+from __future__ import annotations
+
+import contextlib
+import ctypes
+import enum
+import itertools
+import threading
+import time
+
+import numpy as np
+
+from . import _native as N
+from . import memory
+from . import ops as ops_mod
+from .access import AccessMode, AccessSpec
+from .errors import (
+    ConfigurationError,
+    DuplicateAccessError,
+    EngineFailedError,
+    RegistrationError,
+    SpeculationError,
+)
+
+_tid_counter = itertools.count(1)
+_hid_counter = itertools.count(1)
+_id_lock = threading.Lock()
+
+
+def _next_tid() -> int:
+    with _id_lock:
+        return next(_tid_counter)
+
+
+def _reserve_tids(n: int) -> int:
+    """First of ``n`` consecutive process-global task ids."""
+    global _tid_counter
+    with _id_lock:
+        first = next(_tid_counter)
+        _tid_counter = itertools.count(first + n)
+    return first
+
+
+def _next_hid() -> int:
+    with _id_lock:
+        return next(_hid_counter)
+
+
+TASK_DTYPE = np.dtype({
+    "names": ["tid", "graph", "op", "priority", "device", "n_access", "flags", "fparam", "iparam"],
+    "formats": [np.uint64, np.uint32, np.uint32, np.int32, np.int32, np.uint32, np.uint32,
+                (np.float64, 4), (np.int64, 4)],
+    "offsets": [0, 8, 12, 16, 20, 24, 28, 32, 64],
+    "itemsize": 96,
+})
+ACCESS_DTYPE = np.dtype({"names": ["hid", "mode", "reserved"], "formats": [np.uint64, np.uint32, np.uint32],
+                         "offsets": [0, 8, 12], "itemsize": 16})
+assert TASK_DTYPE.itemsize == ctypes.sizeof(N.TaskDesc)
+assert ACCESS_DTYPE.itemsize == ctypes.sizeof(N.AccessDesc)
+
+
+class TaskState(enum.Enum):
+    INSERTED = "inserted"
+    READY = "ready"
+    EXECUTING = "executing"
+    FINISHED = "finished"
+    DISABLED = "disabled"
+
+
+_STATE = {0: TaskState.INSERTED, 1: TaskState.READY, 2: TaskState.EXECUTING, 3: TaskState.FINISHED}
+
+
+class _Entry:
+    __slots__ = ("hid", "obj", "desc")
+
+    def __init__(self, hid, obj, desc):
+        self.hid = hid
+        self.obj = obj
+        self.desc = desc
+
+
+class TaskViewer:
+    """Reference to one inserted task (reference task.py:210-262)."""
+
+    __slots__ = ("_graph", "_tid")
+
+    def __init__(self, graph, tid):
+        self._graph = graph
+        self._tid = tid
+
+    @property
+    def task_id(self) -> int:
+        return self._tid
+
+    @property
+    def state(self) -> TaskState:
+        g = self._graph
+        g._flush_batch()
+        st = ctypes.c_int32(0)
+        N.check(N.lib.sfx_task_state(g._h, self._tid, ctypes.byref(st)), g._h)
+        return _STATE[st.value]
+
+    def set_name(self, name: str) -> "TaskViewer":
+        self._graph._names[self._tid] = name
+        return self
+
+    def wait(self, timeout=None) -> None:
+        g = self._graph
+        g._flush_batch()
+        rc = N.lib.sfx_wait_task(g._h, self._tid, -1.0 if timeout is None else float(timeout))
+        if rc == N.TIMEOUT:
+            raise TimeoutError(f"timed out waiting for {g._label(self._tid)}")
+        if rc == N.ERR_ENGINE_FAILED:
+            raise g._failure()
+        N.check(rc, g._h)
+
+    def get_value(self):
+        """Device ops produce no host value (the reference raises ValueError then)."""
+        self.wait()
+        raise ValueError(f"{self._graph._label(self._tid)} produced no value")
+
+
+class TraceView:
+    """Events of one graph as reference tuples (kind, t_ns, worker, tid, extra)."""
+
+    def __init__(self, graph):
+        self._graph = graph
+        self.enabled = True
+
+    def export_events(self) -> list:
+        g = self._graph
+        g._flush_batch()
+        n = ctypes.c_uint64(0)
+        N.check(N.lib.sfx_trace(g._h, g._gid, None, 0, ctypes.byref(n)), g._h)
+        buf = (N.Event * max(n.value, 1))()
+        N.check(N.lib.sfx_trace(g._h, g._gid, buf, n.value, ctypes.byref(n)), g._h)
+        t0 = g._t0
+        out = []
+        for e in buf[: n.value]:
+            extra = e.extra if e.kind in (N.EV_STAGE_BEGIN, N.EV_STAGE_END) else None
+            out.append((N.EV_NAMES[e.kind], e.t_ns - t0, e.worker, e.tid, extra))
+        out.sort(key=lambda ev: ev[1])
+        return out
+
+
+class TaskGraph:
+    """Sequential task flow over declared data accesses, executed on B200s."""
+
+    def __init__(self, speculation: bool = False, trace: bool = True):
+        if speculation:
+            raise SpeculationError(
+                "speculative execution is not part of the GPU path (the reference also rejects "
+                "device callables in speculative tasks, speculation.py:140-143)")
+        self.engine = None
+        self._h = None
+        self._gid = None
+        self._entries = {}  # id(obj) -> _Entry
+        self._by_hid = {}
+        self._names = {}
+        self._tids = []
+        self._inserter_ident = None
+        self._batch = None
+        self._t0 = time.perf_counter_ns()
+        self.trace = TraceView(self)
+        self.trace.enabled = trace
+        self.speculation_enabled = False
+
+    # -- attachment (graph.py:57-64) -----------------------------------------
+    def compute_on(self, engine) -> "TaskGraph":
+        if self.engine is not None:
+            raise ConfigurationError("graph is already attached to an engine")
+        gid = ctypes.c_uint32(0)
+        N.check(N.lib.sfx_graph_create(engine._h, ctypes.byref(gid)), engine._h)
+        self.engine = engine
+        self._h = engine._h
+        self._gid = gid.value
+        engine.adopt(self)
+        self._t0 = time.perf_counter_ns()
+        return self
+
+    # -- registration (graph.py:68-73, handles.py:140-182) --------------------
+    def _register(self, obj) -> _Entry:
+        desc = memory.describe(obj)
+        hid = _next_hid()
+        N.check(N.lib.sfx_register(self._h, self._gid, hid, desc.ptr, desc.nbytes, desc.rows, desc.cols,
+                                   desc.ld, desc.dtype), self._h)
+        e = _Entry(hid, obj, desc)
+        self._entries[id(obj)] = e
+        self._by_hid[hid] = e
+        return e
+
+    def register(self, obj, nbytes: int = 0):
+        if self.engine is None:
+            raise ConfigurationError("attach the graph to an engine before registering")
+        if id(obj) in self._entries:
+            raise RegistrationError(f"object {type(obj).__name__} is already registered")
+        return self._register(obj).hid
+
+    def unregister(self, obj) -> None:
+        e = self._entries.get(id(obj))
+        if e is None:
+            raise RegistrationError("object is not registered")
+        self._flush_batch()
+        N.check(N.lib.sfx_unregister(self._h, e.hid), self._h)
+        del self._entries[id(obj)]
+        del self._by_hid[e.hid]
+
+    def hid_of(self, obj) -> int:
+        e = self._entries.get(id(obj))
+        if e is None:
+            if self.engine is None:
+                raise ConfigurationError("attach the graph to an engine before inserting")
+            e = self._register(obj)
+        return e.hid
+
+    def place(self, obj, device: int) -> None:
+        """Owner hint for the locality-aware scheduler (e.g. 2-D block-cyclic)."""
+        N.check(N.lib.sfx_set_home(self._h, self.hid_of(obj), int(device)), self._h)
+
+    # -- insertion (graph.py:77-166) -------------------------------------------
+    def task(self, *accesses, host=None, device=None, priority: int = 0, name=None):
+        if __debug__:
+            ident = threading.get_ident()
+            assert self._inserter_ident in (None, ident), "tasks must be inserted by a single thread"
+            self._inserter_ident = ident
+        if self.engine is None:
+            raise ConfigurationError("attach the graph to an engine before inserting")
+        if device is None:
+            if host is not None:
+                raise ConfigurationError(
+                    "host callables run on the CPU oracle only: the GPU engine has no CPU fallback; "
+                    "pass device=<paper_2308_15964_b200.ops op>")
+            raise ConfigurationError("a task needs a host or device callable")
+        if not isinstance(device, ops_mod.Op):
+            raise ConfigurationError(
+                f"device= must be a registered op (paper_2308_15964_b200.ops), got {device!r}")
+        hids = []
+        modes = []
+        for spec in accesses:
+            if not isinstance(spec, AccessSpec):
+                raise ConfigurationError(f"accesses must be built with the access helpers, got {spec!r}")
+            if spec.view is not None:
+                raise ConfigurationError("array-view accesses are host-task constructs (oracle only)")
+            hid = self.hid_of(spec.obj)
+            if hid in hids:
+                raise DuplicateAccessError(f"task declares {type(spec.obj).__name__} twice")
+            hids.append(hid)
+            modes.append(spec.mode.code)
+        tid = _next_tid()
+        if name is not None:
+            self._names[tid] = name
+        self._tids.append(tid)
+        self._submit_one(tid, device, priority, hids, modes)
+        return TaskViewer(self, tid)
+
+    def _submit_one(self, tid, op, priority, hids, modes, dev_hint=-1):
+        if self._batch is not None:
+            self._batch.append((tid, op, priority, hids, modes, dev_hint))
+            return
+        d = N.TaskDesc()
+        d.tid = tid
+        d.graph = self._gid
+        d.op = op.code
+        d.priority = int(priority)
+        d.device = dev_hint
+        d.n_access = len(hids)
+        for k in range(4):
+            d.fparam[k] = op.fparam[k]
+            d.iparam[k] = op.iparam[k]
+        acc = (N.AccessDesc * max(len(hids), 1))()
+        for k, (h, m) in enumerate(zip(hids, modes)):
+            acc[k].hid = h
+            acc[k].mode = m
+        N.check(N.lib.sfx_submit(self._h, 1, ctypes.byref(d), acc), self._h)
+
+    def submit_arrays(self, ops_codes, fparams, iparams, priorities, n_access, acc_hids, acc_modes,
+                      devices=None, names=None) -> np.ndarray:
+        """Vectorised insertion of many tasks in one call (same semantics as a loop of ``task``).
+
+        Arrays are per task (op code, 4 fparams, 4 iparams, priority, access
+        count) plus the flattened access list.  Returns the task ids.
+        """
+        self._flush_batch()
+        n = len(ops_codes)
+        descs = np.zeros(n, dtype=TASK_DTYPE)
+        first = _reserve_tids(n)
+        tids = np.arange(first, first + n, dtype=np.uint64)
+        descs["tid"] = tids
+        descs["graph"] = self._gid
+        descs["op"] = ops_codes
+        descs["priority"] = priorities
+        descs["device"] = -1 if devices is None else devices
+        descs["n_access"] = n_access
+        descs["fparam"] = fparams
+        descs["iparam"] = iparams
+        acc = np.zeros(len(acc_hids), dtype=ACCESS_DTYPE)
+        acc["hid"] = acc_hids
+        acc["mode"] = acc_modes
+        N.check(N.lib.sfx_submit(self._h, n, descs.ctypes.data, acc.ctypes.data if len(acc) else None), self._h)
+        self._tids.extend(int(t) for t in tids)
+        if names is not None:
+            for t, nm in zip(tids, names):
+                if nm is not None:
+                    self._names[int(t)] = nm
+        return tids
+
+    @contextlib.contextmanager
+    def batch(self):
+        """Buffer insertions and submit them in one native call on exit."""
+        outer = self._batch is not None
+        if not outer:
+            self._batch = []
+        try:
+            yield self
+        finally:
+            if not outer:
+                self._flush_batch()
+
+    @contextlib.contextmanager
+    def gated(self):
+        """Insert with the executors held, like the reference's gate task
+        (tests/conftest.py:184-203): the slot layout is then exactly the static one."""
+        self.engine.pause()
+        try:
+            with self.batch():
+                yield self
+        finally:
+            self.engine.resume()
+
+    def _flush_batch(self):
+        if not self._batch:
+            if self._batch is not None:
+                self._batch = None
+            return
+        batch = self._batch
+        self._batch = None
+        n = len(batch)
+        descs = np.zeros(n, dtype=TASK_DTYPE)
+        total = sum(len(b[3]) for b in batch)
+        acc = np.zeros(max(total, 1), dtype=ACCESS_DTYPE)
+        k = 0
+        for i, (tid, op, prio, hids, modes, dev) in enumerate(batch):
+            descs[i]["tid"] = tid
+            descs[i]["graph"] = self._gid
+            descs[i]["op"] = op.code
+            descs[i]["priority"] = prio
+            descs[i]["device"] = dev
+            descs[i]["n_access"] = len(hids)
+            descs[i]["fparam"] = op.fparam
+            descs[i]["iparam"] = op.iparam
+            for h, m in zip(hids, modes):
+                acc[k]["hid"] = h
+                acc[k]["mode"] = m
+                k += 1
+        N.check(N.lib.sfx_submit(self._h, n, descs.ctypes.data, acc.ctypes.data), self._h)
+
+    # -- waiting (graph.py:199-217) --------------------------------------------
+    def _failure(self) -> EngineFailedError:
+        code = ctypes.c_int(0)
+        msg = ctypes.create_string_buffer(1024)
+        N.lib.sfx_failure(self._h, ctypes.byref(code), msg, 1024)
+        text = msg.value.decode(errors="replace")
+        cause = N.error_for(code.value, text)
+        err = EngineFailedError(f"a task failed: {text}")
+        err.__cause__ = cause
+        return err
+
+    def wait_all(self, timeout=None) -> bool:
+        if self.engine is None:
+            return True
+        self._flush_batch()
+        rc = N.lib.sfx_wait_all(self._h, self._gid, -1.0 if timeout is None else float(timeout))
+        if rc == N.TIMEOUT:
+            return False
+        if rc == N.ERR_ENGINE_FAILED:
+            raise self._failure()
+        N.check(rc, self._h)
+        return True
+
+    # -- device flush (graph.py:258-260) -----------------------------------------
+    def flush_to_host(self, obj, keep_device: bool = False) -> TaskViewer:
+        """Insert a flush of ``obj`` to its host buffer.
+
+        Default = the reference's semantics: a host write, so every device copy
+        is dropped afterwards.  ``keep_device=True`` only cleans the dirty copy
+        (read-mode flush) and keeps device copies valid.
+        """
+        self._flush_batch()
+        hid = self.hid_of(obj)
+        tid = _next_tid()
+        self._names[tid] = "flush"
+        self._tids.append(tid)
+        N.check(N.lib.sfx_flush(self._h, self._gid, tid, hid, 0 if keep_device else 1), self._h)
+        return TaskViewer(self, tid)
+
+    def flush_all(self, keep_device: bool = True) -> None:
+        for e in list(self._entries.values()):
+            self.flush_to_host(e.obj, keep_device=keep_device)
+
+    # -- export -----------------------------------------------------------------
+    def _label(self, tid) -> str:
+        return self._names.get(tid) or f"task{tid}"
+
+    def all_task_ids(self) -> list:
+        return list(self._tids)
+
+    def edges(self) -> list:
+        """Successor edges (src tid, dst tid, hid), one per handle pair (trace.py:94-102)."""
+        self._flush_batch()
+        n = ctypes.c_uint64(0)
+        N.check(N.lib.sfx_edges(self._h, self._gid, None, None, None, 0, ctypes.byref(n)), self._h)
+        m = max(n.value, 1)
+        src = np.zeros(m, np.uint64)
+        dst = np.zeros(m, np.uint64)
+        hid = np.zeros(m, np.uint64)
+        N.check(N.lib.sfx_edges(self._h, self._gid, src.ctypes.data, dst.ctypes.data, hid.ctypes.data, m,
+                                ctypes.byref(n)), self._h)
+        k = n.value
+        return list(zip(src[:k].tolist(), dst[:k].tolist(), hid[:k].tolist()))
+
+    def generate_dot(self, path=None, show_deps: bool = False) -> str:
+        from .trace import generate_dot
+
+        return generate_dot(self, path, show_deps)
+
+    def generate_trace_svg(self, path=None, show_dep_arrows: bool = False) -> str:
+        from .trace import generate_trace_svg
+
+        return generate_trace_svg(self, path, show_dep_arrows)
