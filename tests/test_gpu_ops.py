@@ -1,0 +1,164 @@
+"""GPU parity of the tile ops and the tiled workloads against the CPU oracle.
+
+Tolerances (BASELINE.json north_star / SURVEY.md §8d):
+  GEMM       per-element relative error <= 1e-10 (uniform inputs, no cancellation)
+  Cholesky   ||A - L L^T||_F / ||A||_F <= 1e-12, and L within 1e-10 of the oracle's L
+  TRSM       relative residual ||X L^T - B|| / (||L|| ||X||) <= 1e-13, normwise vs oracle <= 1e-12
+  particles  per-particle potential rel err <= 1e-10; |dF_a| / sum_b |F_ab| <= 1e-12
+"""
+
+import numpy as np
+import pytest
+
+import paper_2308_15964_b200 as sf
+from paper_2308_15964_b200 import algorithms as alg
+from oracle import bodies, inputs, programs
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(eng, fn):
+    g = sf.TaskGraph().compute_on(eng)
+    fn(g)
+    g.flush_all(keep_device=False)
+    assert g.wait_all(timeout=120)
+    return g
+
+
+@pytest.mark.parametrize("b,trans_b", [(256, False), (256, True), (512, True), (320, False)])
+def test_dgemm_tile(gpu_engine, b, trans_b):
+    A = inputs.uniform_tile(11, 0, 0, b, b, b)
+    B = inputs.uniform_tile(12, 0, 0, b, b, b)
+    C = inputs.uniform_tile(13, 0, 0, b, b, b)
+    want = C + A @ (B.T if trans_b else B)
+    _run(gpu_engine, lambda g: g.task(sf.read(A), sf.read(B), sf.write(C), device=sf.ops.dgemm(1.0, 1.0, trans_b)))
+    rel = np.abs(C - want) / np.abs(want)
+    assert rel.max() <= 1e-10, rel.max()
+
+
+def test_dsyrk_tile_lower_only(gpu_engine):
+    b = 512
+    A = inputs.uniform_tile(21, 0, 0, b, b, b)
+    C0 = inputs.uniform_tile(22, 0, 0, b, b, b) + b
+    C = C0.copy()
+    want = C0.copy()
+    bodies.syrk_sub(A, want)
+    _run(gpu_engine, lambda g: g.task(sf.read(A), sf.write(C), device=sf.ops.syrk_sub))
+    il = np.tril_indices(b)
+    iu = np.triu_indices(b, 1)
+    assert np.array_equal(C[iu], C0[iu])  # upper triangle untouched
+    assert (np.abs(C[il] - want[il]) / np.abs(want[il])).max() <= 1e-10
+
+
+@pytest.mark.parametrize("b", [256, 1024])
+def test_dtrsm_tile(gpu_engine, b):
+    S = inputs.spd_tile(31, 0, 0, b, b, b)
+    L = np.linalg.cholesky(S)
+    B = inputs.uniform_tile(32, 0, 0, b, b, b)
+    X = B.copy()
+    _run(gpu_engine, lambda g: g.task(sf.read(L), sf.write(X), device=sf.ops.trsm))
+    want = B.copy()
+    bodies.trsm(L, want)
+    res = np.linalg.norm(X @ L.T - B) / (np.linalg.norm(L) * np.linalg.norm(X))
+    assert res <= 1e-13, res
+    # per-element relative error is ill-posed for a solve (entries cancel); normwise instead
+    assert np.linalg.norm(X - want) / np.linalg.norm(want) <= 1e-12
+
+
+@pytest.mark.parametrize("b", [64, 256, 1024])
+def test_dpotrf_tile(gpu_engine, b):
+    A0 = inputs.spd_tile(41, 0, 0, b, b, b)
+    A = A0.copy()
+    _run(gpu_engine, lambda g: g.task(sf.write(A), device=sf.ops.potrf))
+    L = np.tril(A)
+    assert np.linalg.norm(A0 - L @ L.T) / np.linalg.norm(A0) <= 1e-12
+    iu = np.triu_indices(b, 1)
+    assert np.array_equal(A[iu], A0[iu])  # LAPACK 'L' semantics: upper untouched
+    want = A0.copy()
+    bodies.potrf(want)
+    assert (np.abs(L - np.tril(want)).max() / np.abs(want).max()) <= 1e-12
+
+
+def test_generators_bit_identical(gpu_engine):
+    n, b = 512, 256
+    U = alg.TiledMatrix(n, b)
+    S = alg.TiledMatrix(n, b, lower=True)
+    P = [sf.pinned_empty((4, 128)) for _ in range(3)]
+    def fill(g):
+        alg.insert_fill_uniform(g, U, 7)
+        alg.insert_fill_spd(g, S, 3)
+        alg.insert_fill_particles(g, P, 4)
+    _run(gpu_engine, fill)
+    for (i, j), t in U.tiles.items():
+        assert np.array_equal(t, inputs.uniform_tile(7, i * b, j * b, b, b, n))
+    for (i, j), t in S.tiles.items():
+        assert np.array_equal(t, inputs.spd_tile(3, i * b, j * b, b, b, n))
+    for g, p in enumerate(P):
+        assert np.array_equal(p, inputs.particles(4, g * 128, 128))
+
+
+def test_tiled_gemm_matches_oracle(gpu_engine):
+    n, b = 1024, 256
+    objs = programs.gemm_operands(n, b)
+    want = {k: v.copy() for k, v in objs.items()}
+    programs.run_on_oracle(programs.gemm_program(n // b), want, workers=4)
+    A, B, C = (alg.TiledMatrix(n, b) for _ in range(3))
+    for (i, j) in A.tiles:
+        A[i, j][...] = objs[("A", i, j)]
+        B[i, j][...] = objs[("B", i, j)]
+        C[i, j][...] = 0.0
+    _run(gpu_engine, lambda g: alg.insert_gemm(g, A, B, C))
+    for (i, j), t in C.tiles.items():
+        w = want[("C", i, j)]
+        assert (np.abs(t - w) / np.abs(w)).max() <= 1e-10
+
+
+def test_tiled_cholesky_matches_oracle(gpu_engine):
+    n, b = 2048, 256
+    objs = programs.cholesky_operands(n, b)
+    A0 = programs.assemble_lower(objs, n, b)
+    A0 = A0 + np.tril(A0, -1).T
+    want = {k: v.copy() for k, v in objs.items()}
+    programs.run_on_oracle(programs.cholesky_program(n // b), want, workers=4)
+    M = alg.TiledMatrix(n, b, lower=True)
+    for ij, t in M.tiles.items():
+        t[...] = objs[("A",) + ij]
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, 8), scheduler="prio", device_memory=4 << 30)
+    try:
+        _run(eng, lambda g: alg.insert_cholesky(g, M))
+    finally:
+        eng.stop()
+    L = M.to_dense(lower_only=True)
+    assert np.linalg.norm(A0 - L @ L.T) / np.linalg.norm(A0) <= 1e-12
+    Lw = programs.assemble_lower(want, n, b)
+    assert np.abs(L - Lw).max() / np.abs(Lw).max() <= 1e-12
+
+
+def test_particles_match_oracle(gpu_engine):
+    ng, per = 6, 512
+    objs = programs.particle_operands(ng, per)
+    want = {k: v.copy() for k, v in objs.items()}
+    programs.run_on_oracle(programs.particles_program(ng), want, workers=4)
+    P = [sf.pinned_empty((4, per)) for _ in range(ng)]
+    F = [sf.pinned_zeros((4, per)) for _ in range(ng)]
+    for g in range(ng):
+        P[g][...] = objs[("P", g)]
+    _run(gpu_engine, lambda g: alg.insert_particles(g, P, F))
+    for g in range(ng):
+        w = want[("F", g)]
+        got = F[g]
+        pot_rel = np.abs(got[3] - w[3]) / np.abs(w[3])
+        assert pot_rel.max() <= 1e-10, pot_rel.max()
+        # normalised force error: |dF_a| / sum_b |F_ab|  (sum_b |F_ab| bounded below by |F_a|)
+        Pall = np.concatenate([objs[("P", h)] for h in range(ng)], axis=1)
+        a = Pall[:, g * per:(g + 1) * per]
+        dx = a[0][:, None] - Pall[0][None, :]
+        dy = a[1][:, None] - Pall[1][None, :]
+        dz = a[2][:, None] - Pall[2][None, :]
+        r2 = dx * dx + dy * dy + dz * dz + bodies.EPS2
+        mag = a[3][:, None] * Pall[3][None, :] / r2
+        idx = np.arange(per)
+        mag[idx, g * per + idx] = 0.0
+        denom = mag.sum(axis=1)
+        dF = np.sqrt(((got[:3] - w[:3]) ** 2).sum(axis=0))
+        assert (dF / denom).max() <= 1e-12
