@@ -140,6 +140,10 @@ typedef struct sfx_dev_stats {
   uint64_t blocks, bytes_in_use, capacity;
   /* executor */
   uint64_t tasks_executed, kernel_launches, stream_waits;
+  /* host-side time of the executor (ns): planning under the lock, issuing
+   * stream work outside it, releasing successors; completion-thread time;
+   * number of launch groups */
+  uint64_t t_plan_ns, t_issue_ns, t_release_ns, t_complete_ns, groups;
 } sfx_dev_stats;
 
 typedef struct sfx_event {
@@ -194,6 +198,11 @@ int sfx_edges(sfx_runtime* rt, uint32_t gid, uint64_t* src, uint64_t* dst, uint6
               uint64_t* n);
 /* conflict instrumentation (handles.py:88-107): violations observed */
 int sfx_violations(sfx_runtime* rt, uint64_t* n);
+
+/* tuning knobs: "group_max" (ready same-shape tasks fused into one grouped
+ * launch, default 32; 1 disables grouping) and "window" (max in-flight tasks
+ * per device) */
+int sfx_set_option(sfx_runtime* rt, const char* key, int64_t value);
 
 /* pinned host memory (cudaHostAlloc; aligned malloc in sim) for tiles */
 int sfx_host_alloc(uint64_t bytes, int sim, void** out);

@@ -86,7 +86,8 @@ class DevStats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in (
         "bytes_to_device", "copies_to_device", "bytes_from_device", "copies_from_device",
         "bytes_p2p_in", "copies_p2p_in", "hits", "misses", "evictions", "writebacks",
-        "blocks", "bytes_in_use", "capacity", "tasks_executed", "kernel_launches", "stream_waits")]
+        "blocks", "bytes_in_use", "capacity", "tasks_executed", "kernel_launches", "stream_waits",
+        "t_plan_ns", "t_issue_ns", "t_release_ns", "t_complete_ns", "groups")]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -129,6 +130,7 @@ def _load():
         "sfx_trace": ([P, u32, P, u64, ctypes.POINTER(u64)], ctypes.c_int),
         "sfx_edges": ([P, u32, P, P, P, u64, ctypes.POINTER(u64)], ctypes.c_int),
         "sfx_violations": ([P, ctypes.POINTER(u64)], ctypes.c_int),
+        "sfx_set_option": ([P, ctypes.c_char_p, i64], ctypes.c_int),
         "sfx_host_alloc": ([u64, ctypes.c_int, ctypes.POINTER(P)], ctypes.c_int),
         "sfx_host_free": ([P, ctypes.c_int], ctypes.c_int),
         "sfx_fp64_peak": ([ctypes.c_int, ctypes.POINTER(dbl), ctypes.POINTER(dbl)], ctypes.c_int),
@@ -147,7 +149,7 @@ EXPORTED = ("sfx_abi_version", "sfx_device_count", "sfx_create", "sfx_destroy", 
             "sfx_failure", "sfx_graph_create", "sfx_register", "sfx_set_home", "sfx_unregister",
             "sfx_submit", "sfx_pause", "sfx_resume", "sfx_wait_all", "sfx_wait_task",
             "sfx_task_state", "sfx_flush", "sfx_stats", "sfx_resident", "sfx_block_state",
-            "sfx_trace", "sfx_edges", "sfx_violations", "sfx_host_alloc", "sfx_host_free",
+            "sfx_trace", "sfx_edges", "sfx_violations", "sfx_set_option", "sfx_host_alloc", "sfx_host_free",
             "sfx_fp64_peak")
 
 _ERRORS = {

@@ -174,6 +174,10 @@ int sfx_violations(sfx_runtime* r, uint64_t* n) {
   return guarded(r, [&](sfx::Runtime& rt) { return rt.violations(n); });
 }
 
+int sfx_set_option(sfx_runtime* r, const char* key, int64_t value) {
+  return guarded(r, [&](sfx::Runtime& rt) { return rt.set_option(key ? key : "", value); });
+}
+
 int sfx_host_alloc(uint64_t bytes, int sim, void** out) {
   *out = nullptr;
   if (!bytes) bytes = 1;

@@ -24,6 +24,8 @@
 #include <cstdio>
 #include <cudaTypedefs.h>
 
+#include <unordered_map>
+
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -39,18 +41,28 @@ constexpr int A_STAGE = BM * BK * 8;  // 16 KiB
 constexpr int B_STAGE = BN * BK * 8;  // 16 KiB
 constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 2 * STAGES * 8 + 1024;
 
-struct GemmArgs {
+// One launch covers G independent tile tasks of identical shape (grouped
+// launch): CTA blockIdx.x -> (task, output tile).  Each task carries its own
+// TMA descriptors in the (large, __grid_constant__) parameter block.
+struct alignas(64) GemmOperands {
+  CUtensorMap a, b;
   double* C;
+};
+
+template <int G>
+struct GemmGroup {
+  GemmOperands t[G];
   long long ldc;
   int M, N, K;
-  int tiles_n;
+  int tiles_n, tiles_per_task;
   int lower;
   double alpha, beta;
 };
 
-template <bool TRANS_B>
-__global__ void __launch_bounds__(THREADS, 1)
-    dgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs p) {
+constexpr int GROUP_MAX = 32;
+
+template <bool TRANS_B, int G>
+__global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_constant__ GemmGroup<G> p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -58,17 +70,22 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
   uint64_t* empty = full + STAGES;
 
+  const int task = blockIdx.x / p.tiles_per_task;
+  const int tile = blockIdx.x - task * p.tiles_per_task;
+  const CUtensorMap* tmA = &p.t[task].a;
+  const CUtensorMap* tmB = &p.t[task].b;
+  double* const Cbase = p.t[task].C;
   int bm, bn;
   if (p.lower) {
     // triangular enumeration of lower CTA tiles: idx -> (bm >= bn)
-    int idx = blockIdx.x;
+    int idx = tile;
     bm = static_cast<int>((sqrtf(8.0f * idx + 1.0f) - 1.0f) * 0.5f);
     while ((bm + 1) * (bm + 2) / 2 <= idx) ++bm;
     while (bm * (bm + 1) / 2 > idx) --bm;
     bn = idx - bm * (bm + 1) / 2;
   } else {
-    bm = blockIdx.x / p.tiles_n;
-    bn = blockIdx.x % p.tiles_n;
+    bm = tile / p.tiles_n;
+    bn = tile % p.tiles_n;
   }
   const int m0 = bm * BM, n0 = bn * BN;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -87,19 +104,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---- TMA producer warpgroup (one elected lane) ----
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     if (warp == CONSUMER_WARPS && lane == 0) {
-      ptx::prefetch_tmap(&tmA);
-      ptx::prefetch_tmap(&tmB);
+      ptx::prefetch_tmap(tmA);
+      ptx::prefetch_tmap(tmB);
       for (int kt = 0; kt < ktiles; ++kt) {
         const int s = kt % STAGES;
         if (kt >= STAGES) ptx::mbar_wait(&empty[s], ((kt / STAGES) & 1) ^ 1);
         ptx::mbar_arrive_expect_tx(&full[s], A_STAGE + B_STAGE);
-        ptx::tma_load_2d(sA + s * A_STAGE, &tmA, kt * BK, m0, &full[s]);
+        ptx::tma_load_2d(sA + s * A_STAGE, tmA, kt * BK, m0, &full[s]);
         if (TRANS_B) {
-          ptx::tma_load_2d(sB + s * B_STAGE, &tmB, kt * BK, n0, &full[s]);
+          ptx::tma_load_2d(sB + s * B_STAGE, tmB, kt * BK, n0, &full[s]);
         } else {
 #pragma unroll
           for (int q = 0; q < BN / 16; ++q)
-            ptx::tma_load_2d(sB + s * B_STAGE + q * 2048, &tmB, n0 + 16 * q, kt * BK, &full[s]);
+            ptx::tma_load_2d(sB + s * B_STAGE + q * 2048, tmB, n0 + 16 * q, kt * BK, &full[s]);
         }
       }
     }
@@ -167,7 +184,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   for (int i = 0; i < 8; ++i) {
     const int row = m0 + wm * 64 + 8 * i + g;
     if (row >= p.M) continue;
-    double* crow = p.C + static_cast<long long>(row) * p.ldc;
+    double* crow = Cbase + static_cast<long long>(row) * p.ldc;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int col = n0 + wn * 32 + 8 * j + 2 * t;
@@ -207,8 +224,38 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 
 }  // namespace
 
+namespace {
+struct TmapKey {
+  const void* base;
+  uint64_t inner, outer, ld;
+  uint32_t bi, bo, sw;
+  bool operator==(const TmapKey& o) const {
+    return base == o.base && inner == o.inner && outer == o.outer && ld == o.ld && bi == o.bi && bo == o.bo &&
+           sw == o.sw;
+  }
+};
+struct TmapHash {
+  size_t operator()(const TmapKey& k) const {
+    size_t h = reinterpret_cast<size_t>(k.base) * 0x9E3779B97F4A7C15ull;
+    h ^= (k.inner * 31 + k.outer) * 0xBF58476D1CE4E5B9ull + (k.ld << 7) + (k.bi << 3) + k.bo + k.sw;
+    return h;
+  }
+};
+}  // namespace
+
 bool make_tmap_f64_2d(CUtensorMap* tm, const double* base, uint64_t inner, uint64_t outer, uint64_t ld,
                       uint32_t box_inner, uint32_t box_outer, bool swizzle128) {
+  // Encoding a descriptor is a driver call of a few microseconds; tiles keep
+  // their arena address while resident, so descriptors are cached per thread
+  // (one executor thread per device).  The key holds every encode input, so a
+  // hit is always exact even after the arena slot was reused.
+  thread_local std::unordered_map<TmapKey, CUtensorMap, TmapHash> cache;
+  const TmapKey key{base, inner, outer, ld, box_inner, box_outer, swizzle128 ? 1u : 0u};
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *tm = it->second;
+    return true;
+  }
   auto enc = tmap_encoder();
   if (!enc) return false;
   cuuint64_t dims[2] = {inner, outer};
@@ -219,40 +266,35 @@ bool make_tmap_f64_2d(CUtensorMap* tm, const double* base, uint64_t inner, uint6
                    CU_TENSOR_MAP_INTERLEAVE_NONE,
                    swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  if (r != CUDA_SUCCESS) return false;
+  if (cache.size() > (1u << 16)) cache.clear();
+  cache.emplace(key, *tm);
+  return true;
 }
 
-cudaError_t launch_dgemm(const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc,
-                         int M, int N, int K, double alpha, double beta, bool trans_b, bool lower,
-                         cudaStream_t stream) {
-  if (M <= 0 || N <= 0) return cudaSuccess;
-  if ((lda & 1) || (ldb & 1) || (ldc & 1) || (reinterpret_cast<uintptr_t>(A) & 15) ||
-      (reinterpret_cast<uintptr_t>(B) & 15) || (reinterpret_cast<uintptr_t>(C) & 15))
-    return cudaErrorMisalignedAddress;
-  if (K <= 0) {
-    // C = beta*C: a degenerate update (no contraction), handled by the same epilogue
-    // with alpha = 0 would still need operand loads; reject instead.
-    return cudaErrorInvalidValue;
-  }
-  static bool attr_set[64][2] = {};
+namespace {
+
+template <bool TB, int G>
+cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double alpha, double beta, bool lower,
+                           cudaStream_t stream) {
+  static bool attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!attr_set[dev & 63][trans_b]) {
-    cudaError_t e = trans_b ? cudaFuncSetAttribute(dgemm_dmma_kernel<true>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)
-                            : cudaFuncSetAttribute(dgemm_dmma_kernel<false>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (!attr_set[dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(dgemm_dmma_kernel<TB, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr_set[dev & 63][trans_b] = true;
+    attr_set[dev & 63] = true;
   }
-  CUtensorMap tmA, tmB;
-  if (!make_tmap_f64_2d(&tmA, A, K, M, lda, BK, BM, true)) return cudaErrorInvalidValue;
-  bool ok = trans_b ? make_tmap_f64_2d(&tmB, B, K, N, ldb, BK, BN, true)
-                    : make_tmap_f64_2d(&tmB, B, N, K, ldb, 16, BK, true);
-  if (!ok) return cudaErrorInvalidValue;
-  GemmArgs p;
-  p.C = C;
-  p.ldc = ldc;
+  GemmGroup<G> p;
+  for (int i = 0; i < n; ++i) {
+    if (!make_tmap_f64_2d(&p.t[i].a, d[i].A, K, M, d[i].lda, BK, BM, true)) return cudaErrorInvalidValue;
+    const bool ok = TB ? make_tmap_f64_2d(&p.t[i].b, d[i].B, K, N, d[i].ldb, BK, BN, true)
+                       : make_tmap_f64_2d(&p.t[i].b, d[i].B, N, K, d[i].ldb, 16, BK, true);
+    if (!ok) return cudaErrorInvalidValue;
+    p.t[i].C = d[i].C;
+  }
+  p.ldc = d[0].ldc;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -261,12 +303,42 @@ cudaError_t launch_dgemm(const double* A, long long lda, const double* B, long l
   p.lower = lower ? 1 : 0;
   const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
   p.tiles_n = tn;
-  const int grid = lower ? tm * (tm + 1) / 2 : tm * tn;
-  if (trans_b)
-    dgemm_dmma_kernel<true><<<grid, THREADS, SMEM_BYTES, stream>>>(tmA, tmB, p);
-  else
-    dgemm_dmma_kernel<false><<<grid, THREADS, SMEM_BYTES, stream>>>(tmA, tmB, p);
+  p.tiles_per_task = lower ? tm * (tm + 1) / 2 : tm * tn;
+  dgemm_dmma_kernel<TB, G><<<p.tiles_per_task * n, THREADS, SMEM_BYTES, stream>>>(p);
   return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_dgemm_group(const GemmDesc* d, int n, int M, int N, int K, double alpha, double beta,
+                               bool trans_b, bool lower, cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || n <= 0) return cudaSuccess;
+  if (K <= 0) return cudaErrorInvalidValue;
+  for (int i = 0; i < n; ++i) {
+    if ((d[i].lda & 1) || (d[i].ldb & 1) || (d[i].ldc & 1) || (reinterpret_cast<uintptr_t>(d[i].A) & 15) ||
+        (reinterpret_cast<uintptr_t>(d[i].B) & 15) || (reinterpret_cast<uintptr_t>(d[i].C) & 15) ||
+        d[i].ldc != d[0].ldc)
+      return cudaErrorMisalignedAddress;
+  }
+  for (int i0 = 0; i0 < n; i0 += GROUP_MAX) {
+    const int m = n - i0 < GROUP_MAX ? n - i0 : GROUP_MAX;
+    cudaError_t e;
+    if (m == 1)
+      e = trans_b ? launch_group_t<true, 1>(d + i0, 1, M, N, K, alpha, beta, lower, stream)
+                  : launch_group_t<false, 1>(d + i0, 1, M, N, K, alpha, beta, lower, stream);
+    else
+      e = trans_b ? launch_group_t<true, GROUP_MAX>(d + i0, m, M, N, K, alpha, beta, lower, stream)
+                  : launch_group_t<false, GROUP_MAX>(d + i0, m, M, N, K, alpha, beta, lower, stream);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_dgemm(const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc,
+                         int M, int N, int K, double alpha, double beta, bool trans_b, bool lower,
+                         cudaStream_t stream) {
+  GemmDesc d{A, lda, B, ldb, C, ldc};
+  return launch_dgemm_group(&d, 1, M, N, K, alpha, beta, trans_b, lower, stream);
 }
 
 }  // namespace sfx

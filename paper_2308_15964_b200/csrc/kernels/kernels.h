@@ -9,6 +9,19 @@ namespace sfx {
 bool make_tmap_f64_2d(CUtensorMap* tm, const double* base, uint64_t inner, uint64_t outer, uint64_t ld,
                       uint32_t box_inner, uint32_t box_outer, bool swizzle128);
 
+struct GemmDesc {
+  const double* A;
+  long long lda;
+  const double* B;
+  long long ldb;
+  double* C;
+  long long ldc;
+};
+
+// n independent same-shape GEMMs in grouped launches (up to 32 per launch)
+cudaError_t launch_dgemm_group(const GemmDesc* d, int n, int M, int N, int K, double alpha, double beta,
+                               bool trans_b, bool lower, cudaStream_t stream);
+
 // C = beta*C + alpha*A*op(B); op(B) = B^T ([N x K] storage) if trans_b else B ([K x N]).
 // lower: only row >= col of C is computed/stored (square C).
 cudaError_t launch_dgemm(const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc,

@@ -266,6 +266,37 @@ class CudaBackend : public Backend {
     return cuda_err(e, "kernel launch", err);
   }
 
+  int launch_group(int d, int stream, const std::vector<OpLaunch>& ops, std::string& err) override {
+    const OpLaunch& f = ops[0];
+    if (ops.size() > 1 && (f.op == SFX_OP_DGEMM || f.op == SFX_OP_DSYRK)) {
+      std::vector<GemmDesc> g(ops.size());
+      const bool syrk = f.op == SFX_OP_DSYRK;
+      for (size_t i = 0; i < ops.size(); ++i) {
+        const Operand* o = ops[i].o;
+        if (syrk)
+          g[i] = GemmDesc{static_cast<const double*>(o[0].dptr), o[0].ld, static_cast<const double*>(o[0].dptr),
+                          o[0].ld, static_cast<double*>(o[1].dptr), o[1].ld};
+        else
+          g[i] = GemmDesc{static_cast<const double*>(o[0].dptr), o[0].ld, static_cast<const double*>(o[1].dptr),
+                          o[1].ld, static_cast<double*>(o[2].dptr), o[2].ld};
+      }
+      const Operand* o = f.o;
+      cudaError_t e =
+          syrk ? launch_dgemm_group(g.data(), static_cast<int>(g.size()), static_cast<int>(o[1].rows),
+                                    static_cast<int>(o[1].rows), static_cast<int>(o[0].cols), f.fp[0], f.fp[1], true,
+                                    true, devs_[d]->streams[stream])
+               : launch_dgemm_group(g.data(), static_cast<int>(g.size()), static_cast<int>(o[2].rows),
+                                    static_cast<int>(o[2].cols), static_cast<int>(o[0].cols), f.fp[0], f.fp[1],
+                                    f.ip[0] != 0, false, devs_[d]->streams[stream]);
+      return cuda_err(e, "grouped dgemm launch", err);
+    }
+    for (const OpLaunch& op : ops) {
+      int rc = launch(d, stream, op, err);
+      if (rc) return rc;
+    }
+    return SFX_OK;
+  }
+
   void shutdown() override {
     if (shut_) return;
     for (Dev* dp : devs_) {

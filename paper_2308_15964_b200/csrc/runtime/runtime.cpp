@@ -34,6 +34,18 @@ void DevQueue::push(Task* t) {
   }
 }
 
+void DevQueue::push_front(Task* t) {
+  if (!prio)
+    fifo.push_front(t);
+  else
+    push(t);  // heap order is (priority, seq): re-pushing restores its place
+}
+
+Task* DevQueue::peek() const {
+  if (!prio) return fifo.empty() ? nullptr : fifo.front();
+  return heap.empty() ? nullptr : heap.front();
+}
+
 Task* DevQueue::pop() {
   if (!prio) {
     if (fifo.empty()) return nullptr;
@@ -65,7 +77,7 @@ Runtime::Runtime(Backend* be, int ndev, int nstreams, uint32_t sched, uint32_t f
       nstreams_(nstreams),
       sched_(sched),
       flags_(flags),
-      window_(window ? window : 4u * static_cast<uint32_t>(nstreams)),
+      window_(window ? window : 4u * static_cast<uint32_t>(nstreams) + 64u),
       align_(align),
       trace_((flags & SFX_FLAG_TRACE) != 0) {
   paused_ = (flags & SFX_FLAG_PAUSED) != 0;
@@ -713,7 +725,8 @@ int Runtime::ensure_block(int d, int s, Handle* h, std::vector<Action>& acts, st
 
 // ------------------------------------------------------------- execution
 
-int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op, std::string& err) {
+int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op, std::string& err,
+                  bool record_start) {
   Device& D = *devs_[d];
   auto wait_on = [&](const SyncP& p) {
     if (!p || p->complete) return;
@@ -744,7 +757,7 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
   for (const SyncP& w : t->waits) wait_on(w);
   for (auto& a : t->acc)
     if (a.mode == SFX_COMMUTATIVE_WRITE) wait_on(a.h->commute_last);
-  if (t->start) acts.push_back(Action{Action::RECORD, t->start});
+  if (t->start && record_start) acts.push_back(Action{Action::RECORD, t->start});
 
   if (t->op == SFX_OP_FLUSH) {
     // graph.py:258-260 + device.py:318-326: fetch the dirty copy home; a
@@ -869,7 +882,8 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
   return 0;
 }
 
-int Runtime::issue(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op, std::string& err) {
+int Runtime::issue(int d, int s, const std::vector<Task*>& group, std::vector<Action>& acts,
+                   std::vector<OpLaunch>& ops, std::string& err) {
   int rc = 0;
   for (Action& a : acts) {
     switch (a.kind) {
@@ -896,15 +910,61 @@ int Runtime::issue(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& o
     }
     if (rc) return rc;
   }
-  if (!t) return 0;
-  if (op.op != SFX_OP_FLUSH && op.op != SFX_OP_NOOP) {
-    rc = be_->launch(d, s, op, err);
+  if (group.empty()) return 0;
+  std::vector<OpLaunch> kern;
+  kern.reserve(ops.size());
+  for (auto& op : ops)
+    if (op.op != SFX_OP_FLUSH && op.op != SFX_OP_NOOP) kern.push_back(op);
+  if (!kern.empty()) {
+    rc = be_->launch_group(d, s, kern, err);
     if (rc) return rc;
-    devs_[d]->stats.kernel_launches += 1;
+    devs_[d]->stats.kernel_launches += kern.size();
   }
-  rc = be_->event_record(d, s, t->end->event, err);
-  t->end->recorded.store(true, std::memory_order_release);
+  SyncP end = group[0]->end;
+  rc = be_->event_record(d, s, end->event, err);
+  end->recorded.store(true, std::memory_order_release);
   return rc;
+}
+
+bool Runtime::groupable(const Task* t) const {
+  // only ops with a grouped kernel (one launch for the whole group) or trivial
+  // generators: grouping anything else would serialise independent tasks on one stream
+  switch (t->op) {
+    case SFX_OP_DGEMM:
+    case SFX_OP_DSYRK:
+    case SFX_OP_FILL_UNIFORM:
+    case SFX_OP_FILL_SPD:
+    case SFX_OP_FILL_PARTICLES:
+    case SFX_OP_ZERO:
+      return group_max_ > 1;
+    default:
+      return false;
+  }
+}
+
+bool Runtime::same_signature(const Task* a, const Task* b) const {
+  if (a->op != b->op || a->acc.size() != b->acc.size()) return false;
+  for (int k = 0; k < 4; ++k)
+    if (a->fp[k] != b->fp[k] || (a->op == SFX_OP_DGEMM && a->ip[k] != b->ip[k])) return false;
+  for (size_t k = 0; k < a->acc.size(); ++k) {
+    const Handle* x = a->acc[k].h;
+    const Handle* y = b->acc[k].h;
+    if (x->rows != y->rows || x->cols != y->cols || x->ld != y->ld || x->dtype != y->dtype ||
+        a->acc[k].mode != b->acc[k].mode)
+      return false;
+  }
+  return true;
+}
+
+bool Runtime::commute_conflict(const std::vector<Task*>& group, const Task* t) const {
+  // members of one commutative group must never run concurrently on the same handle
+  for (const Access& a : t->acc) {
+    if (a.mode != SFX_COMMUTATIVE_WRITE) continue;
+    for (const Task* g : group)
+      for (const Access& b : g->acc)
+        if (b.h == a.h) return true;
+  }
+  return false;
 }
 
 void Runtime::complete(Task* t) {
@@ -958,34 +1018,81 @@ void Runtime::exec_loop(int d) {
   be_->bind_thread(d);
   Device& D = *devs_[d];
   std::unique_lock<std::mutex> lk(mu_);
+  std::vector<Task*> group;
+  std::vector<Action> acts;
+  std::vector<OpLaunch> ops;
   while (true) {
     D.exec_cv.wait(lk, [&] {
       return stopping_ || (!paused_ && !fail_code_ && D.queue.size() > 0 && D.ninflight < static_cast<int>(window_));
     });
     if (stopping_) return;
-    Task* t = D.queue.pop();
-    t->state = SFX_STATE_EXECUTING;
+    const int64_t t_busy0 = now_ns();
+    // pop the head task, plus (grouped launch) the following ready tasks of the
+    // same op and operand shapes -- up to group_max_, never two commutative
+    // members of one handle
+    group.clear();
+    Task* first = D.queue.pop();
+    group.push_back(first);
+    if (groupable(first)) {
+      while (group.size() < group_max_ && D.queue.size() > 0 &&
+             D.ninflight + static_cast<int>(group.size()) < static_cast<int>(window_)) {
+        Task* nx = D.queue.peek();
+        if (!same_signature(first, nx) || commute_conflict(group, nx)) break;
+        group.push_back(D.queue.pop());
+      }
+    }
     int s = 0;
     for (int k = 1; k < nstreams_; ++k)
       if (D.stream_inflight[k] < D.stream_inflight[s]) s = k;
-    t->stream = s;
-    t->t_pop = now_ns();
-    record(graphs_[t->gid].get(), SFX_EV_POP, t->t_pop, d * nstreams_ + s, t->tid);
-    std::vector<Action> acts;
-    OpLaunch op;
+    SyncP gend = new_sync(d, s, trace_);
+    SyncP gstart = trace_ ? new_sync(d, s, true) : nullptr;
+    const int64_t tpop = now_ns();
+    for (Task* t : group) {
+      t->state = SFX_STATE_EXECUTING;
+      t->stream = s;
+      t->t_pop = tpop;
+      t->end = gend;
+      t->start = gstart;
+      record(graphs_[t->gid].get(), SFX_EV_POP, tpop, d * nstreams_ + s, t->tid);
+    }
+    acts.clear();
+    ops.assign(group.size(), OpLaunch());
     std::string err;
-    int rc;
-    while (true) {
-      acts.clear();
-      rc = plan(d, s, t, acts, op, err);
+    int rc = 0;
+    size_t planned = 0;
+    while (planned < group.size()) {
+      const size_t mark = acts.size();
+      rc = plan(d, s, group[planned], acts, ops[planned], err, false);
+      if (rc == 0) {
+        ++planned;
+        continue;
+      }
       if (rc != 1) break;
-      // every evictable block is pinned by in-flight work: issue the write-backs
-      // planned so far, then wait for a completion anywhere and re-plan
+      if (planned > 0) {
+        // resources exhausted mid-group: launch what is planned, requeue the rest
+        (void)mark;
+        for (size_t k = group.size(); k-- > planned;) {
+          Task* t = group[k];
+          t->end.reset();
+          t->start.reset();
+          t->state = SFX_STATE_READY;
+          D.queue.push_front(t);
+        }
+        group.resize(planned);
+        ops.resize(planned);
+        rc = 0;
+        break;
+      }
+      // nothing planned yet: issue the write-backs planned so far, then wait for
+      // any completion and re-plan
       if (!acts.empty()) {
         lk.unlock();
         std::string e2;
-        int r2 = issue(d, s, nullptr, acts, op, e2);
+        std::vector<Task*> none;
+        std::vector<OpLaunch> noops;
+        int r2 = issue(d, s, none, acts, noops, e2);
         lk.lock();
+        acts.clear();
         if (r2) {
           rc = SFX_ERR_CUDA;
           err = e2;
@@ -1009,23 +1116,44 @@ void Runtime::exec_loop(int d) {
       poison(rc, err);
       continue;
     }
-    D.ninflight += 1;
-    D.stream_inflight[s] += 1;
+    {
+      // every stream wait first, then the group's start stamp, then copies:
+      // waiting earlier is always safe and keeps start >= every predecessor's end
+      std::vector<Action> ordered;
+      ordered.reserve(acts.size() + 1);
+      for (auto& a : acts)
+        if (a.kind == Action::WAIT) ordered.push_back(a);
+      if (gstart) ordered.push_back(Action{Action::RECORD, gstart});
+      for (auto& a : acts)
+        if (a.kind != Action::WAIT) ordered.push_back(a);
+      acts.swap(ordered);
+    }
+    D.ninflight += static_cast<int>(group.size());
+    D.stream_inflight[s] += static_cast<int>(group.size());
+    const int64_t t_plan1 = now_ns();
+    D.stats.t_plan_ns += t_plan1 - t_busy0;
     lk.unlock();
-    rc = issue(d, s, t, acts, op, err);
+    rc = issue(d, s, group, acts, ops, err);
+    const int64_t t_issue1 = now_ns();
+    D.stats.t_issue_ns += t_issue1 - t_plan1;
+    D.stats.groups += 1;
     lk.lock();
     if (rc) {
       poison(SFX_ERR_CUDA, err);
       continue;
     }
+    const int64_t t_rel0 = now_ns();
     if (be_->is_sim()) {
-      complete(t);  // synchronous device: stage_out + task_end before release
-      release(t);
+      for (Task* t : group) {
+        complete(t);  // synchronous device: stage_out + task_end before release
+        release(t);
+      }
     } else {
-      release(t);
-      D.inflight.push_back(t);
+      for (Task* t : group) release(t);
+      for (Task* t : group) D.inflight.push_back(t);
       D.comp_cv.notify_one();
     }
+    D.stats.t_release_ns += now_ns() - t_rel0;
   }
 }
 
@@ -1046,9 +1174,11 @@ void Runtime::comp_loop(int d) {
     std::string err;
     int rc = be_->event_sync(d, ev, err);
     lk.lock();
+    const int64_t tc0 = now_ns();
     D.inflight.pop_front();
     if (rc) poison(SFX_ERR_CUDA, err);
     complete(t);
+    D.stats.t_complete_ns += now_ns() - tc0;
   }
 }
 
@@ -1211,6 +1341,20 @@ int Runtime::violations(uint64_t* n) {
         }
   }
   *n = bad;
+  return SFX_OK;
+}
+
+int Runtime::set_option(const std::string& key, int64_t value) {
+  std::unique_lock<std::mutex> lk(mu_);
+  if (key == "group_max") {
+    group_max_ = static_cast<uint32_t>(std::max<int64_t>(1, std::min<int64_t>(value, 1024)));
+  } else if (key == "window") {
+    window_ = static_cast<uint32_t>(std::max<int64_t>(1, value));
+    for (auto& d : devs_) d->exec_cv.notify_all();
+  } else {
+    last_error = "unknown option " + key;
+    return SFX_ERR_CONFIG;
+  }
   return SFX_OK;
 }
 

@@ -172,6 +172,14 @@ class Backend {
   virtual int copy_p2p(int d, int stream, uint64_t dst_off, int src_dev, uint64_t src_off, uint64_t n,
                        std::string& err) = 0;
   virtual int launch(int d, int stream, const OpLaunch& op, std::string& err) = 0;
+  // several independent ready tasks on one stream (grouped kernels where available)
+  virtual int launch_group(int d, int stream, const std::vector<OpLaunch>& ops, std::string& err) {
+    for (const OpLaunch& op : ops) {
+      int rc = launch(d, stream, op, err);
+      if (rc) return rc;
+    }
+    return 0;
+  }
   virtual bool supports(uint32_t op) const = 0;
   virtual void shutdown() = 0;
 };
@@ -195,7 +203,9 @@ struct DevQueue {
   std::vector<Task*> heap;
   size_t size() const { return prio ? heap.size() : fifo.size(); }
   void push(Task* t);
+  void push_front(Task* t);
   Task* pop();
+  Task* peek() const;
 };
 
 struct Device {
@@ -237,6 +247,7 @@ class Runtime {
   int edges(uint32_t gid, uint64_t* src, uint64_t* dst, uint64_t* hid, uint64_t cap, uint64_t* n);
   int violations(uint64_t* n);
   int failure(int* code, char* msg, uint64_t cap);
+  int set_option(const std::string& key, int64_t value);
 
   std::string last_error;
 
@@ -247,7 +258,10 @@ class Runtime {
   int place(Task* t);
   void release(Task* t);
   void advance(Handle* h);
-  int plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op, std::string& err);
+  int plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op, std::string& err, bool record_start);
+  bool groupable(const Task* t) const;
+  bool same_signature(const Task* a, const Task* b) const;
+  bool commute_conflict(const std::vector<Task*>& group, const Task* t) const;
   int ensure_block(int d, int s, Handle* h, std::vector<Action>& acts, std::vector<Block*>& tmp_pins, Block** out,
                    std::string& err);
   int evict_one(int d, int s, std::vector<Action>& acts, std::string& err);
@@ -255,7 +269,8 @@ class Runtime {
   void free_space(int d, uint64_t off, uint64_t size);
   bool alloc_space(int d, uint64_t size, uint64_t* off);
   SyncP new_sync(int d, int s, bool timing);
-  int issue(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op, std::string& err);
+  int issue(int d, int s, const std::vector<Task*>& group, std::vector<Action>& acts, std::vector<OpLaunch>& ops,
+            std::string& err);
   void complete(Task* t);
   void poison(int code, const std::string& msg);
   void record(Graph* g, int kind, int64_t t, int wid, uint64_t tid, int64_t extra = 0);
@@ -265,6 +280,7 @@ class Runtime {
   Backend* be_;
   int ndev_, nstreams_;
   uint32_t sched_, flags_, window_;
+  uint32_t group_max_ = 32;
   uint64_t align_;
   bool trace_;
   std::mutex mu_;

@@ -71,7 +71,8 @@ class ComputeEngine:
     """A native runtime over the team's devices, serving any number of graphs."""
 
     def __init__(self, team, scheduler=None, device_memory=None, *, backend: str = "cuda",
-                 trace: bool = True, window: int = 0, ordinals=None, arena_align: int = 0):
+                 trace: bool = True, window: int = 0, ordinals=None, arena_align: int = 0,
+                 group_max: int = 32):
         if isinstance(team, (list, tuple)):
             team = WorkerTeam(team)
         devices = team.device_indexes()
@@ -113,6 +114,7 @@ class ComputeEngine:
         N.check(N.lib.sfx_create(self.ndev, ords, self.streams_per_device, arenas, self.policy,
                                  flags, int(window), ctypes.byref(handle)))
         self._h = handle
+        self.set_option("group_max", group_max)
         self.graphs = []
         self._stopped = False
 
@@ -124,6 +126,10 @@ class ComputeEngine:
         return {DEVICE}
 
     # -- control --------------------------------------------------------------
+    def set_option(self, key: str, value: int) -> None:
+        """Runtime knobs: ``group_max`` (grouped launches), ``window`` (in-flight tasks)."""
+        N.check(N.lib.sfx_set_option(self._h, key.encode(), int(value)), self._h)
+
     def pause(self) -> None:
         """Hold the executors (the gate task of the reference's gated insertion)."""
         N.check(N.lib.sfx_pause(self._h), self._h)

@@ -1,0 +1,400 @@
+"""The native runtime's bookkeeping on the simulated backend (no GPU).
+
+The same libsfx.so that drives the B200s runs here against host-memory
+devices (the reference's own simulated-device design), so its
+dependency core, scheduler order, LRU arena and coherency are checked against
+the golden fixtures produced by the real reference.  Only runtime test ops
+execute in sim mode; tile ops are refused (test_native_abi.py).
+"""
+
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+import paper_2308_15964_b200 as sf
+from oracle import programs
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+MODE = {"read": sf.read, "write": sf.write, "atomic": sf.atomic_write, "commute": sf.commutative_write,
+        "maybe": sf.maybe_write}
+
+
+def sim_engine(devices=1, streams=1, sched=None, **kw):
+    return sf.create_engine(sf.WorkerTeam.of_devices(devices, streams), scheduler=sched, backend="sim", **kw)
+
+
+def insert_program(g, prog):
+    cells = [sf.Cell(i + 1) for i in range(prog["n_cells"])]
+    tids = []
+    for mode, target, reads, a, b in prog["tasks"]:
+        acc = [MODE[mode](cells[target])] + [sf.read(cells[r]) for r in reads]
+        tids.append(g.task(*acc, device=sf.ops.cell(mode, a, b)).task_id)
+    return cells, tids
+
+
+def pop_indices(g, tids):
+    index = {t: i for i, t in enumerate(tids)}
+    return [index[e[3]] for e in g.trace.export_events() if e[0] == "Pop" and e[3] in index]
+
+
+def edge_indices(g, tids):
+    index = {t: i for i, t in enumerate(tids)}
+    return sorted({(index[s], index[d]) for s, d, _ in g.edges() if s in index and d in index})
+
+
+@pytest.fixture(scope="module")
+def random_programs():
+    with open(os.path.join(GOLD, "random_programs.json")) as fh:
+        return json.load(fh)
+
+
+def test_random_programs_gated_match_reference(random_programs):
+    eng = sim_engine()
+    try:
+        for p in random_programs:
+            g = sf.TaskGraph().compute_on(eng)
+            with g.gated():
+                cells, tids = insert_program(g, p)
+            for c in cells:
+                g.flush_to_host(c)
+            assert g.wait_all(timeout=30)
+            assert [c.value for c in cells] == p["sequential"]
+            assert edge_indices(g, tids) == sorted(tuple(e) for e in p["edges"])
+            assert pop_indices(g, tids) == p["pop_order"]
+    finally:
+        eng.stop()
+
+
+@pytest.mark.parametrize("devices,streams", [(1, 2), (1, 8), (2, 1), (4, 2)])
+def test_random_programs_serial_equivalence(random_programs, devices, streams):
+    eng = sim_engine(devices, streams)
+    try:
+        for p in random_programs:
+            g = sf.TaskGraph().compute_on(eng)
+            cells, _ = insert_program(g, p)
+            for c in cells:
+                g.flush_to_host(c)
+            assert g.wait_all(timeout=30)
+            assert [c.value for c in cells] == p["sequential"]
+    finally:
+        eng.stop()
+
+
+@pytest.mark.parametrize("name,prog", [
+    ("gemm_nt8", programs.gemm_program(8)),
+    ("cholesky_nt8", programs.cholesky_program(8)),
+    ("cholesky_nt32", programs.cholesky_program(32)),
+    ("particles_g16", programs.particles_program(16)),
+])
+def test_tile_graphs_gated_match_reference(name, prog):
+    gold = np.load(os.path.join(GOLD, "tile_graphs.npz"))
+    eng = sim_engine()
+    try:
+        g = sf.TaskGraph().compute_on(eng)
+        objs = {}
+        tids = []
+        with g.gated():
+            for kind, acc, _ in prog:
+                specs = []
+                for mode, key in acc:
+                    if key not in objs:
+                        objs[key] = np.zeros(1)
+                    specs.append({"read": sf.read, "write": sf.write,
+                                  "commutative_write": sf.commutative_write}[mode](objs[key]))
+                tids.append(g.task(*specs, device=sf.ops.noop, name=kind).task_id)
+        assert g.wait_all(timeout=60)
+        assert edge_indices(g, tids) == sorted(map(tuple, gold[f"{name}_edges"].tolist()))
+        assert pop_indices(g, tids) == gold[f"{name}_pop"].tolist()
+    finally:
+        eng.stop()
+
+
+def test_lru_matches_reference_arena():
+    with open(os.path.join(GOLD, "lru.json")) as fh:
+        cases = json.load(fh)
+    for c in cases[:120]:
+        eng = sim_engine(device_memory=c["capacity"], arena_align=8)
+        try:
+            g = sf.TaskGraph().compute_on(eng)
+            bufs = [bytearray([h % 256] * c["size"]) for h in range(12)]
+            hid = {}
+            for h, b in enumerate(bufs):
+                hid[g.register(b)] = h
+            for h, want in zip(c["seq"], c["resident"]):
+                g.task(sf.read(bufs[h]), device=sf.ops.noop)
+                assert g.wait_all(timeout=10)
+                assert sorted(hid[x] for x in eng.resident(0)) == want
+        finally:
+            eng.stop()
+
+
+def test_restaging_unmodified_data_moves_nothing():
+    # reference tests/test_device.py:161-177 and criterion 5
+    eng = sim_engine()
+    try:
+        g = sf.TaskGraph().compute_on(eng)
+        buf = bytearray(range(64))
+        g.task(sf.read(buf), device=sf.ops.noop)
+        g.wait_all(timeout=10)
+        assert eng.stats(0)["bytes_to_device"] == 64
+        g.task(sf.read(buf), device=sf.ops.noop)
+        g.wait_all(timeout=10)
+        assert eng.stats(0)["bytes_to_device"] == 64
+        assert eng.stats(0)["hits"] == 1
+    finally:
+        eng.stop()
+
+
+def test_host_coherency_round_trip():
+    # reference tests/test_device.py:180-207 (host reads go through an explicit flush)
+    eng = sim_engine()
+    try:
+        g = sf.TaskGraph().compute_on(eng)
+        buf = bytearray(16)
+        g.task(sf.write(buf), device=sf.ops.bytes_add(0, 16, 7))
+        g.wait_all(timeout=10)
+        hid = g.hid_of(buf)
+        st = eng.block_state(hid, 0)
+        assert st["dirty"] and not st["host_valid"]
+        assert buf == bytearray(16)  # host copy is stale until flushed
+        g.flush_to_host(buf)
+        g.wait_all(timeout=10)
+        assert buf == bytearray([7] * 16)
+        assert not eng.block_state(hid, 0)["present"]  # host write drops device copies
+        before = eng.stats(0)["bytes_to_device"]
+        g.task(sf.write(buf), device=sf.ops.bytes_add(0, 1, 1))
+        g.flush_to_host(buf, keep_device=True)
+        g.wait_all(timeout=10)
+        assert buf[0] == 8
+        assert eng.stats(0)["bytes_to_device"] == before + 16
+        st = eng.block_state(hid, 0)
+        assert st["valid"] and not st["dirty"] and st["host_valid"]
+    finally:
+        eng.stop()
+
+
+def _random_byte_program(rng):
+    # reference tests/test_acceptance.py:225-236
+    bufs = [bytearray(rng.randrange(256) for _ in range(rng.choice((16, 24, 32)))) for _ in range(rng.randint(2, 4))]
+    ops = []
+    for _ in range(rng.randint(4, 12)):
+        b = rng.randrange(len(bufs))
+        size = len(bufs[b])
+        off = rng.randrange(size)
+        length = rng.randint(1, size - off)
+        ops.append((b, off, length, rng.randint(1, 255)))
+    return bufs, ops
+
+
+def test_tiny_arena_round_trips_match_host_execution():
+    # criterion 5: 100 random byte programs through a 64-byte arena (forced eviction)
+    rng = random.Random(5)
+    eng = sim_engine(device_memory=64, arena_align=8)
+    try:
+        for _ in range(100):
+            bufs, ops = _random_byte_program(rng)
+            expected = [bytearray(b) for b in bufs]
+            for b, off, length, delta in ops:
+                for i in range(off, off + length):
+                    expected[b][i] = (expected[b][i] + delta) % 256
+            g = sf.TaskGraph().compute_on(eng)
+            for b, off, length, delta in ops:
+                g.task(sf.write(bufs[b]), device=sf.ops.bytes_add(off, length, delta))
+            for b in bufs:
+                g.flush_to_host(b)
+            assert g.wait_all(timeout=30)
+            assert bufs == expected
+        assert eng.stats(0)["evictions"] > 0
+    finally:
+        eng.stop()
+
+
+def test_pinned_exhaustion_poisons_cleanly():
+    # reference tests/test_device.py:255-263
+    eng = sim_engine(device_memory=64, arena_align=8)
+    try:
+        g = sf.TaskGraph().compute_on(eng)
+        a, b = bytearray(48), bytearray(48)
+        g.task(sf.read(a), sf.read(b), device=sf.ops.noop)
+        with pytest.raises(sf.EngineFailedError) as info:
+            g.wait_all(timeout=10)
+        assert isinstance(info.value.__cause__, sf.StagingError)
+        assert "pinned" in str(info.value.__cause__)
+    finally:
+        eng.stop()
+
+
+def test_oversized_object_rejected():
+    eng = sim_engine(device_memory=16, arena_align=8)
+    try:
+        g = sf.TaskGraph().compute_on(eng)
+        g.task(sf.read(bytearray(32)), device=sf.ops.noop)
+        with pytest.raises(sf.EngineFailedError) as info:
+            g.wait_all(timeout=10)
+        assert isinstance(info.value.__cause__, sf.StagingError)
+        assert "exceeds" in str(info.value.__cause__)
+    finally:
+        eng.stop()
+
+
+def test_cross_device_reads_pull_peer_to_peer():
+    """Deliberate divergence from reference tests/test_device.py:210-236: the
+    freshest copy moves device -> device (NVLink) and the host stays stale."""
+    eng = sim_engine(devices=2)
+    try:
+        g = sf.TaskGraph().compute_on(eng)
+        buf = bytearray(32)
+        g.task(sf.write(buf), device=sf.ops.bytes_add(0, 4, 9), priority=0)
+        g.wait_all(timeout=10)
+        hid = g.hid_of(buf)
+        owner = 0 if eng.block_state(hid, 0)["dirty"] else 1
+        other = 1 - owner
+        # force the reader onto the other device
+        g._submit_one(9_000_000_001, sf.ops.noop, 0, [hid], [0], dev_hint=other)
+        g.wait_all(timeout=10)
+        assert eng.stats(other)["bytes_p2p_in"] == 32
+        assert eng.stats(other)["bytes_to_device"] == 0
+        assert eng.block_state(hid, owner)["dirty"]          # owner keeps the single dirty copy
+        assert eng.block_state(hid, other)["valid"]
+        assert not eng.block_state(hid, owner)["host_valid"]  # host not touched
+        # a writer on `other` invalidates the owner's copy
+        g._submit_one(9_000_000_002, sf.ops.bytes_add(0, 1, 1), 0, [hid], [1], dev_hint=other)
+        g.wait_all(timeout=10)
+        assert not eng.block_state(hid, owner)["present"]
+        assert eng.block_state(hid, other)["dirty"]
+        g.flush_to_host(buf)
+        g.wait_all(timeout=10)
+        assert buf[:4] == bytearray([10, 9, 9, 9])
+    finally:
+        eng.stop()
+
+
+def test_priority_scheduler_pops_in_priority_order():
+    rng = random.Random(99)
+    eng = sim_engine(sched="prio")
+    try:
+        for _ in range(30):
+            g = sf.TaskGraph().compute_on(eng)
+            prios = [rng.randint(-50, 50) for _ in range(rng.randint(2, 30))]
+            tids = []
+            with g.gated():
+                for p in prios:
+                    tids.append(g.task(sf.write(sf.Cell(0)), device=sf.ops.noop, priority=p).task_id)
+            assert g.wait_all(timeout=10)
+            order = pop_indices(g, tids)
+            popped = [prios[i] for i in order]
+            assert all(a >= b for a, b in zip(popped, popped[1:]))
+            # FIFO among equal priorities (scheduler.py:111)
+            for a, b in zip(order, order[1:]):
+                if prios[a] == prios[b]:
+                    assert a < b
+    finally:
+        eng.stop()
+
+
+def test_wait_all_timeout_and_resume():
+    eng = sim_engine()
+    try:
+        g = sf.TaskGraph().compute_on(eng)
+        eng.pause()
+        c = sf.Cell(1)
+        g.task(sf.write(c), device=sf.ops.cell("write", 2, 0))
+        assert g.wait_all(timeout=0.2) is False
+        eng.resume()
+        assert g.wait_all(timeout=10) is True
+    finally:
+        eng.stop()
+
+
+def test_insertion_errors_match_reference():
+    eng = sim_engine()
+    try:
+        g = sf.TaskGraph()
+        with pytest.raises(sf.ConfigurationError):
+            g.task(sf.write(sf.Cell(0)), device=sf.ops.noop)  # not attached
+        g.compute_on(eng)
+        with pytest.raises(sf.ConfigurationError):
+            g.compute_on(eng)
+        c = sf.Cell(0)
+        with pytest.raises(sf.DuplicateAccessError):
+            g.task(sf.read(c), sf.write(c), device=sf.ops.noop)
+        with pytest.raises(sf.ConfigurationError, match="oracle"):
+            g.task(sf.write(c), host=lambda x: None)
+        with pytest.raises(sf.ConfigurationError):
+            g.task(sf.write(c), device=lambda v: None)
+        with pytest.raises(sf.ConfigurationError):
+            g.task(sf.write(c))
+        with pytest.raises(sf.ConfigurationError):
+            g.task("not an access", device=sf.ops.noop)
+        with pytest.raises(sf.SpeculationError):
+            sf.TaskGraph(speculation=True)
+        assert g.wait_all(timeout=5)
+    finally:
+        eng.stop()
+
+
+def test_dot_dialect_matches_reference_parser():
+    # reference tests/conftest.py:206-226
+    import re
+
+    node = re.compile(r"^  t(\d+) \[(.*)\];$")
+    edge = re.compile(r"^  t(\d+) -> t(\d+)(?: \[label=(.*)\])?;$")
+    eng = sim_engine()
+    try:
+        g = sf.TaskGraph().compute_on(eng)
+        a, b = sf.Cell(1), sf.Cell(2)
+        t1 = g.task(sf.write(a), device=sf.ops.noop, name='first "q"')
+        t2 = g.task(sf.read(a), sf.write(b), device=sf.ops.noop)
+        g.wait_all(timeout=5)
+        for show in (False, True):
+            lines = g.generate_dot(show_deps=show).strip().splitlines()
+            assert lines[0] == "digraph taskgraph {" and lines[-1] == "}"
+            edges = []
+            for line in lines[1:-1]:
+                if node.match(line):
+                    continue
+                m = edge.match(line)
+                assert m, line
+                edges.append((int(m.group(1)), int(m.group(2))))
+            assert edges == [(t1.task_id, t2.task_id)]
+    finally:
+        eng.stop()
+
+
+def test_trace_has_four_events_per_task_and_push_precedes_pop():
+    # reference tests/test_trace.py:116-139
+    eng = sim_engine(streams=2)
+    try:
+        g = sf.TaskGraph().compute_on(eng)
+        cells = [sf.Cell(i) for i in range(4)]
+        for i in range(40):
+            g.task(sf.write(cells[i % 4]), sf.read(cells[(i + 1) % 4]), device=sf.ops.noop)
+        g.wait_all(timeout=10)
+        ev = g.trace.export_events()
+        per = {}
+        for kind, t, wid, tid, _ in ev:
+            per.setdefault(tid, {})[kind] = t
+        assert len(per) == 40
+        for tid, kinds in per.items():
+            assert set(kinds) == {"Push", "Pop", "TaskStart", "TaskEnd"}
+            assert kinds["Push"] <= kinds["Pop"] <= kinds["TaskStart"] <= kinds["TaskEnd"]
+        svg = g.generate_trace_svg()
+        assert svg.startswith("<svg")
+        assert eng.violations() == 0
+    finally:
+        eng.stop()
+
+
+def test_cell_semantics():
+    c = sf.Cell(3)
+    assert c.value == 3 and c == sf.Cell(3) and c != sf.Cell(3.0)
+    f = sf.Cell(1.5)
+    f.value = 2.5
+    assert f.value == 2.5
+    with pytest.raises(TypeError):
+        f.value = 1
+    b = sf.Cell(True)
+    assert b.value is True
