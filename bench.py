@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""Benchmark of the STF GPU execution path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (one process per GPU)
+
+Workload at N=1 (BASELINE.json configs[1]): tiled DGEMM 16384 x 16384 FP64
+with 512 x 512 tiles ("1024 tiles") -> 32,768 GEMM tasks per step, inserted
+through the drop-in TaskGraph API and executed by the native runtime.  A step
+is one full tiled C += A B pass; inputs (3 x 2 GiB) are far larger than the
+126 MB L2, so no flush is needed between steps.  With N ranks every rank runs
+its own C2 instance on its GPU (weak scaling, no data-path collective: the
+DGEMM configs are 1 GPU per config).
+
+Legs of the JSON line:
+  value      device-resident inputs, FP64 GFLOP/s summed over ranks (CUDA
+             events on the device, max step time over ranks)
+  e2e        same metric through the public API from pinned HOST buffers: every
+             step stages A, B, C host->device on demand and flushes C back
+  roofline   FP64 DMMA pipe: achieved TFLOP/s of the DGEMM kernel over the timed
+             region vs the DMMA peak measured in-run on this GPU
+  cpu_baseline  the reference algorithm on the host cores (oracle restatement of
+             the reference STF engine + numpy bodies; rank 0, N=1), bounded sample
+  secondary  Cholesky 32768/1024 (C3) and particles 2^20/256 groups (C4) on one
+             GPU, and the runtime overhead in us/task (reference protocol)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 GFLOP/s tiled Cholesky/GEMM at 1/2/4/8 B200 (% FP64 peak); µs/task"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--b", type=int, default=512)
+    ap.add_argument("--streams", type=int, default=16)
+    ap.add_argument("--group", type=int, default=32)
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- distributed
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self, backend="nccl"):
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def done(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ----------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._th = threading.Thread(target=run, daemon=True)
+        self._th.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=10)
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            for name, v in zip(names, s[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- CPU leg
+
+def cpu_baseline(n: int, b: int, seconds: float):
+    """Reference algorithm on the host: the oracle's restatement of the reference
+    STF engine (one worker thread per core) running numpy tile bodies, on the
+    first block-rows of the same tiled DGEMM (bounded sample)."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+
+    from oracle import bodies, stf
+
+    cores = os.cpu_count() or 1
+    nt = n // b
+    rng = np.random.default_rng(1)
+    A = [[rng.random((b, b)) for _ in range(nt)] for _ in range(2)]
+    B = [[rng.random((b, b)) for _ in range(nt)] for _ in range(nt)]
+
+    def run_rows(rows):
+        C = [[np.zeros((b, b)) for _ in range(nt)] for _ in range(rows)]
+        orc = stf.Oracle(workers=cores, trace=False)
+        t0 = time.perf_counter()
+        for i in range(rows):
+            for j in range(nt):
+                for k in range(nt):
+                    orc.task([(stf.READ, A[i % 2][k]), (stf.READ, B[k][j]), (stf.WRITE, C[i][j])],
+                             body=bodies.gemm_nn)
+        orc.wait_all()
+        dt = time.perf_counter() - t0
+        orc.stop()
+        return dt
+
+    with threadpool_limits(1):
+        t1 = run_rows(1)
+        rows = max(1, min(nt, int(seconds / max(t1, 1e-3))))
+        dt = run_rows(rows) if rows > 1 else t1
+    flops = 2.0 * b ** 3 * nt * nt * rows
+    return {"value": flops / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "port",
+            "sample": f"tiled DGEMM {n}/{b}: block-rows 0..{rows - 1} of C ({rows * nt * nt} tasks, "
+                      f"{flops / 1e12:.2f} TFLOP) on the oracle STF engine (restated reference, "
+                      f"{cores} host worker threads, numpy bodies, 1 BLAS thread each)",
+            "seconds": dt}
+
+
+def run_reference(args, dist):
+    if dist.rank != 0:
+        return  # under torchrun only rank 0 runs the CPU reference
+    res = cpu_baseline(args.n, args.b, args.cpu_seconds)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": res["value"], "unit": "GFLOP/s", "n_gpus": args.gpus,
+        "steps": 1, "warmup": 0, "ms_per_step": res["seconds"] * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"tiled DGEMM {args.n}x{args.n} fp64, {args.b}x{args.b} tiles (C2), bounded CPU sample",
+                   "n": args.n, "b": args.b},
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": res["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU legs
+
+def main_ours(args, dist):
+    import numpy as np
+    import torch
+
+    import paper_2308_15964_b200 as sf
+    from paper_2308_15964_b200 import algorithms as alg
+
+    dev = dist.local if dist.world > 1 else 0
+    torch.cuda.set_device(dev)
+    peak_tf, _ = sf.fp64_peak(dev)
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, args.streams), scheduler="prio", trace=False,
+                           ordinals=[dev], group_max=args.group)
+    n, b = args.n, args.b
+    nt = n // b
+    flops = alg.flops_gemm(n)
+    A, B, C = (alg.TiledMatrix(n, b) for _ in range(3))
+    g = sf.TaskGraph().compute_on(eng)
+    alg.insert_fill_uniform(g, A, 1)
+    alg.insert_fill_uniform(g, B, 2)
+    alg.insert_zero(g, C)
+    g.wait_all()
+
+    def step():
+        alg.insert_gemm(g, A, B, C)
+        g.wait_all()
+
+    for _ in range(args.warmup):
+        step()
+    st0 = eng.stats(0)
+    clocks = ClockSampler(dev)
+    clocks.start()
+    times = []
+    for _ in range(args.steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step()
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+    clk = clocks.stop()
+    st1 = eng.stats(0)
+    step_s = dist.max(statistics.mean(times))
+    value = flops * dist.world / step_s / 1e9
+    launches = st1["kernel_launches"] - st0["kernel_launches"]
+
+    # ---- e2e: host-resident inputs through the public API ----
+    def e2e_step():
+        alg.insert_gemm(g, A, B, C)
+        for t in C.tiles.values():
+            g.flush_to_host(t)                      # C back to the host (write-mode flush)
+        for M in (A, B):
+            for t in M.tiles.values():
+                g.flush_to_host(t)                  # clean copies dropped: next step restages
+        g.wait_all()
+
+    e2e_step()  # first pass moves everything to the host side
+    s0 = eng.stats(0)
+    et = []
+    for _ in range(max(2, args.steps // 2)):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        et.append(e0.elapsed_time(e1) / 1e3)
+    s1 = eng.stats(0)
+    ksteps = len(et)
+    e2e_s = dist.max(statistics.mean(et))
+    e2e = {"value": flops * dist.world / e2e_s / 1e9, "unit": "GFLOP/s",
+           "h2d_bytes_per_step": (s1["bytes_to_device"] - s0["bytes_to_device"]) // ksteps,
+           "d2h_bytes_per_step": (s1["bytes_from_device"] - s0["bytes_from_device"]) // ksteps,
+           "ms_per_step": e2e_s * 1e3}
+    eng.stop()
+    del A, B, C
+
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "dgemm_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    achieved = value / dist.world / 1e3  # per-GPU TFLOP/s of the DGEMM kernel (100% of the step's work)
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": achieved / peak_tf, "traffic": traffic,
+                "peak_source": "FP64 DMMA (mma.sync m8n8k4 -> DMMA.8x8x4) peak measured in-run on this GPU "
+                               "by sfx_fp64_peak; MEASURED_PEAKS.json has no FP64 entry",
+                "kernel": "dgemm_dmma_kernel (grouped, TMA + DMMA)",
+                "algorithmic_flops_per_task": 2 * b ** 3}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": dist.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (splitmix64 uniform tiles generated on device)",
+        "config": {"workload": f"tiled DGEMM {n}x{n} fp64, {b}x{b} tiles (BASELINE configs[1], C2), "
+                               f"{nt ** 3} GEMM tasks per step per GPU",
+                   "n": n, "b": b, "tasks_per_step": nt ** 3, "streams_per_gpu": args.streams,
+                   "group_max": args.group, "scheduler": "prio",
+                   "l2": "inputs (6 GiB) larger than L2; no flush", "parallelism": f"replica x{dist.world}"},
+        "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+        "pct_fp64_peak": 100.0 * achieved / peak_tf,
+    }
+
+    if dist.rank == 0 and dist.world == 1 and not args.no_secondary:
+        line["secondary"] = secondary(sf, alg, dev, args, peak_tf)
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
+        try:
+            cb = cpu_baseline(n, b, args.cpu_seconds)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as exc:  # the CPU leg must not hide the GPU line
+            line["cpu_baseline"] = {"error": repr(exc)}
+    if dist.rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def secondary(sf, alg, dev, args, peak_tf):
+    import torch
+
+    out = {}
+    # C3: tiled Cholesky 32768 / 1024 on one GPU
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, args.streams), scheduler="prio", trace=False,
+                           ordinals=[dev], group_max=args.group)
+    n, b = 32768, 1024
+    M = alg.TiledMatrix(n, b, lower=True)
+    g = sf.TaskGraph().compute_on(eng)
+    ts = []
+    for rep in range(3):
+        alg.insert_fill_spd(g, M, 3)
+        g.wait_all()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        alg.insert_cholesky(g, M)
+        g.wait_all()
+        e1.record()
+        torch.cuda.synchronize()
+        if rep:
+            ts.append(e0.elapsed_time(e1) / 1e3)
+    t = statistics.mean(ts)
+    out["cholesky_C3"] = {"n": n, "b": b, "tasks": 5984, "seconds": t, "gflops": alg.flops_cholesky(n) / t / 1e9,
+                          "pct_fp64_peak": 100 * alg.flops_cholesky(n) / t / 1e12 / peak_tf}
+    eng.stop()
+    del M
+    # C4: particles 2^20 in 256 groups, one evaluation
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, args.streams), trace=False, ordinals=[dev])
+    ng, per = 256, 4096
+    P = [sf.pinned_empty((4, per)) for _ in range(ng)]
+    F = [sf.pinned_empty((4, per)) for _ in range(ng)]
+    g = sf.TaskGraph().compute_on(eng)
+    alg.insert_fill_particles(g, P, 4)
+    for f in F:
+        g.task(sf.write(f), device=sf.ops.zero())
+    g.wait_all()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    alg.insert_particles(g, P, F)
+    g.wait_all()
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / 1e3
+    inter = alg.interactions(ng * per)
+    out["particles_C4"] = {"particles": ng * per, "groups": ng, "tasks": 32896, "seconds": t,
+                           "interactions_per_s": inter / t,
+                           "gflops_20flop_convention": inter * alg.FLOP_PER_INTERACTION / t / 1e9}
+    eng.stop()
+    # runtime overhead per task: reference protocol (src/bench.py:67-117), T chains x N tasks, D = 0
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, 4), trace=False, ordinals=[dev])
+    g = sf.TaskGraph().compute_on(eng)
+    T, N = 4, 5000
+    cells = [sf.Cell(0) for _ in range(T)]
+    for rep in range(2):
+        t0 = time.perf_counter()
+        for i in range(N):
+            for c in cells:
+                g.task(sf.write(c), device=sf.ops.noop)
+        t1 = time.perf_counter()
+        g.wait_all()
+        t2 = time.perf_counter()
+    out["runtime_overhead"] = {"protocol": "T=4 chains x N=5000 empty tasks (D=0), per-task python insertion",
+                               "insert_us_per_task": (t1 - t0) / (T * N) * 1e6,
+                               "total_us_per_task": (t2 - t0) / (T * N) * 1e6,
+                               "O_avg_us": ((t2 - t0) / N) * 1e6}
+    eng.stop()
+    return out
+
+
+def main():
+    args = parse()
+    dist = Dist()
+    if args.impl == "reference":
+        run_reference(args, dist)
+        return
+    dist.init("nccl")
+    main_ours(args, dist)
+    dist.done()
+
+
+if __name__ == "__main__":
+    main()

@@ -138,7 +138,8 @@ typedef struct sfx_dev_stats {
   /* tile cache */
   uint64_t hits, misses, evictions, writebacks;
   uint64_t blocks, bytes_in_use, capacity;
-  /* executor */
+  /* executor; kernel_launches = CUDA kernels launched by this process's ops
+   * (sim: ops executed) */
   uint64_t tasks_executed, kernel_launches, stream_waits;
   /* host-side time of the executor (ns): planning under the lock, issuing
    * stream work outside it, releasing successors; completion-thread time;

@@ -18,8 +18,9 @@ Loop orders follow SURVEY.md §8c (the order of probe A.7):
 
 Priorities (used only with the priority scheduler, scheduler.py:97-126):
 critical-path tasks -- POTRF, TRSM and updates of the next panel column -- get
-``2*nt`` on top of ``nt - k`` so step k+1's panel overtakes step k's trailing
-GEMMs (one-step lookahead).
+10^6 on top of ``nt - k`` so step k+1's panel overtakes step k's trailing
+GEMMs (one-step lookahead); the GPU runtime launches priorities >= 10^6 on its
+high-priority CUDA streams.
 """
 
 from __future__ import annotations
@@ -40,7 +41,7 @@ def cholesky_program(nt: int):
     prog = []
     for k in range(nt):
         base = nt - k
-        crit = 2 * nt + base
+        crit = 1_000_000 + base
         prog.append(("potrf", [(WRITE, ("A", k, k))], crit))
         for i in range(k + 1, nt):
             prog.append(("trsm", [(READ, ("A", k, k)), (WRITE, ("A", i, k))], crit))

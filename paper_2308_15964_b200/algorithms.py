@@ -113,10 +113,14 @@ def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: boo
     return batch.submit() if batch else None
 
 
+URGENT = 1_000_000  # runtime default "urgent_priority": launched on high-priority CUDA streams
+
+
 def cholesky_priorities(nt: int, kind: str, k: int, i: int = 0, j: int = 0) -> int:
-    """Critical path first: POTRF, TRSM and next-column updates get 2*nt on top of nt-k."""
+    """Critical path first: POTRF, TRSM and next-column updates are urgent (>= URGENT),
+    earlier panels before later ones (nt - k)."""
     base = nt - k
-    crit = 2 * nt + base
+    crit = URGENT + base
     if kind in ("potrf", "trsm"):
         return crit
     if kind == "syrk":

@@ -304,6 +304,7 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
   const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
   p.tiles_n = tn;
   p.tiles_per_task = lower ? tm * (tm + 1) / 2 : tm * tn;
+  count_launch();
   dgemm_dmma_kernel<TB, G><<<p.tiles_per_task * n, THREADS, SMEM_BYTES, stream>>>(p);
   return cudaGetLastError();
 }

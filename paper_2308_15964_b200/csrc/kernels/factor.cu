@@ -105,6 +105,7 @@ cudaError_t launch_dtrsm(const double* L, long long ldl, double* B, long long ld
       if (e) return e;
       attr[dev & 63] = true;
     }
+    count_launch();
     trsm_leaf_kernel<<<(M + TRSM_THREADS - 1) / TRSM_THREADS, TRSM_THREADS, smem, s>>>(B, ldb, M, n, L, ldl);
     return cudaGetLastError();
   }
@@ -120,6 +121,7 @@ cudaError_t launch_dtrsm(const double* L, long long ldl, double* B, long long ld
 cudaError_t launch_dpotrf(double* A, long long lda, int n, int* info, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   if (n <= LEAF) {
+    count_launch();
     potrf_leaf_kernel<<<1, 256, 0, s>>>(A, lda, n, info);
     return cudaGetLastError();
   }

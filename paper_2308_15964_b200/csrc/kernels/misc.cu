@@ -5,6 +5,9 @@
 #include "ptx.cuh"
 
 namespace sfx {
+
+std::atomic<unsigned long long> g_kernel_launches{0};
+
 namespace {
 
 constexpr long long kMod = 10000019;  // reference tests/conftest.py:22
@@ -127,6 +130,7 @@ cudaError_t launch_fill_uniform(double* a, long long rows, long long cols, long 
                                 long long row0, long long col0, long long ncols_total, cudaStream_t s) {
   long long n = rows * cols;
   if (n <= 0) return cudaSuccess;
+  count_launch();
   fill_uniform_kernel<<<grid_for(n, 256), 256, 0, s>>>(a, rows, cols, ld, seed, row0, col0, ncols_total);
   return cudaGetLastError();
 }
@@ -135,6 +139,7 @@ cudaError_t launch_fill_spd(double* a, long long rows, long long cols, long long
                             long long col0, long long n, cudaStream_t s) {
   long long m = rows * cols;
   if (m <= 0) return cudaSuccess;
+  count_launch();
   fill_spd_kernel<<<grid_for(m, 256), 256, 0, s>>>(a, rows, cols, ld, seed, row0, col0, n);
   return cudaGetLastError();
 }
@@ -142,11 +147,13 @@ cudaError_t launch_fill_spd(double* a, long long rows, long long cols, long long
 cudaError_t launch_fill_particles(double* p, long long n, long long ld, long long seed, long long first,
                                   cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
+  count_launch();
   fill_particles_kernel<<<grid_for(n, 256), 256, 0, s>>>(p, n, ld, seed, first);
   return cudaGetLastError();
 }
 
 cudaError_t launch_spin(long long ns, cudaStream_t s) {
+  count_launch();
   spin_kernel<<<1, 32, 0, s>>>(ns);
   return cudaGetLastError();
 }
@@ -160,12 +167,14 @@ cudaError_t launch_cell(long long* target, const long long* const* reads, int nr
   c.kind = kind;
   c.a = a;
   c.b = b;
+  count_launch();
   cell_kernel<<<1, 1, 0, s>>>(c);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bytes_add(unsigned char* p, long long off, long long len, long long delta, cudaStream_t s) {
   if (len <= 0) return cudaSuccess;
+  count_launch();
   bytes_add_kernel<<<grid_for(len, 256), 256, 0, s>>>(p, off, len, delta);
   return cudaGetLastError();
 }
@@ -183,8 +192,10 @@ cudaError_t fp64_dmma_peak(int iters, double* tflops) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const int warps = 16;
+  count_launch();
   dmma_peak_kernel<<<sms, 32 * warps>>>(out, 100);  // warm-up
   cudaEventRecord(e0);
+  count_launch();
   dmma_peak_kernel<<<sms, 32 * warps>>>(out, iters);
   cudaEventRecord(e1);
   e = cudaEventSynchronize(e1);

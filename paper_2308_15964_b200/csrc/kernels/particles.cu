@@ -111,10 +111,12 @@ cudaError_t launch_p2p(const double* Pi, long long ldpi, int ni, const double* P
   P2PSide a{Pi, self ? Pi : Pj, Fi, ldpi, self ? ldpi : ldpj, ldfi, ni, self ? ni : nj, self ? 1 : 0};
   const int b0 = (ni + per_block - 1) / per_block;
   if (self) {
+    count_launch();
     p2p_kernel<<<b0, THREADS, 0, s>>>(a, a, b0, eps2);
   } else {
     P2PSide b{Pj, Pi, Fj, ldpj, ldpi, ldfj, nj, ni, 0};
     const int b1 = (nj + per_block - 1) / per_block;
+    count_launch();
     p2p_kernel<<<b0 + b1, THREADS, 0, s>>>(a, b, b0, eps2);
   }
   return cudaGetLastError();

@@ -51,7 +51,7 @@ class CudaBackend : public Backend {
   }
   bool is_sim() const override { return false; }
 
-  int init_device(int d, int, int nstreams, uint64_t bytes, std::string& err) override {
+  int init_device(int d, int, int nstreams, int nurgent, uint64_t bytes, std::string& err) override {
     Dev& D = *devs_[d];
     cudaError_t e = cudaSetDevice(D.ordinal);
     if (e) return cuda_err(e, "cudaSetDevice", err);
@@ -75,9 +75,9 @@ class CudaBackend : public Backend {
     cudaMemset(D.info, 0, sizeof(int));
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    D.streams.resize(nstreams);
-    for (int s = 0; s < nstreams; ++s) {
-      e = cudaStreamCreateWithPriority(&D.streams[s], cudaStreamNonBlocking, least);
+    D.streams.resize(nstreams + nurgent);
+    for (int s = 0; s < nstreams + nurgent; ++s) {
+      e = cudaStreamCreateWithPriority(&D.streams[s], cudaStreamNonBlocking, s < nstreams ? least : greatest);
       if (e) return cuda_err(e, "cudaStreamCreate", err);
     }
     // peer access to every device initialised before this one (both ways)
@@ -181,6 +181,7 @@ class CudaBackend : public Backend {
                                         devs_[sd]->ordinal, n, devs_[d]->streams[stream]),
                     "peer copy", err);
   }
+  uint64_t kernel_launches() const override { return g_kernel_launches.load(); }
   bool supports(uint32_t op) const override {
     switch (op) {
       case SFX_OP_NOOP:

@@ -77,10 +77,11 @@ Runtime::Runtime(Backend* be, int ndev, int nstreams, uint32_t sched, uint32_t f
       nstreams_(nstreams),
       sched_(sched),
       flags_(flags),
-      window_(window ? window : 4u * static_cast<uint32_t>(nstreams) + 64u),
+      window_(window ? window : 4096u),
       align_(align),
       trace_((flags & SFX_FLAG_TRACE) != 0) {
   paused_ = (flags & SFX_FLAG_PAUSED) != 0;
+  nurgent_ = nstreams >= 2 ? std::max(2, nstreams / 4) : 0;
 }
 
 int Runtime::init(const uint64_t* arena_bytes, std::string& err) {
@@ -88,8 +89,9 @@ int Runtime::init(const uint64_t* arena_bytes, std::string& err) {
     auto dev = std::make_unique<Device>();
     dev->index = d;
     dev->queue.prio = sched_ == SFX_SCHED_PRIO;
-    dev->stream_inflight.assign(nstreams_, 0);
-    int rc = be_->init_device(d, d, nstreams_, arena_bytes ? arena_bytes[d] : 0, err);
+    dev->stream_inflight.assign(nstreams_ + nurgent_, 0);
+    dev->stream_groups.assign(nstreams_ + nurgent_, 0);
+    int rc = be_->init_device(d, d, nstreams_, nurgent_, arena_bytes ? arena_bytes[d] : 0, err);
     if (rc) return rc;
     dev->capacity = be_->arena_capacity(d);
     dev->free_bytes = dev->capacity;
@@ -918,7 +920,7 @@ int Runtime::issue(int d, int s, const std::vector<Task*>& group, std::vector<Ac
   if (!kern.empty()) {
     rc = be_->launch_group(d, s, kern, err);
     if (rc) return rc;
-    devs_[d]->stats.kernel_launches += kern.size();
+    devs_[d]->stats.kernel_launches += kern.size();  // sim: ops executed
   }
   SyncP end = group[0]->end;
   rc = be_->event_record(d, s, end->event, err);
@@ -969,6 +971,10 @@ bool Runtime::commute_conflict(const std::vector<Task*>& group, const Task* t) c
 
 void Runtime::complete(Task* t) {
   Device& D = *devs_[t->dev];
+  if (t->end && !t->end->group_counted) {
+    t->end->group_counted = true;
+    D.stream_groups[t->stream] -= 1;
+  }
   if (t->end) t->end->complete = true;
   if (t->start) t->start->complete = true;
   for (auto& c : t->copy_syncs) c->complete = true;
@@ -986,7 +992,7 @@ void Runtime::complete(Task* t) {
   if (trace_ && t->start && t->end) {
     t->t_start = be_->event_time_ns(t->dev, t->start->event);
     t->t_end = be_->event_time_ns(t->dev, t->end->event);
-    const int wid = t->dev * nstreams_ + t->stream;
+    const int wid = t->dev * (nstreams_ + nurgent_) + t->stream;
     record(g, SFX_EV_START, t->t_start, wid, t->tid);
     record(g, SFX_EV_END, t->t_end, wid, t->tid);
   }
@@ -1022,8 +1028,26 @@ void Runtime::exec_loop(int d) {
   std::vector<Action> acts;
   std::vector<OpLaunch> ops;
   while (true) {
+    auto free_in = [&](int lo, int hi) {
+      int best = -1;
+      for (int k = lo; k < hi; ++k)
+        if (D.stream_groups[k] < static_cast<int>(groups_per_stream_) &&
+            (best < 0 || D.stream_inflight[k] < D.stream_inflight[best]))
+          best = k;
+      return best;
+    };
+    // urgent tasks prefer the high-priority streams and may fall back to normal
+    // ones; normal tasks never take an urgent stream
+    auto free_stream = [&](const Task* t) {
+      if (nurgent_ > 0 && t->prio >= urgent_priority_) {
+        int s = free_in(nstreams_, nstreams_ + nurgent_);
+        return s >= 0 ? s : free_in(0, nstreams_);
+      }
+      return free_in(0, nstreams_);
+    };
     D.exec_cv.wait(lk, [&] {
-      return stopping_ || (!paused_ && !fail_code_ && D.queue.size() > 0 && D.ninflight < static_cast<int>(window_));
+      return stopping_ || (!paused_ && !fail_code_ && D.queue.size() > 0 &&
+                           D.ninflight < static_cast<int>(window_) && free_stream(D.queue.peek()) >= 0);
     });
     if (stopping_) return;
     const int64_t t_busy0 = now_ns();
@@ -1034,16 +1058,16 @@ void Runtime::exec_loop(int d) {
     Task* first = D.queue.pop();
     group.push_back(first);
     if (groupable(first)) {
+      const bool urgent = first->prio >= urgent_priority_;
       while (group.size() < group_max_ && D.queue.size() > 0 &&
              D.ninflight + static_cast<int>(group.size()) < static_cast<int>(window_)) {
         Task* nx = D.queue.peek();
-        if (!same_signature(first, nx) || commute_conflict(group, nx)) break;
+        if (!same_signature(first, nx) || commute_conflict(group, nx) || (nx->prio >= urgent_priority_) != urgent)
+          break;
         group.push_back(D.queue.pop());
       }
     }
-    int s = 0;
-    for (int k = 1; k < nstreams_; ++k)
-      if (D.stream_inflight[k] < D.stream_inflight[s]) s = k;
+    const int s = free_stream(first);
     SyncP gend = new_sync(d, s, trace_);
     SyncP gstart = trace_ ? new_sync(d, s, true) : nullptr;
     const int64_t tpop = now_ns();
@@ -1053,7 +1077,7 @@ void Runtime::exec_loop(int d) {
       t->t_pop = tpop;
       t->end = gend;
       t->start = gstart;
-      record(graphs_[t->gid].get(), SFX_EV_POP, tpop, d * nstreams_ + s, t->tid);
+      record(graphs_[t->gid].get(), SFX_EV_POP, tpop, d * (nstreams_ + nurgent_) + s, t->tid);
     }
     acts.clear();
     ops.assign(group.size(), OpLaunch());
@@ -1130,6 +1154,7 @@ void Runtime::exec_loop(int d) {
     }
     D.ninflight += static_cast<int>(group.size());
     D.stream_inflight[s] += static_cast<int>(group.size());
+    D.stream_groups[s] += 1;
     const int64_t t_plan1 = now_ns();
     D.stats.t_plan_ns += t_plan1 - t_busy0;
     lk.unlock();
@@ -1252,6 +1277,7 @@ int Runtime::stats(int dev, sfx_dev_stats* out) {
     return SFX_ERR_CONFIG;
   }
   *out = devs_[dev]->stats;
+  if (!be_->is_sim()) out->kernel_launches = be_->kernel_launches();  // process-wide kernel count
   return SFX_OK;
 }
 
@@ -1348,6 +1374,11 @@ int Runtime::set_option(const std::string& key, int64_t value) {
   std::unique_lock<std::mutex> lk(mu_);
   if (key == "group_max") {
     group_max_ = static_cast<uint32_t>(std::max<int64_t>(1, std::min<int64_t>(value, 1024)));
+  } else if (key == "groups_per_stream") {
+    groups_per_stream_ = static_cast<uint32_t>(std::max<int64_t>(1, value));
+    for (auto& d : devs_) d->exec_cv.notify_all();
+  } else if (key == "urgent_priority") {
+    urgent_priority_ = value;
   } else if (key == "window") {
     window_ = static_cast<uint32_t>(std::max<int64_t>(1, value));
     for (auto& d : devs_) d->exec_cv.notify_all();

@@ -60,7 +60,8 @@ struct Sync {
   void* event = nullptr;
   bool timing = false;
   std::atomic<bool> recorded{false};
-  bool complete = false;  // guarded by the runtime mutex
+  bool complete = false;       // guarded by the runtime mutex
+  bool group_counted = false;  // launch group already retired from its stream
   ~Sync();
 };
 using SyncP = std::shared_ptr<Sync>;
@@ -156,7 +157,8 @@ class Backend {
  public:
   virtual ~Backend() {}
   virtual bool is_sim() const = 0;
-  virtual int init_device(int d, int ordinal, int nstreams, uint64_t arena_bytes, std::string& err) = 0;
+  // nstreams normal-priority streams followed by nurgent highest-priority streams
+  virtual int init_device(int d, int ordinal, int nstreams, int nurgent, uint64_t arena_bytes, std::string& err) = 0;
   virtual void bind_thread(int d) = 0;
   virtual uint64_t arena_capacity(int d) = 0;
   virtual void* arena_ptr(int d, uint64_t off) = 0;
@@ -181,6 +183,8 @@ class Backend {
     return 0;
   }
   virtual bool supports(uint32_t op) const = 0;
+  // kernels launched so far by this process's ops (0 for the simulator)
+  virtual uint64_t kernel_launches() const { return 0; }
   virtual void shutdown() = 0;
 };
 
@@ -216,7 +220,8 @@ struct Device {
   uint64_t clock = 0;
   DevQueue queue;
   std::deque<Task*> inflight;
-  std::vector<int> stream_inflight;
+  std::vector<int> stream_inflight;  // tasks in flight per stream
+  std::vector<int> stream_groups;    // launch groups in flight per stream
   int ninflight = 0;
   std::condition_variable exec_cv, comp_cv;
   std::thread exec_thread, comp_thread;
@@ -281,6 +286,12 @@ class Runtime {
   int ndev_, nstreams_;
   uint32_t sched_, flags_, window_;
   uint32_t group_max_ = 32;
+  uint32_t groups_per_stream_ = 2;  // launches queued ahead on each stream
+  // tasks with priority >= urgent_priority_ go to the high-priority CUDA
+  // streams (indices nstreams_ .. nstreams_+nurgent_-1): the block scheduler
+  // then starts their CTAs first whenever an SM frees up (critical path)
+  int nurgent_ = 0;
+  int64_t urgent_priority_ = 1000000;
   uint64_t align_;
   bool trace_;
   std::mutex mu_;
