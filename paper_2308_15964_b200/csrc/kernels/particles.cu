@@ -14,7 +14,8 @@
 // Layout/roofline choices: one thread owns TPT targets in registers; source
 // tiles are staged in shared memory with coalesced loads and read back as
 // broadcasts (every lane reads the same source), so the inner loop is pure
-// FP64 pipe work (3 DADD + 3 DFMA + rsqrt + 1 DFMA + 3 DMUL + 3 DFMA).
+// FP64 pipe work: 3 DADD + 3 DFMA (r2) + MUFU.RSQ64H + 8 (Newton) + 3 DMUL +
+// 1 DADD + 3 DFMA = 21 FP64 ops per ordered interaction.
 // Commutative accumulation into F is exclusive per handle (the runtime chains
 // members of a commutative group), so the epilogue is a plain read-add-write.
 //
@@ -25,8 +26,21 @@ namespace sfx {
 namespace {
 
 constexpr int THREADS = 128;
-constexpr int TPT = 2;  // targets per thread
+constexpr int TPT = 4;  // targets per thread (ILP + one smem broadcast per 4 interactions)
 constexpr int TILE = 256;
+
+// 1/sqrt(x) for normal x > 0 (r2 >= eps2 > 0 here): the MUFU.RSQ64H seed
+// (~23 bits) refined by two Newton steps (~46 -> full double).  4 FP64 ops per
+// step, no special-case slow path (CUDA's rsqrt(double) branches to one).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x * y, y, 1.0);
+  y = fma(0.5 * y, e, y);
+  e = fma(-x * y, y, 1.0);
+  y = fma(0.5 * y, e, y);
+  return y;
+}
 
 struct P2PSide {
   const double* tgt;  // 4 x nt (ld)
@@ -80,7 +94,7 @@ __global__ void __launch_bounds__(THREADS) p2p_kernel(P2PSide s0, P2PSide s1, in
       for (int u = 0; u < TPT; ++u) {
         const double dx = xi[u] - p.x, dy = yi[u] - p.y, dz = zi[u] - p.z;
         const double r2 = fma(dx, dx, fma(dy, dy, fma(dz, dz, eps2)));
-        double inv = rsqrt(r2);
+        double inv = rsqrt_nr(r2);
         if (S.self && j0 + k == ti[u]) inv = 0.0;
         const double qi = p.w * inv;        // q_b / r
         const double s3 = qi * inv * inv;   // q_b / r^3

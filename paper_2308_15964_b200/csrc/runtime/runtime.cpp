@@ -443,6 +443,9 @@ int Runtime::submit(uint32_t n, const sfx_task_desc* descs, const sfx_access* ac
     t->acc.reserve(d.n_access);
     for (uint32_t k = 0; k < d.n_access; ++k) bind(t, handles_[acc[ai + k].hid], acc[ai + k].mode);
     ai += d.n_access;
+    for (auto& a : t->acc)
+      if (a.mode == SFX_COMMUTATIVE_WRITE) t->commute.push_back(a.h);
+    std::sort(t->commute.begin(), t->commute.end(), [](const Handle* x, const Handle* y) { return x->hid < y->hid; });
     Graph* g = graphs_[d.graph].get();
     g->tasks.push_back(t);
     g->inserted += 1;
@@ -958,6 +961,31 @@ bool Runtime::same_signature(const Task* a, const Task* b) const {
   return true;
 }
 
+bool Runtime::acquire_commute(Task* t) {
+  // all-or-nothing in hid order; on failure the task parks on the busy handle
+  for (Handle* h : t->commute) {
+    if (h->commute_owner && h->commute_owner != t) {
+      h->commute_waiters.push_back(t);
+      return false;
+    }
+  }
+  for (Handle* h : t->commute) h->commute_owner = t;
+  return true;
+}
+
+void Runtime::release_commute(Task* t) {
+  for (Handle* h : t->commute) {
+    if (h->commute_owner != t) continue;
+    h->commute_owner = nullptr;
+    // wake the parked members in FIFO order; each re-enters its device queue
+    while (!h->commute_waiters.empty()) {
+      Task* w = h->commute_waiters.front();
+      h->commute_waiters.pop_front();
+      push_ready(w, -1);
+    }
+  }
+}
+
 bool Runtime::commute_conflict(const std::vector<Task*>& group, const Task* t) const {
   // members of one commutative group must never run concurrently on the same handle
   for (const Access& a : t->acc) {
@@ -999,6 +1027,7 @@ void Runtime::complete(Task* t) {
   t->start.reset();
   t->end.reset();
   t->state = SFX_STATE_FINISHED;
+  if (!t->commute.empty()) release_commute(t);
   g->completed += 1;
   D.ninflight -= 1;
   D.stream_inflight[t->stream] -= 1;
@@ -1056,6 +1085,7 @@ void Runtime::exec_loop(int d) {
     // members of one handle
     group.clear();
     Task* first = D.queue.pop();
+    if (!first->commute.empty() && !acquire_commute(first)) continue;  // parked until the guard frees
     group.push_back(first);
     if (groupable(first)) {
       const bool urgent = first->prio >= urgent_priority_;
@@ -1064,7 +1094,9 @@ void Runtime::exec_loop(int d) {
         Task* nx = D.queue.peek();
         if (!same_signature(first, nx) || commute_conflict(group, nx) || (nx->prio >= urgent_priority_) != urgent)
           break;
-        group.push_back(D.queue.pop());
+        D.queue.pop();
+        if (!nx->commute.empty() && !acquire_commute(nx)) continue;
+        group.push_back(nx);
       }
     }
     const int s = free_stream(first);
@@ -1100,6 +1132,8 @@ void Runtime::exec_loop(int d) {
           t->end.reset();
           t->start.reset();
           t->state = SFX_STATE_READY;
+          for (Handle* h : t->commute)
+            if (h->commute_owner == t) h->commute_owner = nullptr;
           D.queue.push_front(t);
         }
         group.resize(planned);

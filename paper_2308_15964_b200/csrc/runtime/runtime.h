@@ -99,6 +99,11 @@ struct Handle {
   bool host_valid = true;
   SyncP host_ready;     // host buffer is current once this completes
   SyncP commute_last;   // end of the last launched commutative member
+  // commutative exclusivity guard (handles.py:249-270): held from launch until
+  // the owner COMPLETES; tasks that fail to acquire park on the handle instead
+  // of being re-offered (no quadratic re-offer scan, handles.py:317-328)
+  Task* commute_owner = nullptr;
+  std::deque<Task*> commute_waiters;
   int group_dev = -1;   // device of the active atomic/commutative group
   int home = -1;        // owner hint (2-D block-cyclic distribution)
 };
@@ -126,6 +131,7 @@ struct Task {
   std::vector<Block*> pinned;     // unpinned at completion
   std::vector<SyncP> copy_syncs;  // copies issued on this task's stream
   int64_t t_push = 0, t_pop = 0, t_start = 0, t_end = 0;
+  std::vector<Handle*> commute;  // commutative handles sorted by hid (graph.py:150-157)
 };
 
 struct Operand {
@@ -267,6 +273,8 @@ class Runtime {
   bool groupable(const Task* t) const;
   bool same_signature(const Task* a, const Task* b) const;
   bool commute_conflict(const std::vector<Task*>& group, const Task* t) const;
+  bool acquire_commute(Task* t);
+  void release_commute(Task* t);
   int ensure_block(int d, int s, Handle* h, std::vector<Action>& acts, std::vector<Block*>& tmp_pins, Block** out,
                    std::string& err);
   int evict_one(int d, int s, std::vector<Action>& acts, std::string& err);
