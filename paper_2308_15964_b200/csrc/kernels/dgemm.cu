@@ -22,6 +22,7 @@
 //  * FP64 has no tcgen05 kind, so there is no TMEM accumulator: accumulators
 //    live in registers (64 doubles / thread).
 #include <cstdio>
+#include <cstdlib>
 #include <cudaTypedefs.h>
 
 #include <unordered_map>
@@ -53,6 +54,7 @@ template <int G>
 struct GemmGroup {
   GemmOperands t[G];
   long long ldc;
+  int ntasks;
   int M, N, K;
   int tiles_n, tiles_per_task;
   int lower;
@@ -70,26 +72,27 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
   uint64_t* empty = full + STAGES;
 
-  const int task = blockIdx.x / p.tiles_per_task;
-  const int tile = blockIdx.x - task * p.tiles_per_task;
-  const CUtensorMap* tmA = &p.t[task].a;
-  const CUtensorMap* tmB = &p.t[task].b;
-  double* const Cbase = p.t[task].C;
-  int bm, bn;
-  if (p.lower) {
-    // triangular enumeration of lower CTA tiles: idx -> (bm >= bn)
-    int idx = tile;
-    bm = static_cast<int>((sqrtf(8.0f * idx + 1.0f) - 1.0f) * 0.5f);
-    while ((bm + 1) * (bm + 2) / 2 <= idx) ++bm;
-    while (bm * (bm + 1) / 2 > idx) --bm;
-    bn = idx - bm * (bm + 1) / 2;
-  } else {
-    bm = tile / p.tiles_n;
-    bn = tile % p.tiles_n;
-  }
-  const int m0 = bm * BM, n0 = bn * BN;
+  const int total = p.ntasks * p.tiles_per_task;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ktiles = (p.K + BK - 1) / BK;
+
+  // linear tile index -> (task, m0, n0); lower = triangular enumeration (bm >= bn)
+  auto coords = [&](int lin, int& task, int& m0, int& n0) {
+    task = lin / p.tiles_per_task;
+    const int tile = lin - task * p.tiles_per_task;
+    int bm, bn;
+    if (p.lower) {
+      bm = static_cast<int>((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+      while ((bm + 1) * (bm + 2) / 2 <= tile) ++bm;
+      while (bm * (bm + 1) / 2 > tile) --bm;
+      bn = tile - bm * (bm + 1) / 2;
+    } else {
+      bm = tile / p.tiles_n;
+      bn = tile % p.tiles_n;
+    }
+    m0 = bm * BM;
+    n0 = bn * BN;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -102,21 +105,30 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
 
   if (warp >= CONSUMER_WARPS) {
     // ---- TMA producer warpgroup (one elected lane) ----
+    // Persistent: the smem ring runs across this CTA's tiles, so the next
+    // tile's operands stream in while the consumers finish the current one.
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     if (warp == CONSUMER_WARPS && lane == 0) {
-      ptx::prefetch_tmap(tmA);
-      ptx::prefetch_tmap(tmB);
-      for (int kt = 0; kt < ktiles; ++kt) {
-        const int s = kt % STAGES;
-        if (kt >= STAGES) ptx::mbar_wait(&empty[s], ((kt / STAGES) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[s], A_STAGE + B_STAGE);
-        ptx::tma_load_2d(sA + s * A_STAGE, tmA, kt * BK, m0, &full[s]);
-        if (TRANS_B) {
-          ptx::tma_load_2d(sB + s * B_STAGE, tmB, kt * BK, n0, &full[s]);
-        } else {
+      int it = 0;
+      for (int lin = blockIdx.x; lin < total; lin += gridDim.x) {
+        int task, m0, n0;
+        coords(lin, task, m0, n0);
+        const CUtensorMap* tmA = &p.t[task].a;
+        const CUtensorMap* tmB = &p.t[task].b;
+        ptx::prefetch_tmap(tmA);
+        ptx::prefetch_tmap(tmB);
+        for (int kt = 0; kt < ktiles; ++kt, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[s], A_STAGE + B_STAGE);
+          ptx::tma_load_2d(sA + s * A_STAGE, tmA, kt * BK, m0, &full[s]);
+          if (TRANS_B) {
+            ptx::tma_load_2d(sB + s * B_STAGE, tmB, kt * BK, n0, &full[s]);
+          } else {
 #pragma unroll
-          for (int q = 0; q < BN / 16; ++q)
-            ptx::tma_load_2d(sB + s * B_STAGE + q * 2048, tmB, n0 + 16 * q, kt * BK, &full[s]);
+            for (int q = 0; q < BN / 16; ++q)
+              ptx::tma_load_2d(sB + s * B_STAGE + q * 2048, tmB, n0 + 16 * q, kt * BK, &full[s]);
+          }
         }
       }
     }
@@ -127,84 +139,126 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
   asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
   const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warp grid, warp tile 64 x 32
   const int g = lane >> 2, t = lane & 3;
-  double acc[8][4][2];
+  int it = 0;
+  for (int lin = blockIdx.x; lin < total; lin += gridDim.x) {
+    int task, m0, n0;
+    coords(lin, task, m0, n0);
+    double acc[8][4][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const uint32_t sA_u = ptx::smem_u32(sA), sB_u = ptx::smem_u32(sB);
-  for (int kt = 0; kt < ktiles; ++kt) {
-    const int s = kt % STAGES;
-    ptx::mbar_wait(&full[s], (kt / STAGES) & 1);
-    const uint32_t aBase = sA_u + s * A_STAGE;
-    const uint32_t bBase = sB_u + s * B_STAGE;
+    for (int kt = 0; kt < ktiles; ++kt, ++it) {
+      const int s = it % STAGES;
+      ptx::mbar_wait(&full[s], (it / STAGES) & 1);
+      const uint32_t aS = ptx::smem_u32(sA) + s * A_STAGE;
+      const uint32_t bS = ptx::smem_u32(sB) + s * B_STAGE;
+      // operands (true k = 4t + 2h + e): ordered shared loads; the DMMAs are
+      // not volatile, so ptxas can slide this half's DMMAs past the next loads
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {  // k half: true k = 4t + 2h + {0,1}
-      double a[8][2], b[4][2];
+      for (int h = 0; h < 2; ++h) {
+        double a[8][2], b[4][2];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int r = wm * 64 + 8 * i + g;  // r % 8 == g
-        double2 v = ptx::lds128(aBase + r * 128 + (((2 * t + h) ^ g) << 4));
-        a[i][0] = v.x;
-        a[i][1] = v.y;
-      }
-      if (TRANS_B) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int r = wn * 32 + 8 * j + g;
-          double2 v = ptx::lds128(bBase + r * 128 + (((2 * t + h) ^ g) << 4));
-          b[j][0] = v.x;
-          b[j][1] = v.y;
+        for (int i = 0; i < 8; ++i) {
+          const int r = wm * 64 + 8 * i + g;  // r % 8 == g
+          const double2 v = ptx::lds128(aS + r * 128 + (((2 * t + h) ^ g) << 4));
+          a[i][0] = v.x;
+          a[i][1] = v.y;
         }
-      } else {
+        if (TRANS_B) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int n = wn * 32 + 8 * j + g;
-          const int q = n >> 4, nn = n & 15;
+          for (int j = 0; j < 4; ++j) {
+            const int r = wn * 32 + 8 * j + g;
+            const double2 v = ptx::lds128(bS + r * 128 + (((2 * t + h) ^ g) << 4));
+            b[j][0] = v.x;
+            b[j][1] = v.y;
+          }
+        } else {
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int k = 4 * t + 2 * h + e;
-            b[j][e] = ptx::lds64(bBase + q * 2048 + k * 128 + ((((nn >> 1) ^ (k & 7))) << 4) + (nn & 1) * 8);
+          for (int j = 0; j < 4; ++j) {
+            const int n = wn * 32 + 8 * j + g;
+            const int q = n >> 4, nn = n & 15;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int k = 4 * t + 2 * h + e;
+              b[j][e] = ptx::lds64(bS + q * 2048 + k * 128 + (((nn >> 1) ^ (k & 7)) << 4) + (nn & 1) * 8);
+            }
           }
         }
+        if (h == 1) ptx::mbar_arrive(&empty[s]);  // operands are in registers: the slot may be refilled
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i][e], b[j][e]);
       }
-      if (h == 1) ptx::mbar_arrive(&empty[s]);  // operands are in registers
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i][e], b[j][e]);
     }
-  }
 
-  // ---- epilogue: C = beta*C + alpha*acc ----
+    // ---- epilogue: C = beta*C + alpha*acc ----
+    // Interior tiles batch all 32 C loads before any FMA/store so the loads
+    // overlap (one HBM round trip per tile instead of one per fragment).
+    double* const Cbase = p.t[task].C;
+    const bool interior = !p.lower && m0 + BM <= p.M && n0 + BN <= p.N;
+    if (interior) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int row = m0 + wm * 64 + 8 * i + g;
-    if (row >= p.M) continue;
-    double* crow = Cbase + static_cast<long long>(row) * p.ldc;
+      for (int half = 0; half < 4; ++half) {  // 4 x 8 fragments: loads in flight together, no spills
+        double2 cv[2][4];
+        if (p.beta != 0.0) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int col = n0 + wn * 32 + 8 * j + 2 * t;
-      const bool ok0 = col < p.N && (!p.lower || row >= col);
-      const bool ok1 = col + 1 < p.N && (!p.lower || row >= col + 1);
-      if (ok0 && ok1) {
-        double2* cp = reinterpret_cast<double2*>(crow + col);
-        double2 v;
-        if (p.beta == 0.0) {
-          v.x = p.alpha * acc[i][j][0];
-          v.y = p.alpha * acc[i][j][1];
-        } else {
-          double2 o = *cp;
-          v.x = fma(p.beta, o.x, p.alpha * acc[i][j][0]);
-          v.y = fma(p.beta, o.y, p.alpha * acc[i][j][1]);
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              cv[i][j] = *reinterpret_cast<const double2*>(
+                  Cbase + static_cast<long long>(m0 + wm * 64 + 8 * (2 * half + i) + g) * p.ldc + n0 + wn * 32 +
+                  8 * j + 2 * t);
         }
-        *cp = v;
-      } else {
-        if (ok0) crow[col] = (p.beta == 0.0 ? 0.0 : p.beta * crow[col]) + p.alpha * acc[i][j][0];
-        if (ok1) crow[col + 1] = (p.beta == 0.0 ? 0.0 : p.beta * crow[col + 1]) + p.alpha * acc[i][j][1];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int ii = 2 * half + i;
+            double2 v;
+            if (p.beta != 0.0) {
+              v.x = fma(p.beta, cv[i][j].x, p.alpha * acc[ii][j][0]);
+              v.y = fma(p.beta, cv[i][j].y, p.alpha * acc[ii][j][1]);
+            } else {
+              v.x = p.alpha * acc[ii][j][0];
+              v.y = p.alpha * acc[ii][j][1];
+            }
+            *reinterpret_cast<double2*>(Cbase + static_cast<long long>(m0 + wm * 64 + 8 * ii + g) * p.ldc + n0 +
+                                        wn * 32 + 8 * j + 2 * t) = v;
+          }
+      }
+      continue;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = m0 + wm * 64 + 8 * i + g;
+      if (row >= p.M) continue;
+      double* crow = Cbase + static_cast<long long>(row) * p.ldc;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int col = n0 + wn * 32 + 8 * j + 2 * t;
+        const bool ok0 = col < p.N && (!p.lower || row >= col);
+        const bool ok1 = col + 1 < p.N && (!p.lower || row >= col + 1);
+        if (ok0 && ok1) {
+          double2* cp = reinterpret_cast<double2*>(crow + col);
+          double2 v;
+          if (p.beta == 0.0) {
+            v.x = p.alpha * acc[i][j][0];
+            v.y = p.alpha * acc[i][j][1];
+          } else {
+            double2 o = *cp;
+            v.x = fma(p.beta, o.x, p.alpha * acc[i][j][0]);
+            v.y = fma(p.beta, o.y, p.alpha * acc[i][j][1]);
+          }
+          *cp = v;
+        } else {
+          if (ok0) crow[col] = (p.beta == 0.0 ? 0.0 : p.beta * crow[col]) + p.alpha * acc[i][j][0];
+          if (ok1) crow[col + 1] = (p.beta == 0.0 ? 0.0 : p.beta * crow[col + 1]) + p.alpha * acc[i][j][1];
+        }
       }
     }
   }
@@ -274,6 +328,30 @@ bool make_tmap_f64_2d(CUtensorMap* tm, const double* base, uint64_t inner, uint6
 
 namespace {
 
+int num_sms() {
+  static int n[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!n[dev & 63]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev & 63] = v > 0 ? v : 148;
+  }
+  return n[dev & 63];
+}
+
+// Output tiles per persistent CTA: 2 once the launch has at least two waves of
+// tiles (the second tile's operands stream in under the first one's epilogue),
+// else 1 so small launches still spread over every SM.
+int tiles_per_cta(int total) {
+  static int forced = [] {
+    const char* e = getenv("SFX_GEMM_TILES_PER_CTA");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced > 0) return forced;
+  return total >= 2 * num_sms() ? 2 : 1;
+}
+
 template <bool TB, int G>
 cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double alpha, double beta, bool lower,
                            cudaStream_t stream) {
@@ -304,8 +382,15 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
   const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
   p.tiles_n = tn;
   p.tiles_per_task = lower ? tm * (tm + 1) / 2 : tm * tn;
+  p.ntasks = n;
+  const int total = p.tiles_per_task * n;
+  // persistent CTAs, at most tiles_per_cta() output tiles each: the operand
+  // ring streams the next tile during the epilogue, while SMs still free up
+  // often enough for high-priority (critical-path) kernels to get in
+  const int per = tiles_per_cta(total);
+  const int grid = (total + per - 1) / per;
   count_launch();
-  dgemm_dmma_kernel<TB, G><<<p.tiles_per_task * n, THREADS, SMEM_BYTES, stream>>>(p);
+  dgemm_dmma_kernel<TB, G><<<grid, THREADS, SMEM_BYTES, stream>>>(p);
   return cudaGetLastError();
 }
 

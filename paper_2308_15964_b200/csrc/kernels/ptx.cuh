@@ -64,9 +64,10 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, in
 // D(8x8) += A(8x4, row) * B(4x8, col), FP64.  Thread (g = lane>>2, t = lane&3)
 // holds a = A[g][t], b = B[t][g], d = D[g][2t..2t+1].
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
+  // not volatile: a pure register op the scheduler may interleave with loads
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
 }
 
 __device__ __forceinline__ double2 lds128(uint32_t addr) {
