@@ -55,6 +55,7 @@ struct GemmGroup {
   GemmOperands t[G];
   long long ldc;
   int ntasks;
+  int ksplit;  // > 1: split-K, partial products are atomically added into C (beta == 1)
   int M, N, K;
   int tiles_n, tiles_per_task;
   int lower;
@@ -72,12 +73,17 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
   uint64_t* empty = full + STAGES;
 
-  const int total = p.ntasks * p.tiles_per_task;
+  const int total = p.ntasks * p.tiles_per_task * p.ksplit;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ktiles = (p.K + BK - 1) / BK;
+  const int ktiles_all = (p.K + BK - 1) / BK;
+  const int kchunk = (ktiles_all + p.ksplit - 1) / p.ksplit;
 
-  // linear tile index -> (task, m0, n0); lower = triangular enumeration (bm >= bn)
-  auto coords = [&](int lin, int& task, int& m0, int& n0) {
+  // linear work index -> (task, m0, n0, k-slice); lower = triangular enumeration (bm >= bn)
+  auto coords = [&](int lin, int& task, int& m0, int& n0, int& kt0, int& kt1) {
+    const int ks = lin % p.ksplit;
+    lin /= p.ksplit;
+    kt0 = ks * kchunk;
+    kt1 = min(ktiles_all, kt0 + kchunk);
     task = lin / p.tiles_per_task;
     const int tile = lin - task * p.tiles_per_task;
     int bm, bn;
@@ -111,13 +117,13 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
     if (warp == CONSUMER_WARPS && lane == 0) {
       int it = 0;
       for (int lin = blockIdx.x; lin < total; lin += gridDim.x) {
-        int task, m0, n0;
-        coords(lin, task, m0, n0);
+        int task, m0, n0, kt0, kt1;
+        coords(lin, task, m0, n0, kt0, kt1);
         const CUtensorMap* tmA = &p.t[task].a;
         const CUtensorMap* tmB = &p.t[task].b;
         ptx::prefetch_tmap(tmA);
         ptx::prefetch_tmap(tmB);
-        for (int kt = 0; kt < ktiles; ++kt, ++it) {
+        for (int kt = kt0; kt < kt1; ++kt, ++it) {
           const int s = it % STAGES;
           if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           ptx::mbar_arrive_expect_tx(&full[s], A_STAGE + B_STAGE);
@@ -141,15 +147,15 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
   const int g = lane >> 2, t = lane & 3;
   int it = 0;
   for (int lin = blockIdx.x; lin < total; lin += gridDim.x) {
-    int task, m0, n0;
-    coords(lin, task, m0, n0);
+    int task, m0, n0, kt0, kt1;
+    coords(lin, task, m0, n0, kt0, kt1);
     double acc[8][4][2];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    for (int kt = 0; kt < ktiles; ++kt, ++it) {
+    for (int kt = kt0; kt < kt1; ++kt, ++it) {
       const int s = it % STAGES;
       ptx::mbar_wait(&full[s], (it / STAGES) & 1);
       const uint32_t aS = ptx::smem_u32(sA) + s * A_STAGE;
@@ -200,6 +206,22 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
     // Interior tiles batch all 32 C loads before any FMA/store so the loads
     // overlap (one HBM round trip per tile instead of one per fragment).
     double* const Cbase = p.t[task].C;
+    if (p.ksplit > 1) {
+      // split-K partial sum: C += alpha * acc (beta == 1 enforced by the launcher)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int row = m0 + wm * 64 + 8 * i + g;
+        if (row >= p.M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int col = n0 + wn * 32 + 8 * j + 2 * t;
+          double* cp = Cbase + static_cast<long long>(row) * p.ldc + col;
+          if (col < p.N && (!p.lower || row >= col)) atomicAdd(cp, p.alpha * acc[i][j][0]);
+          if (col + 1 < p.N && (!p.lower || row >= col + 1)) atomicAdd(cp + 1, p.alpha * acc[i][j][1]);
+        }
+      }
+      continue;
+    }
     const bool interior = !p.lower && m0 + BM <= p.M && n0 + BN <= p.N;
     if (interior) {
 #pragma unroll
@@ -383,7 +405,14 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
   p.tiles_n = tn;
   p.tiles_per_task = lower ? tm * (tm + 1) / 2 : tm * tn;
   p.ntasks = n;
-  const int total = p.tiles_per_task * n;
+  // Small launches (the critical-path GEMMs inside TRSM/POTRF) split K so that
+  // they still cover the SMs: each slice keeps >= 8 K-steps of 16.
+  p.ksplit = 1;
+  if (beta == 1.0) {
+    const int tiles = p.tiles_per_task * n, ksteps = (K + BK - 1) / BK;
+    while (tiles * p.ksplit * 2 <= num_sms() && ksteps / (p.ksplit * 2) >= 8) p.ksplit *= 2;
+  }
+  const int total = p.tiles_per_task * n * p.ksplit;
   // persistent CTAs, at most tiles_per_cta() output tiles each: the operand
   // ring streams the next tile during the epilogue, while SMs still free up
   // often enough for high-priority (critical-path) kernels to get in

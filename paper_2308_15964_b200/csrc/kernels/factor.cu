@@ -15,74 +15,116 @@ namespace sfx {
 namespace {
 
 constexpr int LEAF = 64;
-constexpr int TRSM_THREADS = 128;
 
-// X L^T = B for a leaf: one thread per row of B, n <= 64 columns.
-// x_j = (b_j - sum_{k<j} L[j][k] x_k) / L[j][j]
-__global__ void __launch_bounds__(TRSM_THREADS) trsm_leaf_kernel(double* B, long long ldb, int M, int n,
-                                                                   const double* L, long long ldl) {
-  extern __shared__ double trsm_smem[];
-  double(*Ls)[LEAF + 1] = reinterpret_cast<double(*)[LEAF + 1]>(trsm_smem);
-  double(*xs)[TRSM_THREADS] = reinterpret_cast<double(*)[TRSM_THREADS]>(trsm_smem + LEAF * (LEAF + 1));
+// X L^T = B for a leaf of <= 64 columns (L padded with identity to 64).
+// One thread per row of B: the row lives in registers and is solved
+// right-looking (x_j = b_j / L_jj, then b_i -= L_ij x_j for every i > j), so
+// each step is a run of independent FMAs instead of a dependent dot product.
+// B rows are staged through shared memory so global loads/stores coalesce.
+__global__ void __launch_bounds__(LEAF) trsm_leaf_kernel(double* B, long long ldb, int M, int n, const double* L,
+                                                         long long ldl) {
+  // one buffer, used as the B staging area and then as LsT[j][i] = L[i][j]
+  __shared__ double buf[LEAF][LEAF + 1];
   const int tid = threadIdx.x;
-  for (int e = tid; e < n * n; e += TRSM_THREADS) {
-    const int j = e / n, k = e % n;
-    Ls[j][k] = (k <= j) ? L[j * ldl + k] : 0.0;
+  const int r0 = blockIdx.x * LEAF;
+#pragma unroll 16
+  for (int e = tid; e < LEAF * LEAF; e += LEAF) {
+    const int i = e / LEAF, j = e % LEAF;  // coalesced over j
+    const int r = r0 + i;
+    buf[i][j] = (r < M && j < n) ? B[r * ldb + j] : 0.0;
   }
-  const int r = blockIdx.x * TRSM_THREADS + tid;
-  if (r < M)
-    for (int j = 0; j < n; ++j) xs[j][tid] = B[r * ldb + j];
   __syncthreads();
-  if (r < M) {
-    for (int j = 0; j < n; ++j) {
-      double s0 = xs[j][tid], s1 = 0.0;
-      int k = 0;
-      for (; k + 1 < j; k += 2) {
-        s0 = fma(-Ls[j][k], xs[k][tid], s0);
-        s1 = fma(-Ls[j][k + 1], xs[k + 1][tid], s1);
-      }
-      if (k < j) s0 = fma(-Ls[j][k], xs[k][tid], s0);
-      xs[j][tid] = (s0 + s1) / Ls[j][j];
-    }
-    for (int j = 0; j < n; ++j) B[r * ldb + j] = xs[j][tid];
+  double x[LEAF];
+#pragma unroll
+  for (int c = 0; c < LEAF; ++c) x[c] = buf[tid][c];
+  __syncthreads();
+#pragma unroll 16
+  for (int e = tid; e < LEAF * LEAF; e += LEAF) {
+    const int i = e / LEAF, j = e % LEAF;
+    double v = (i == j) ? 1.0 : 0.0;
+    if (i < n && j < n && j <= i) v = L[i * ldl + j];
+    buf[j][i] = v;
+  }
+  __syncthreads();
+  double(*LsT)[LEAF + 1] = buf;
+#pragma unroll
+  for (int j = 0; j < LEAF; ++j) {
+    x[j] = x[j] / LsT[j][j];
+#pragma unroll
+    for (int i = j + 1; i < LEAF; ++i) x[i] = fma(-LsT[j][i], x[j], x[i]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < LEAF; ++c) buf[tid][c] = x[c];
+  __syncthreads();
+#pragma unroll 16
+  for (int e = tid; e < LEAF * LEAF; e += LEAF) {
+    const int i = e / LEAF, j = e % LEAF;
+    const int r = r0 + i;
+    if (r < M && j < n) B[r * ldb + j] = buf[i][j];
   }
 }
 
-// In-place lower Cholesky of an n <= 64 leaf in shared memory (outer-product
-// form; the column scaling is deferred so each step needs one barrier).
+// In-place lower Cholesky of a <= 64 leaf (padded with identity): 256 threads,
+// each owning a 4x4 block of the lower triangle in registers (outer-product
+// form, column scaling deferred).  Column j is broadcast through a
+// double-buffered shared vector: one barrier and <= 16 FMAs per thread per step.
 __global__ void __launch_bounds__(256) potrf_leaf_kernel(double* A, long long lda, int n, int* info) {
-  __shared__ double As[LEAF][LEAF + 1];
+  __shared__ double colbuf[2][LEAF];
+  __shared__ double pivs[LEAF];
   const int tid = threadIdx.x;
-  for (int e = tid; e < n * n; e += 256) {
-    const int i = e / n, k = e % n;
-    As[i][k] = (k <= i) ? A[i * lda + k] : 0.0;
-  }
-  __syncthreads();
-  for (int j = 0; j < n; ++j) {
-    const double piv = As[j][j];
-    if (piv <= 0.0) {
-      if (tid == 0 && info) atomicCAS(info, 0, j + 1);
-      return;
+  const int ti = tid >> 4, tk = tid & 15;
+  const int R = ti * 4, C = tk * 4;
+  const bool active = tk <= ti;
+  double a[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = R + r, k = C + c;
+      double v = (i == k) ? 1.0 : 0.0;
+      if (active && i < n && k < n && k <= i) v = A[i * lda + k];
+      a[r][c] = v;
     }
-    const double inv = 1.0 / piv;
-    // trailing update A[i][k] -= A[i][j] * A[k][j] / A[j][j], j < k <= i
-    const int m = n - j - 1;
-    const int cnt = m * (m + 1) / 2;
-    for (int e = tid; e < cnt; e += 256) {
-      // e -> (ii, kk) with 0 <= kk <= ii < m
-      int ii = static_cast<int>((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
-      while ((ii + 1) * (ii + 2) / 2 <= e) ++ii;
-      while (ii * (ii + 1) / 2 > e) --ii;
-      const int kk = e - ii * (ii + 1) / 2;
-      const int i = j + 1 + ii, k = j + 1 + kk;
-      As[i][k] = fma(-As[i][j] * inv, As[k][j], As[i][k]);
+  for (int j = 0; j < LEAF; ++j) {
+    const int buf = j & 1;
+    if (active && tk == (j >> 2)) {
+      const int jj = j & 3;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const double v = jj == 0 ? a[r][0] : jj == 1 ? a[r][1] : jj == 2 ? a[r][2] : a[r][3];
+        colbuf[buf][R + r] = v;
+      }
     }
     __syncthreads();
+    const double piv = colbuf[buf][j];
+    if (tid == 0) pivs[j] = piv;
+    if (active && C + 3 > j) {
+      const double inv = 1.0 / piv;
+      double cr[4], cc[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) cr[r] = colbuf[buf][R + r] * inv;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cc[c] = colbuf[buf][C + c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (C + c > j && R + r >= C + c) a[r][c] = fma(-cr[r], cc[c], a[r][c]);
+    }
   }
-  for (int e = tid; e < n * n; e += 256) {
-    const int i = e / n, k = e % n;
-    if (k <= i) A[i * lda + k] = (i == k) ? sqrt(As[i][i]) : As[i][k] / sqrt(As[k][k]);
+  __syncthreads();
+  if (tid < LEAF && !(pivs[tid] > 0.0) && tid < n) {
+    if (info) atomicCAS(info, 0, tid + 1);
   }
+  if (!active) return;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = R + r, k = C + c;
+      if (i < n && k < n && k <= i) A[i * lda + k] = (i == k) ? sqrt(pivs[i]) : a[r][c] / sqrt(pivs[k]);
+    }
 }
 
 int split(int n) {
@@ -96,17 +138,8 @@ int split(int n) {
 cudaError_t launch_dtrsm(const double* L, long long ldl, double* B, long long ldb, int M, int n, cudaStream_t s) {
   if (M <= 0 || n <= 0) return cudaSuccess;
   if (n <= LEAF) {
-    constexpr int smem = (LEAF * (LEAF + 1) + LEAF * TRSM_THREADS) * 8;
-    static bool attr[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!attr[dev & 63]) {
-      cudaError_t e = cudaFuncSetAttribute(trsm_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e) return e;
-      attr[dev & 63] = true;
-    }
     count_launch();
-    trsm_leaf_kernel<<<(M + TRSM_THREADS - 1) / TRSM_THREADS, TRSM_THREADS, smem, s>>>(B, ldb, M, n, L, ldl);
+    trsm_leaf_kernel<<<(M + LEAF - 1) / LEAF, LEAF, 0, s>>>(B, ldb, M, n, L, ldl);
     return cudaGetLastError();
   }
   const int n1 = split(n), n2 = n - n1;

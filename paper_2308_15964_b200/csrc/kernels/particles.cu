@@ -26,8 +26,9 @@ namespace sfx {
 namespace {
 
 constexpr int THREADS = 128;
-constexpr int TPT = 4;  // targets per thread (ILP + one smem broadcast per 4 interactions)
-constexpr int TILE = 256;
+constexpr int TPT = 2;     // targets per thread (ILP + one smem broadcast per 2 interactions)
+constexpr int TILE = 256;  // sources staged per shared-memory round
+constexpr int SPLIT_SRC = 1024;  // sources per block: a task spreads over (targets/256) x (sources/1024) blocks
 
 // 1/sqrt(x) for normal x > 0 (r2 >= eps2 > 0 here): the MUFU.RSQ64H seed
 // (~23 bits) refined by two Newton steps (~46 -> full double).  4 FP64 ops per
@@ -55,7 +56,10 @@ __global__ void __launch_bounds__(THREADS) p2p_kernel(P2PSide s0, P2PSide s1, in
   __shared__ double4 sp[TILE];
   const bool second = blockIdx.x >= blocks0;
   const P2PSide& S = second ? s1 : s0;
-  const int blk = second ? blockIdx.x - blocks0 : blockIdx.x;
+  const int blk_lin = second ? blockIdx.x - blocks0 : blockIdx.x;
+  const int nsplit = (S.ns + SPLIT_SRC - 1) / SPLIT_SRC;
+  const int blk = blk_lin / nsplit, split = blk_lin - blk * nsplit;
+  const int j_begin = split * SPLIT_SRC, j_end = min(S.ns, j_begin + SPLIT_SRC);
   const int base = blk * THREADS * TPT;
   double xi[TPT], yi[TPT], zi[TPT];
   double ax[TPT], ay[TPT], az[TPT], ap[TPT];
@@ -69,12 +73,12 @@ __global__ void __launch_bounds__(THREADS) p2p_kernel(P2PSide s0, P2PSide s1, in
     zi[u] = S.tgt[2 * S.ld_t + t];
     ax[u] = ay[u] = az[u] = ap[u] = 0.0;
   }
-  for (int j0 = 0; j0 < S.ns; j0 += TILE) {
+  for (int j0 = j_begin; j0 < j_end; j0 += TILE) {
     __syncthreads();
     for (int k = threadIdx.x; k < TILE; k += THREADS) {
       const int j = j0 + k;
       double4 v;
-      if (j < S.ns) {
+      if (j < j_end) {
         v.x = S.src[j];
         v.y = S.src[S.ld_s + j];
         v.z = S.src[2 * S.ld_s + j];
@@ -86,7 +90,7 @@ __global__ void __launch_bounds__(THREADS) p2p_kernel(P2PSide s0, P2PSide s1, in
       sp[k] = v;
     }
     __syncthreads();
-    const int jn = min(TILE, S.ns - j0);
+    const int jn = min(TILE, j_end - j0);
 #pragma unroll 4
     for (int k = 0; k < jn; ++k) {
       const double4 p = sp[k];
@@ -109,11 +113,13 @@ __global__ void __launch_bounds__(THREADS) p2p_kernel(P2PSide s0, P2PSide s1, in
   for (int u = 0; u < TPT; ++u) {
     const int t = ti[u];
     if (t >= S.nt) continue;
+    // source splits of one task add into the same targets: FP64 atomics
+    // (the runtime already keeps different tasks of a commutative group apart)
     const double qa = S.tgt[3 * S.ld_t + t];
-    S.acc[t] += qa * ax[u];
-    S.acc[S.ld_a + t] += qa * ay[u];
-    S.acc[2 * S.ld_a + t] += qa * az[u];
-    S.acc[3 * S.ld_a + t] += ap[u];
+    atomicAdd(&S.acc[t], qa * ax[u]);
+    atomicAdd(&S.acc[S.ld_a + t], qa * ay[u]);
+    atomicAdd(&S.acc[2 * S.ld_a + t], qa * az[u]);
+    atomicAdd(&S.acc[3 * S.ld_a + t], ap[u]);
   }
 }
 
@@ -123,13 +129,13 @@ cudaError_t launch_p2p(const double* Pi, long long ldpi, int ni, const double* P
                        long long ldfi, double* Fj, long long ldfj, bool self, double eps2, cudaStream_t s) {
   const int per_block = THREADS * TPT;
   P2PSide a{Pi, self ? Pi : Pj, Fi, ldpi, self ? ldpi : ldpj, ldfi, ni, self ? ni : nj, self ? 1 : 0};
-  const int b0 = (ni + per_block - 1) / per_block;
+  const int b0 = (ni + per_block - 1) / per_block * ((a.ns + SPLIT_SRC - 1) / SPLIT_SRC);
   if (self) {
     count_launch();
     p2p_kernel<<<b0, THREADS, 0, s>>>(a, a, b0, eps2);
   } else {
     P2PSide b{Pj, Pi, Fj, ldpj, ldpi, ldfj, nj, ni, 0};
-    const int b1 = (nj + per_block - 1) / per_block;
+    const int b1 = (nj + per_block - 1) / per_block * ((b.ns + SPLIT_SRC - 1) / SPLIT_SRC);
     count_launch();
     p2p_kernel<<<b0 + b1, THREADS, 0, s>>>(a, b, b0, eps2);
   }
