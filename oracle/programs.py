@@ -16,11 +16,10 @@ Loop orders follow SURVEY.md §8c (the order of probe A.7):
                         for i>k: SYRK  r(A_ik) w(A_ii); for k<j<i: GEMM r(A_ik) r(A_jk) w(A_ij)
   particles:     for g: SELF r(P_g) cw(F_g);  for i<j: PAIR r(P_i) r(P_j) cw(F_i) cw(F_j)
 
-Priorities (used only with the priority scheduler, scheduler.py:97-126):
-critical-path tasks -- POTRF, TRSM and updates of the next panel column -- get
-10^6 on top of ``nt - k`` so step k+1's panel overtakes step k's trailing
-GEMMs (one-step lookahead); the GPU runtime launches priorities >= 10^6 on its
-high-priority CUDA streams.
+Priorities (used only with the priority scheduler, scheduler.py:97-126): a
+task is as urgent as the column of the tile it writes (earlier columns first);
+writes into the current or next panel column add 10^6, which the GPU runtime
+launches on its high-priority CUDA streams.
 """
 
 from __future__ import annotations
@@ -37,19 +36,25 @@ def gemm_program(nt: int):
     return prog
 
 
+def _chol_prio(nt, kind, k, i=0, j=0):
+    # same rule as paper_2308_15964_b200.algorithms.cholesky_priorities
+    col = {"potrf": k, "trsm": k, "syrk_sub": i, "gemm_nt_sub": j}[kind]
+    bonus = {"potrf": 3, "trsm": 2, "syrk_sub": 1, "gemm_nt_sub": 0}[kind]
+    p = (nt - col) * 4 + bonus + (1 if kind == "trsm" and i == k + 1 else 0)
+    return p + (1_000_000 if col <= k + 1 else 0)
+
+
 def cholesky_program(nt: int):
     prog = []
     for k in range(nt):
-        base = nt - k
-        crit = 1_000_000 + base
-        prog.append(("potrf", [(WRITE, ("A", k, k))], crit))
+        prog.append(("potrf", [(WRITE, ("A", k, k))], _chol_prio(nt, "potrf", k)))
         for i in range(k + 1, nt):
-            prog.append(("trsm", [(READ, ("A", k, k)), (WRITE, ("A", i, k))], crit))
+            prog.append(("trsm", [(READ, ("A", k, k)), (WRITE, ("A", i, k))], _chol_prio(nt, "trsm", k, i)))
         for i in range(k + 1, nt):
-            prog.append(("syrk_sub", [(READ, ("A", i, k)), (WRITE, ("A", i, i))], crit if i == k + 1 else base))
+            prog.append(("syrk_sub", [(READ, ("A", i, k)), (WRITE, ("A", i, i))], _chol_prio(nt, "syrk_sub", k, i)))
             for j in range(k + 1, i):
                 prog.append(("gemm_nt_sub", [(READ, ("A", i, k)), (READ, ("A", j, k)), (WRITE, ("A", i, j))],
-                             crit if j == k + 1 else base))
+                             _chol_prio(nt, "gemm_nt_sub", k, i, j)))
     return prog
 
 

@@ -117,15 +117,22 @@ URGENT = 1_000_000  # runtime default "urgent_priority": launched on high-priori
 
 
 def cholesky_priorities(nt: int, kind: str, k: int, i: int = 0, j: int = 0) -> int:
-    """Critical path first: POTRF, TRSM and next-column updates are urgent (>= URGENT),
-    earlier panels before later ones (nt - k)."""
-    base = nt - k
-    crit = URGENT + base
-    if kind in ("potrf", "trsm"):
-        return crit
-    if kind == "syrk":
-        return crit if i == k + 1 else base
-    return crit if j == k + 1 else base
+    """Priority of a Cholesky tile task: how soon its OUTPUT tile's column becomes a panel.
+
+    POTRF(k) and TRSM(i,k) write column k, SYRK(i,k) writes A_ii (column i),
+    GEMM(i,j,k) writes A_ij (column j).  Earlier columns first; tasks whose output
+    column is the current or next panel (<= k+1) are urgent (>= URGENT): they run on
+    the high-priority CUDA streams.  The next panel's TRSM is one above its
+    siblings so it launches alone, ahead of the grouped rest.
+    """
+    col = {"potrf": k, "trsm": k, "syrk": i, "gemm": j}[kind]
+    bonus = {"potrf": 3, "trsm": 2, "syrk": 1, "gemm": 0}[kind]
+    p = (nt - col) * 4 + bonus
+    if kind == "trsm" and i == k + 1:
+        p += 1
+    if col <= k + 1:
+        p += URGENT
+    return p
 
 
 def insert_cholesky(graph, A: TiledMatrix, fast: bool = True, priorities: bool = True):
@@ -143,7 +150,7 @@ def insert_cholesky(graph, A: TiledMatrix, fast: bool = True, priorities: bool =
     for k in range(nt):
         emit(ops.potrf, (write(A[k, k]),), P("potrf", k), "potrf")
         for i in range(k + 1, nt):
-            emit(ops.trsm, (read(A[k, k]), write(A[i, k])), P("trsm", k), "trsm")
+            emit(ops.trsm, (read(A[k, k]), write(A[i, k])), P("trsm", k, i), "trsm")
         for i in range(k + 1, nt):
             emit(ops.syrk_sub, (read(A[i, k]), write(A[i, i])), P("syrk", k, i), "syrk")
             for j in range(k + 1, i):

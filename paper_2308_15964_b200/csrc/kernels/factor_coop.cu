@@ -1,0 +1,477 @@
+// Single-launch (cooperative) tile DPOTRF and DTRSM for the Cholesky critical path.
+//
+// The recursive versions in factor.cu issue ~100 small dependent launches per
+// 1024x1024 tile; on the critical path (POTRF(k) -> TRSM(k+1,k) -> SYRK ->
+// POTRF(k+1)) the launch gaps and tiny grids dominate.  Here one cooperative
+// launch walks the 64-wide block columns with grid-wide barriers:
+//
+//   DPOTRF  for kb: [CTA 0] factor A_kk in registers, invert L_kk (64x64)
+//                   barrier; panel A_ik <- A_ik * inv(L_kk)^T (one CTA per block)
+//                   barrier; trailing A_ij -= A_ik A_jk^T (lower part of diagonal blocks)
+//                   barrier
+//   DTRSM   inverses of all 64x64 diagonal blocks of L (one CTA each); barrier;
+//           for kb: X_{:,kb} <- B_{:,kb} * inv(L_kk)^T; barrier;
+//                   B_{:,j} -= X_{:,kb} L_{j,kb}^T for j > kb; barrier
+//
+// Multiplying by the inverse of a 64x64 diagonal block (instead of substituting)
+// is the standard blocked-TRSM formulation; its error grows with cond(L_kk) of
+// the small block only.  Block products are 64x64x64 DFMA register tiles (4x4
+// per thread) from K-major shared memory (conflict-free LDS.128).
+// Oracle: oracle/bodies.py potrf / trsm (LAPACK semantics: upper triangle of
+// the POTRF tile untouched).
+#include <cooperative_groups.h>
+
+#include "kernels.h"
+
+namespace sfx {
+namespace {
+
+constexpr int T = 64;       // block size
+constexpr int P = T + 2;    // shared pitch (doubles): 528 B, 16-byte aligned rows
+constexpr int THREADS = 256;
+constexpr int COOP_GRID = 64;
+constexpr int SMEM = 3 * T * P * 8 + 2 * T * 8 + T * 8;
+
+struct Smem {
+  double a[T][P];  // K-major operand A (a[k][m])
+  double b[T][P];  // K-major operand B (b[k][n])
+  double c[T][P];  // scratch / row-major tile
+  double col[2][T];
+  double piv[T];
+};
+
+// Sense-free grid barrier: counter returns to 0, generation only grows.
+__device__ void grid_barrier(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = bar + 1;
+    const unsigned int g0 = *gen;
+    __threadfence();
+    const unsigned int arrived = atomicAdd(bar, 1u) + 1;
+    if (arrived == gridDim.x) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g0) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// dst[k][m] = src[m][k] (64x64 block, global row-major).  All 8 16-byte loads
+// of a thread are issued before any shared store: one memory round trip per block.
+__device__ __forceinline__ void load_T(double (*dst)[P], const double* src, long long ld) {
+  double2 v[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int e = threadIdx.x + u * THREADS;  // pair index: row m = e >> 5, cols 2*(e & 31)
+    v[u] = *reinterpret_cast<const double2*>(src + (e >> 5) * ld + 2 * (e & 31));
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int e = threadIdx.x + u * THREADS;
+    const int m = e >> 5, k = 2 * (e & 31);
+    dst[k][m] = v[u].x;
+    dst[k + 1][m] = v[u].y;
+  }
+}
+
+// dst[r][c] = src[r][c]
+__device__ __forceinline__ void load_N(double (*dst)[P], const double* src, long long ld) {
+  double2 v[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int e = threadIdx.x + u * THREADS;
+    v[u] = *reinterpret_cast<const double2*>(src + (e >> 5) * ld + 2 * (e & 31));
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int e = threadIdx.x + u * THREADS;
+    *reinterpret_cast<double2*>(&dst[e >> 5][2 * (e & 31)]) = v[u];
+  }
+}
+
+// acc[r][c] += sum_k A[m][k] B[n][k] over the thread's 4x4 patch (m = 4ty+r, n = 4tx+c),
+// operands K-major in shared memory
+__device__ __forceinline__ void mm_nt(double acc[4][4], const double (*AT)[P], const double (*BT)[P]) {
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+#pragma unroll 4
+  for (int k = 0; k < T; ++k) {
+    const double2 a01 = *reinterpret_cast<const double2*>(&AT[k][4 * ty]);
+    const double2 a23 = *reinterpret_cast<const double2*>(&AT[k][4 * ty + 2]);
+    const double2 b01 = *reinterpret_cast<const double2*>(&BT[k][4 * tx]);
+    const double2 b23 = *reinterpret_cast<const double2*>(&BT[k][4 * tx + 2]);
+    const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+    const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = fma(av[r], bv[c], acc[r][c]);
+  }
+}
+
+// In-place lower Cholesky of s.c (row-major 64x64, lower part valid) and
+// s.b <- inv(L)^T stored K-major for mm_nt (s.b[k][n] = inv(L)[n][k]).
+// Returns false (all threads) if a pivot is not positive.
+__device__ bool potrf_inv64(Smem& s) {
+  const int tid = threadIdx.x;
+  const int ti = tid >> 4, tk = tid & 15;
+  const int R = ti * 4, C = tk * 4;
+  const bool active = tk <= ti;
+  double a[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) a[r][c] = (active && C + c <= R + r) ? s.c[R + r][C + c] : 0.0;
+  for (int j = 0; j < T; ++j) {
+    const int buf = j & 1;
+    if (active && tk == (j >> 2)) {
+      const int jj = j & 3;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) s.col[buf][R + r] = jj == 0 ? a[r][0] : jj == 1 ? a[r][1] : jj == 2 ? a[r][2] : a[r][3];
+    }
+    __syncthreads();
+    const double piv = s.col[buf][j];
+    if (tid == 0) s.piv[j] = piv;
+    if (active && C + 3 > j) {
+      const double inv = 1.0 / piv;
+      double cr[4], cc[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) cr[r] = s.col[buf][R + r] * inv;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cc[c] = s.col[buf][C + c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (C + c > j && R + r >= C + c) a[r][c] = fma(-cr[r], cc[c], a[r][c]);
+    }
+  }
+  __syncthreads();
+  bool ok = true;
+  for (int j = 0; j < T; ++j) ok &= s.piv[j] > 0.0;
+  if (tid < T) s.col[0][tid] = sqrt(s.piv[tid]);  // sqrt(pivot) once per column
+  __syncthreads();
+  // L[i][k] = a / sqrt(piv_k), L[i][i] = sqrt(piv_i); zero above the diagonal
+  if (active) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = R + r, k = C + c;
+        if (k < i) s.c[i][k] = a[r][c] / s.col[0][k];
+        else if (k == i) s.c[i][k] = s.col[0][i];
+        else s.c[i][k] = 0.0;
+      }
+  } else {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) s.c[R + r][C + c] = 0.0;
+  }
+  __syncthreads();
+  return ok;
+}
+
+// s.b[k][n] = inv(L)[n][k] from a lower-triangular L in s.c (row-major).
+// X = inv(L) solves L X = I row by row: X[i][:] = (e_i - sum_{r<i} L[i][r] X[r][:]) / L[i][i].
+// Right-looking over all 256 threads: each owns a 4x4 patch of the running sums
+// acc[r][n] = sum_{q<i} L[r][q] X[q][n]; at step i the owners of row i finish it,
+// broadcast it through a double-buffered row, and everyone applies the rank-1
+// update -- one barrier and <= 16 FMAs per thread per step.
+__device__ void inv_lower64(Smem& s) {
+  const int tid = threadIdx.x;
+  const int ti = tid >> 4, tk = tid & 15;
+  const int R = ti * 4, C = tk * 4;
+  double acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+  for (int i = 0; i < T; ++i) {
+    const int buf = i & 1;
+    if (ti == (i >> 2)) {
+      const int ii = i & 3;
+      const double d = s.c[i][i];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double a = ii == 0 ? acc[0][c] : ii == 1 ? acc[1][c] : ii == 2 ? acc[2][c] : acc[3][c];
+        const int n = C + c;
+        const double x = n <= i ? ((n == i ? 1.0 : 0.0) - a) / d : 0.0;
+        s.col[buf][n] = x;       // row i of X
+        s.a[n][i] = x;           // K-major copy: a[n][i] = X[i][n] = inv[i][n]
+      }
+    }
+    __syncthreads();
+    if (R + 3 > i) {
+      double xr[4], lr[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) xr[c] = s.col[buf][C + c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) lr[r] = (R + r > i) ? s.c[R + r][i] : 0.0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = fma(lr[r], xr[c], acc[r][c]);
+    }
+  }
+  __syncthreads();
+  // b[k][n] = inv[n][k]: s.a[n][i] holds inv[i][n], i.e. a[x][y] = inv[y][x] -> b = a
+  for (int e = tid; e < T * T; e += THREADS) {
+    const int r = e >> 6, c = e & 63;
+    s.b[r][c] = s.a[r][c];
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void store_tile(double* dst, long long ld, const double acc[4][4], bool lower_only,
+                                           const double (*orig)[P]) {
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int i = 4 * ty + r;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int k = 4 * tx + c;
+      if (!lower_only || k <= i) dst[i * ld + k] = acc[r][c];
+      else if (orig) dst[i * ld + k] = orig[i][k];
+    }
+  }
+}
+
+// factor the diagonal block kb in place (lower), inverse^T (K-major) to ws
+__device__ void factor_block(Smem& s, double* A, long long lda, int kb, double* ws, int* info) {
+  const int tid = threadIdx.x;
+  double* Akk = A + (kb * T) * lda + kb * T;
+  load_N(s.c, Akk, lda);
+  __syncthreads();
+  const bool ok = potrf_inv64(s);
+  if (!ok && tid == 0 && info) atomicCAS(info, 0, kb * T + 1);
+  for (int e = tid; e < T * T; e += THREADS) {  // L back, original upper triangle kept
+    const int i = e >> 6, k = e & 63;
+    if (k <= i) Akk[i * lda + k] = s.c[i][k];
+  }
+  inv_lower64(s);
+  for (int e = tid; e < T * T; e += THREADS) ws[e] = s.b[e >> 6][e & 63];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(THREADS) potrf_coop_kernel(double* A, long long lda, int nb, unsigned int* bar,
+                                                              double* ws, int* info) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+  const int tid = threadIdx.x;
+  if (blockIdx.x == 0) factor_block(s, A, lda, 0, ws, info);
+  grid_barrier(bar);
+  for (int kb = 0; kb + 1 < nb; ++kb) {
+    // ---- panel: A_ik <- A_ik inv(L_kk)^T ----
+    const int npanel = nb - 1 - kb;
+    bool loaded = false;
+    for (int w = blockIdx.x; w < npanel; w += gridDim.x) {
+      if (!loaded) {
+        for (int e = tid; e < T * T; e += THREADS) s.b[e >> 6][e & 63] = ws[e];
+        loaded = true;
+      }
+      double* Aik = A + ((kb + 1 + w) * T) * lda + kb * T;
+      load_T(s.a, Aik, lda);
+      __syncthreads();
+      double acc[4][4] = {};
+      mm_nt(acc, s.a, s.b);
+      __syncthreads();
+      store_tile(Aik, lda, acc, false, nullptr);
+    }
+    grid_barrier(bar);
+    // ---- trailing update A_ij -= A_ik A_jk^T, kb < j <= i; work item 0 is the
+    //      next diagonal block: CTA 0 updates it first and factors it right away
+    //      (overlapping the next POTRF step with this step's trailing update) ----
+    const int ntiles = npanel * (npanel + 1) / 2;
+    for (int w = blockIdx.x; w < ntiles; w += gridDim.x) {
+      int ii = static_cast<int>((sqrtf(8.0f * w + 1.0f) - 1.0f) * 0.5f);
+      while ((ii + 1) * (ii + 2) / 2 <= w) ++ii;
+      while (ii * (ii + 1) / 2 > w) --ii;
+      const int jj = w - ii * (ii + 1) / 2;
+      const int ib = kb + 1 + ii, jb = kb + 1 + jj;
+      double* Aij = A + (ib * T) * lda + jb * T;
+      load_T(s.a, A + (ib * T) * lda + kb * T, lda);
+      load_T(s.b, A + (jb * T) * lda + kb * T, lda);
+      load_N(s.c, Aij, lda);
+      __syncthreads();
+      double acc[4][4];
+      const int ty = tid >> 4, tx = tid & 15;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+      mm_nt(acc, s.a, s.b);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = s.c[4 * ty + r][4 * tx + c] - acc[r][c];
+      __syncthreads();
+      store_tile(Aij, lda, acc, ib == jb, nullptr);
+      if (w == 0) {
+        __syncthreads();
+        factor_block(s, A, lda, kb + 1, ws, info);
+      }
+    }
+    grid_barrier(bar);
+  }
+}
+
+struct TrsmTask {
+  const double* L;
+  double* B;
+};
+
+constexpr int TRSM_GROUP_MAX = 32;
+
+struct TrsmGroup {
+  TrsmTask t[TRSM_GROUP_MAX];
+  int ntasks, mb, nb;
+  long long ldl, ldb;
+  unsigned int* bar;
+  double* ws;  // ntasks * nb inverse blocks (64 x 64, K-major inverse transpose)
+};
+
+// One cooperative launch solves X L^T = B for every task of the group (shared
+// barriers; work items are spread over the whole grid).
+__global__ void __launch_bounds__(THREADS) trsm_coop_kernel(const __grid_constant__ TrsmGroup g) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int mb = g.mb, nb = g.nb;
+  // ---- inverses of every diagonal block of every task's L ----
+  for (int w = blockIdx.x; w < g.ntasks * nb; w += gridDim.x) {
+    const int task = w / nb, j = w - task * nb;
+    const double* Ljj = g.t[task].L + (j * T) * g.ldl + j * T;
+    for (int e = tid; e < T * T; e += THREADS) {
+      const int i = e >> 6, k = e & 63;
+      s.c[i][k] = k <= i ? Ljj[i * g.ldl + k] : 0.0;
+    }
+    __syncthreads();
+    inv_lower64(s);
+    double* out = g.ws + static_cast<long long>(w) * T * T;
+    for (int e = tid; e < T * T; e += THREADS) out[e] = s.b[e >> 6][e & 63];
+    __syncthreads();
+  }
+  grid_barrier(g.bar);
+  for (int kb = 0; kb < nb; ++kb) {
+    // ---- X_{:,kb} = B_{:,kb} inv(L_kk)^T ----
+    for (int w = blockIdx.x; w < g.ntasks * mb; w += gridDim.x) {
+      const int task = w / mb, rb = w - task * mb;
+      const double* inv = g.ws + (static_cast<long long>(task) * nb + kb) * T * T;
+      for (int e = tid; e < T * T; e += THREADS) s.b[e >> 6][e & 63] = inv[e];
+      double* Bt = g.t[task].B + (rb * T) * g.ldb + kb * T;
+      load_T(s.a, Bt, g.ldb);
+      __syncthreads();
+      double acc[4][4] = {};
+      mm_nt(acc, s.a, s.b);
+      __syncthreads();
+      store_tile(Bt, g.ldb, acc, false, nullptr);
+    }
+    if (kb + 1 == nb) break;
+    grid_barrier(g.bar);
+    // ---- B_{:,j} -= X_{:,kb} L_{j,kb}^T, j > kb ----
+    const int ncol = nb - 1 - kb;
+    const int per_task = mb * ncol;
+    for (int w = blockIdx.x; w < g.ntasks * per_task; w += gridDim.x) {
+      const int task = w / per_task, t = w - task * per_task;
+      const int rb = t / ncol, jb = kb + 1 + t % ncol;
+      double* B = g.t[task].B;
+      double* Bt = B + (rb * T) * g.ldb + jb * T;
+      load_T(s.a, B + (rb * T) * g.ldb + kb * T, g.ldb);
+      load_T(s.b, g.t[task].L + (jb * T) * g.ldl + kb * T, g.ldl);
+      load_N(s.c, Bt, g.ldb);
+      __syncthreads();
+      double acc[4][4] = {};
+      mm_nt(acc, s.a, s.b);
+      const int ty = tid >> 4, tx = tid & 15;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = s.c[4 * ty + r][4 * tx + c] - acc[r][c];
+      __syncthreads();
+      store_tile(Bt, g.ldb, acc, false, nullptr);
+    }
+    grid_barrier(g.bar);
+  }
+}
+
+int num_sms_coop() {
+  static int n[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!n[dev & 63]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev & 63] = v > 0 ? v : 148;
+  }
+  return n[dev & 63];
+}
+
+bool set_smem_attrs() {
+  static bool done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done[dev & 63]) return true;
+  if (cudaFuncSetAttribute(potrf_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
+    return false;
+  if (cudaFuncSetAttribute(trsm_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
+    return false;
+  done[dev & 63] = true;
+  return true;
+}
+
+}  // namespace
+
+size_t coop_workspace_bytes(int n) { return 256 + static_cast<size_t>((n + T - 1) / T) * T * T * sizeof(double); }
+
+bool coop_supported(int M, int n) { return n % T == 0 && M % T == 0 && n >= T && n <= 4096; }
+
+cudaError_t launch_dpotrf_coop(double* A, long long lda, int n, int* info, void* workspace, cudaStream_t s) {
+  if (!set_smem_attrs()) return cudaErrorInvalidValue;
+  unsigned int* bar = static_cast<unsigned int*>(workspace);
+  double* ws = reinterpret_cast<double*>(static_cast<char*>(workspace) + 256);
+  int nb = n / T;
+  void* args[] = {&A, &lda, &nb, &bar, &ws, &info};
+  count_launch();
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(potrf_coop_kernel), dim3(COOP_GRID), dim3(THREADS), args,
+                                     SMEM, s);
+}
+
+cudaError_t launch_dtrsm_coop_group(const TrsmDesc* d, int ntasks, int M, int n, void* workspace, size_t ws_bytes,
+                                    cudaStream_t s) {
+  if (!set_smem_attrs()) return cudaErrorInvalidValue;
+  const int mb = M / T, nb = n / T;
+  for (int i0 = 0; i0 < ntasks; i0 += TRSM_GROUP_MAX) {
+    const int cnt = ntasks - i0 < TRSM_GROUP_MAX ? ntasks - i0 : TRSM_GROUP_MAX;
+    if (256 + static_cast<size_t>(cnt) * nb * T * T * sizeof(double) > ws_bytes) return cudaErrorMemoryAllocation;
+    TrsmGroup g;
+    for (int i = 0; i < cnt; ++i) {
+      g.t[i].L = d[i0 + i].L;
+      g.t[i].B = d[i0 + i].B;
+      if (d[i0 + i].ldl != d[i0].ldl || d[i0 + i].ldb != d[i0].ldb) return cudaErrorInvalidValue;
+    }
+    g.ntasks = cnt;
+    g.mb = mb;
+    g.nb = nb;
+    g.ldl = d[i0].ldl;
+    g.ldb = d[i0].ldb;
+    g.bar = static_cast<unsigned int*>(workspace);
+    g.ws = reinterpret_cast<double*>(static_cast<char*>(workspace) + 256);
+    // at most one CTA per SM: two concurrent cooperative grids always fit together
+    int grid = cnt * mb * (nb > 1 ? nb - 1 : 1);
+    if (grid > num_sms_coop()) grid = num_sms_coop();
+    if (grid < 1) grid = 1;
+    void* args[] = {&g};
+    count_launch();
+    cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(trsm_coop_kernel), dim3(grid), dim3(THREADS),
+                                                args, SMEM, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace sfx

@@ -34,6 +34,20 @@ cudaError_t launch_dgemm(const double* A, long long lda, const double* B, long l
                          int M, int N, int K, double alpha, double beta, bool trans_b, bool lower,
                          cudaStream_t stream);
 
+// cooperative (single-launch) factorization kernels, n and M multiples of 64;
+// workspace: per-stream scratch whose first 256 bytes are zero-initialised barrier words
+struct TrsmDesc {
+  const double* L;
+  long long ldl;
+  double* B;
+  long long ldb;
+};
+size_t coop_workspace_bytes(int n);
+bool coop_supported(int M, int n);
+cudaError_t launch_dpotrf_coop(double* A, long long lda, int n, int* info, void* workspace, cudaStream_t s);
+cudaError_t launch_dtrsm_coop_group(const TrsmDesc* d, int ntasks, int M, int n, void* workspace, size_t ws_bytes,
+                                    cudaStream_t s);
+
 cudaError_t launch_dtrsm(const double* L, long long ldl, double* B, long long ldb, int M, int n, cudaStream_t s);
 cudaError_t launch_dpotrf(double* A, long long lda, int n, int* info, cudaStream_t s);
 cudaError_t launch_p2p(const double* Pi, long long ldpi, int ni, const double* Pj, long long ldpj, int nj, double* Fi,

@@ -36,7 +36,9 @@ class CudaBackend : public Backend {
     int64_t base_ns = 0;
     int* info = nullptr;
     bool ready = false;
+    std::vector<void*> scratch;  // per stream (cooperative streams only)
   };
+  static constexpr size_t kScratchBytes = 64ull << 20;
 
  public:
   CudaBackend(int ndev, const int* ordinals) : devs_(ndev) {
@@ -51,7 +53,7 @@ class CudaBackend : public Backend {
   }
   bool is_sim() const override { return false; }
 
-  int init_device(int d, int, int nstreams, int nurgent, uint64_t bytes, std::string& err) override {
+  int init_device(int d, int, int nstreams, int nurgent, int ncoop, uint64_t bytes, std::string& err) override {
     Dev& D = *devs_[d];
     cudaError_t e = cudaSetDevice(D.ordinal);
     if (e) return cuda_err(e, "cudaSetDevice", err);
@@ -75,10 +77,17 @@ class CudaBackend : public Backend {
     cudaMemset(D.info, 0, sizeof(int));
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    D.streams.resize(nstreams + nurgent);
-    for (int s = 0; s < nstreams + nurgent; ++s) {
+    const int total = nstreams + nurgent + ncoop;
+    D.streams.resize(total);
+    D.scratch.assign(total, nullptr);
+    for (int s = 0; s < total; ++s) {
       e = cudaStreamCreateWithPriority(&D.streams[s], cudaStreamNonBlocking, s < nstreams ? least : greatest);
       if (e) return cuda_err(e, "cudaStreamCreate", err);
+      if (s >= nstreams + nurgent) {  // cooperative-kernel streams: barrier words + inverse blocks
+        e = cudaMalloc(&D.scratch[s], kScratchBytes);
+        if (e) return cuda_err(e, "scratch cudaMalloc", err);
+        cudaMemset(D.scratch[s], 0, kScratchBytes);
+      }
     }
     // peer access to every device initialised before this one (both ways)
     for (int o = 0; o < d; ++o) {
@@ -246,11 +255,21 @@ class CudaBackend : public Backend {
                          static_cast<int>(o[1].rows), static_cast<int>(o[0].cols), op.fp[0], op.fp[1], true, true, s);
         break;
       case SFX_OP_DTRSM:
-        e = launch_dtrsm(f64(o[0]), o[0].ld, f64(o[1]), o[1].ld, static_cast<int>(o[1].rows),
-                         static_cast<int>(o[1].cols), s);
+        if (devs_[d]->scratch[stream] && coop_supported(static_cast<int>(o[1].rows), static_cast<int>(o[1].cols))) {
+          TrsmDesc td{f64(o[0]), o[0].ld, f64(o[1]), o[1].ld};
+          e = launch_dtrsm_coop_group(&td, 1, static_cast<int>(o[1].rows), static_cast<int>(o[1].cols),
+                                      devs_[d]->scratch[stream], kScratchBytes, s);
+        } else {
+          e = launch_dtrsm(f64(o[0]), o[0].ld, f64(o[1]), o[1].ld, static_cast<int>(o[1].rows),
+                           static_cast<int>(o[1].cols), s);
+        }
         break;
       case SFX_OP_DPOTRF:
-        e = launch_dpotrf(f64(o[0]), o[0].ld, static_cast<int>(o[0].rows), devs_[d]->info, s);
+        if (devs_[d]->scratch[stream] && coop_supported(static_cast<int>(o[0].rows), static_cast<int>(o[0].rows)))
+          e = launch_dpotrf_coop(f64(o[0]), o[0].ld, static_cast<int>(o[0].rows), devs_[d]->info,
+                                 devs_[d]->scratch[stream], s);
+        else
+          e = launch_dpotrf(f64(o[0]), o[0].ld, static_cast<int>(o[0].rows), devs_[d]->info, s);
         break;
       case SFX_OP_P2P_PAIR:
         e = launch_p2p(f64(o[0]), o[0].ld, static_cast<int>(o[0].cols), f64(o[1]), o[1].ld, static_cast<int>(o[1].cols),
@@ -291,6 +310,16 @@ class CudaBackend : public Backend {
                                     f.ip[0] != 0, false, devs_[d]->streams[stream]);
       return cuda_err(e, "grouped dgemm launch", err);
     }
+    if (ops.size() > 1 && f.op == SFX_OP_DTRSM && devs_[d]->scratch[stream]) {
+      std::vector<TrsmDesc> td(ops.size());
+      for (size_t i = 0; i < ops.size(); ++i)
+        td[i] = TrsmDesc{static_cast<const double*>(ops[i].o[0].dptr), ops[i].o[0].ld,
+                         static_cast<double*>(ops[i].o[1].dptr), ops[i].o[1].ld};
+      cudaError_t e = launch_dtrsm_coop_group(td.data(), static_cast<int>(td.size()), static_cast<int>(f.o[1].rows),
+                                              static_cast<int>(f.o[1].cols), devs_[d]->scratch[stream],
+                                              kScratchBytes, devs_[d]->streams[stream]);
+      return cuda_err(e, "grouped cooperative dtrsm launch", err);
+    }
     for (const OpLaunch& op : ops) {
       int rc = launch(d, stream, op, err);
       if (rc) return rc;
@@ -321,6 +350,9 @@ class CudaBackend : public Backend {
       D.streams.clear();
       if (D.arena) cudaFree(D.arena);
       if (D.info) cudaFree(D.info);
+      for (void* p : D.scratch)
+        if (p) cudaFree(p);
+      D.scratch.clear();
       D.arena = nullptr;
       D.ready = false;
     }

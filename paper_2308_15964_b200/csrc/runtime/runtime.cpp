@@ -89,9 +89,10 @@ int Runtime::init(const uint64_t* arena_bytes, std::string& err) {
     auto dev = std::make_unique<Device>();
     dev->index = d;
     dev->queue.prio = sched_ == SFX_SCHED_PRIO;
-    dev->stream_inflight.assign(nstreams_ + nurgent_, 0);
-    dev->stream_groups.assign(nstreams_ + nurgent_, 0);
-    int rc = be_->init_device(d, d, nstreams_, nurgent_, arena_bytes ? arena_bytes[d] : 0, err);
+    if (be_->is_sim()) ncoop_ = 0;
+    dev->stream_inflight.assign(nstreams_ + nurgent_ + ncoop_, 0);
+    dev->stream_groups.assign(nstreams_ + nurgent_ + ncoop_, 0);
+    int rc = be_->init_device(d, d, nstreams_, nurgent_, ncoop_, arena_bytes ? arena_bytes[d] : 0, err);
     if (rc) return rc;
     dev->capacity = be_->arena_capacity(d);
     dev->free_bytes = dev->capacity;
@@ -931,10 +932,20 @@ int Runtime::issue(int d, int s, const std::vector<Task*>& group, std::vector<Ac
   return rc;
 }
 
+bool Runtime::is_coop(const Task* t) const {
+  if (ncoop_ == 0) return false;
+  if (t->op == SFX_OP_DPOTRF) return t->acc[0].h->rows % 64 == 0 && t->acc[0].h->rows <= 4096;
+  if (t->op == SFX_OP_DTRSM)
+    return t->acc[0].h->rows % 64 == 0 && t->acc[0].h->rows <= 4096 && t->acc[1].h->rows % 64 == 0;
+  return false;
+}
+
 bool Runtime::groupable(const Task* t) const {
   // only ops with a grouped kernel (one launch for the whole group) or trivial
   // generators: grouping anything else would serialise independent tasks on one stream
   switch (t->op) {
+    case SFX_OP_DTRSM:
+      return group_max_ > 1 && is_coop(t);  // grouped cooperative TRSM
     case SFX_OP_DGEMM:
     case SFX_OP_DSYRK:
     case SFX_OP_FILL_UNIFORM:
@@ -1020,7 +1031,7 @@ void Runtime::complete(Task* t) {
   if (trace_ && t->start && t->end) {
     t->t_start = be_->event_time_ns(t->dev, t->start->event);
     t->t_end = be_->event_time_ns(t->dev, t->end->event);
-    const int wid = t->dev * (nstreams_ + nurgent_) + t->stream;
+    const int wid = t->dev * (nstreams_ + nurgent_ + ncoop_) + t->stream;
     record(g, SFX_EV_START, t->t_start, wid, t->tid);
     record(g, SFX_EV_END, t->t_end, wid, t->tid);
   }
@@ -1068,6 +1079,7 @@ void Runtime::exec_loop(int d) {
     // urgent tasks prefer the high-priority streams and may fall back to normal
     // ones; normal tasks never take an urgent stream
     auto free_stream = [&](const Task* t) {
+      if (is_coop(t)) return free_in(nstreams_ + nurgent_, nstreams_ + nurgent_ + ncoop_);
       if (nurgent_ > 0 && t->prio >= urgent_priority_) {
         int s = free_in(nstreams_, nstreams_ + nurgent_);
         return s >= 0 ? s : free_in(0, nstreams_);
@@ -1094,6 +1106,7 @@ void Runtime::exec_loop(int d) {
         Task* nx = D.queue.peek();
         if (!same_signature(first, nx) || commute_conflict(group, nx) || (nx->prio >= urgent_priority_) != urgent)
           break;
+        if (first->op == SFX_OP_DTRSM && nx->prio != first->prio) break;  // a critical TRSM launches alone
         D.queue.pop();
         if (!nx->commute.empty() && !acquire_commute(nx)) continue;
         group.push_back(nx);
@@ -1109,7 +1122,7 @@ void Runtime::exec_loop(int d) {
       t->t_pop = tpop;
       t->end = gend;
       t->start = gstart;
-      record(graphs_[t->gid].get(), SFX_EV_POP, tpop, d * (nstreams_ + nurgent_) + s, t->tid);
+      record(graphs_[t->gid].get(), SFX_EV_POP, tpop, d * (nstreams_ + nurgent_ + ncoop_) + s, t->tid);
     }
     acts.clear();
     ops.assign(group.size(), OpLaunch());

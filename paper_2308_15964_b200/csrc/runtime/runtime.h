@@ -163,8 +163,10 @@ class Backend {
  public:
   virtual ~Backend() {}
   virtual bool is_sim() const = 0;
-  // nstreams normal-priority streams followed by nurgent highest-priority streams
-  virtual int init_device(int d, int ordinal, int nstreams, int nurgent, uint64_t arena_bytes, std::string& err) = 0;
+  // nstreams normal-priority streams, then nurgent highest-priority streams, then
+  // ncoop highest-priority streams reserved for cooperative (grid-barrier) kernels
+  virtual int init_device(int d, int ordinal, int nstreams, int nurgent, int ncoop, uint64_t arena_bytes,
+                          std::string& err) = 0;
   virtual void bind_thread(int d) = 0;
   virtual uint64_t arena_capacity(int d) = 0;
   virtual void* arena_ptr(int d, uint64_t off) = 0;
@@ -300,6 +302,10 @@ class Runtime {
   // then starts their CTAs first whenever an SM frees up (critical path)
   int nurgent_ = 0;
   int64_t urgent_priority_ = 1000000;
+  // cooperative POTRF/TRSM kernels run only on these (at most ncoop_ of them
+  // co-resident, so their grid barriers can never starve each other)
+  int ncoop_ = 2;
+  bool is_coop(const Task* t) const;
   uint64_t align_;
   bool trace_;
   std::mutex mu_;
