@@ -48,8 +48,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--n", type=int, default=16384)
-    ap.add_argument("--b", type=int, default=512)
+    ap.add_argument("--workload", choices=("gemm", "cholesky"), default="gemm",
+                    help="gemm: C2 tiled DGEMM (default, BASELINE configs[1]); cholesky: tiled Cholesky over "
+                         "all --gpus GPUs from one runtime (C3 at n=32768/1024, C5 at n=65536/1024)")
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--b", type=int, default=None)
     ap.add_argument("--streams", type=int, default=16)
     ap.add_argument("--group", type=int, default=32)
     ap.add_argument("--no-secondary", action="store_true")
@@ -188,6 +191,7 @@ def cpu_baseline(n: int, b: int, seconds: float):
 def run_reference(args, dist):
     if dist.rank != 0:
         return  # under torchrun only rank 0 runs the CPU reference
+    args.n, args.b = args.n or 16384, args.b or 512
     res = cpu_baseline(args.n, args.b, args.cpu_seconds)
     line = {
         "impl": "reference", "metric": METRIC, "value": res["value"], "unit": "GFLOP/s", "n_gpus": args.gpus,
@@ -394,6 +398,78 @@ def secondary(sf, alg, dev, args, peak_tf):
     return out
 
 
+def main_cholesky(args, dist):
+    """Tiled Cholesky over all GPUs of the node from ONE runtime (rank 0).
+
+    The STF runtime is a single-process multi-device engine (the reference's
+    WorkerTeam.of_host_and_device_workers(devices=N)); placement is owner-computes
+    on a 2-D block-cyclic tile distribution and remote panels move peer-to-peer
+    over NVLink.  Under torchrun, ranks > 0 only join the barriers.
+    """
+    import torch
+
+    import paper_2308_15964_b200 as sf
+    from paper_2308_15964_b200 import algorithms as alg
+
+    ndev = max(args.gpus, dist.world)
+    if dist.rank != 0:
+        dist.barrier()
+        return
+    n, b = args.n or 32768, args.b or 1024
+    nt = n // b
+    peak_tf, _ = sf.fp64_peak(0)
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(ndev, args.streams), scheduler="prio", trace=False,
+                           ordinals=list(range(ndev)), group_max=args.group)
+    M = alg.TiledMatrix(n, b, lower=True)
+    P, Q = alg.grid_shape(ndev)
+    times = []
+    clocks = ClockSampler(0)
+    for rep in range(args.warmup + args.steps):
+        g = sf.TaskGraph().compute_on(eng)
+        alg.block_cyclic(g, M, P, Q)
+        alg.insert_fill_spd(g, M, 3)
+        g.wait_all()
+        for d in range(ndev):
+            torch.cuda.synchronize(d)
+        if rep == args.warmup:
+            clocks.start()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        alg.insert_cholesky(g, M)
+        g.wait_all()
+        e1.record()
+        torch.cuda.synchronize()
+        if rep >= args.warmup:
+            times.append(e0.elapsed_time(e1) / 1e3)
+    clk = clocks.stop()
+    stats = [eng.stats(d) for d in range(ndev)]
+    eng.stop()
+    t = statistics.mean(times)
+    flops = alg.flops_cholesky(n)
+    value = flops / t / 1e9
+    ntasks = nt + nt * (nt - 1) + nt * (nt - 1) * (nt - 2) // 6  # potrf + trsm + syrk + gemm
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ndev, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic SPD (R+R^T)/2 + n*I, generated on device",
+        "config": {"workload": f"tiled Cholesky {n}x{n} fp64, {b}x{b} tiles, {ndev} GPU(s) from one runtime",
+                   "n": n, "b": b, "tasks": ntasks, "grid": [P, Q], "streams_per_gpu": args.streams,
+                   "parallelism": f"owner-computes 2-D block-cyclic {P}x{Q}, NVLink peer pulls",
+                   "l2": "working set (%.1f GiB) larger than L2" % (len(M.tiles) * b * b * 8 / 2 ** 30)},
+        "clocks": clk,
+        "pct_fp64_peak": 100.0 * value / 1e3 / (peak_tf * ndev),
+        "roofline": {"bound": "tensor", "achieved": value / 1e3 / ndev, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": value / 1e3 / ndev / peak_tf, "traffic": None,
+                     "peak_source": "FP64 DMMA peak measured in-run (sfx_fp64_peak), per GPU"},
+        "p2p_bytes": sum(s["bytes_p2p_in"] for s in stats),
+        "gpu_launches": stats[0]["kernel_launches"],
+    }
+    print(json.dumps(line), flush=True)
+    dist.barrier()
+
+
 def main():
     args = parse()
     dist = Dist()
@@ -401,7 +477,11 @@ def main():
         run_reference(args, dist)
         return
     dist.init("nccl")
-    main_ours(args, dist)
+    if args.workload == "cholesky":
+        main_cholesky(args, dist)
+    else:
+        args.n, args.b = args.n or 16384, args.b or 512
+        main_ours(args, dist)
     dist.done()
 
 

@@ -51,6 +51,24 @@ def potrf(A):
     A[il] = Lf[il]
 
 
+def potrf_inv(A, block=64):
+    """potrf + inv(L_jj)^T of each 64x64 diagonal block in its strict upper triangle."""
+    potrf(A)
+    n = A.shape[0]
+    for j0 in range(0, n, block):
+        j1 = min(n, j0 + block)
+        Ljj = np.tril(A[j0:j1, j0:j1])
+        inv = scipy.linalg.solve_triangular(Ljj, np.eye(j1 - j0), lower=True, check_finite=False)
+        iu = np.triu_indices(j1 - j0, 1)
+        blk = A[j0:j1, j0:j1]
+        blk[iu] = inv.T[iu]
+
+
+def trsm_inv(L, B):
+    """Same result as trsm (B L^-T); the operand's upper triangle is ignored."""
+    trsm(np.tril(L), B)
+
+
 def _one_side(Pt, Ps, Ft, eps2, self_pair, block=512):
     """F_t += interactions on targets Pt from sources Ps."""
     nt = Pt.shape[1]
@@ -93,6 +111,8 @@ BODIES = {
     "syrk_sub": syrk_sub,
     "trsm": trsm,
     "potrf": potrf,
+    "potrf_inv": potrf_inv,
+    "trsm_inv": trsm_inv,
     "p2p_pair": p2p_pair,
     "p2p_self": p2p_self,
     "noop": noop,
@@ -105,4 +125,6 @@ FLOPS = {
     "syrk_sub": lambda b: b ** 3,
     "trsm": lambda b: b ** 3,
     "potrf": lambda b: b ** 3 / 3,
+    "trsm_inv": lambda b: b ** 3,
+    "potrf_inv": lambda b: b ** 3 / 3,
 }

@@ -135,9 +135,18 @@ def cholesky_priorities(nt: int, kind: str, k: int, i: int = 0, j: int = 0) -> i
     return p
 
 
-def insert_cholesky(graph, A: TiledMatrix, fast: bool = True, priorities: bool = True):
-    """In-place right-looking tiled Cholesky of the lower tiles of A (A = L L^T)."""
+def insert_cholesky(graph, A: TiledMatrix, fast: bool = True, priorities: bool = True,
+                    inverse_blocks: bool = True):
+    """In-place right-looking tiled Cholesky of the lower tiles of A (A = L L^T).
+
+    ``inverse_blocks`` (default): POTRF also leaves the inverses of its 64x64
+    diagonal blocks in the diagonal tile's upper triangle and every TRSM runs as
+    DMMA GEMM sweeps on them.  The factor L (lower tiles) is the same; only the
+    otherwise unused upper triangle of the diagonal tiles differs.
+    """
     nt = A.nt
+    potrf_op = ops.potrf_inv if inverse_blocks else ops.potrf
+    trsm_op = ops.trsm_inv if inverse_blocks else ops.trsm
     P = (lambda *a: cholesky_priorities(nt, *a)) if priorities else (lambda *a: 0)
     batch = _emit(graph, fast)
 
@@ -148,9 +157,9 @@ def insert_cholesky(graph, A: TiledMatrix, fast: bool = True, priorities: bool =
             graph.task(*acc, device=op, priority=prio, name=name)
 
     for k in range(nt):
-        emit(ops.potrf, (write(A[k, k]),), P("potrf", k), "potrf")
+        emit(potrf_op, (write(A[k, k]),), P("potrf", k), "potrf")
         for i in range(k + 1, nt):
-            emit(ops.trsm, (read(A[k, k]), write(A[i, k])), P("trsm", k, i), "trsm")
+            emit(trsm_op, (read(A[k, k]), write(A[i, k])), P("trsm", k, i), "trsm")
         for i in range(k + 1, nt):
             emit(ops.syrk_sub, (read(A[i, k]), write(A[i, i])), P("syrk", k, i), "syrk")
             for j in range(k + 1, i):
@@ -206,6 +215,25 @@ def insert_fill_particles(graph, P: list, seed: int):
     for g, p in enumerate(P):
         batch.add(ops.fill_particles(seed, g * p.shape[1]), (write(p),), 0, "fill")
     return batch.submit()
+
+
+def block_cyclic(graph, M: TiledMatrix, P: int, Q: int) -> None:
+    """2-D block-cyclic ownership: tile (i, j) lives on device (i % P) * Q + (j % Q).
+
+    The locality-aware scheduler then runs every task on the owner of the tile
+    it writes (owner computes) and pulls remote operands peer-to-peer.
+    """
+    for (i, j), t in M.tiles.items():
+        graph.place(t, (i % P) * Q + (j % Q))
+
+
+def grid_shape(ndev: int):
+    """P x Q device grid with P <= Q, P*Q = ndev, P as large as possible (2x4 for 8)."""
+    P = 1
+    for p in range(1, ndev + 1):
+        if ndev % p == 0 and p * p <= ndev:
+            P = p
+    return P, ndev // P
 
 
 def flops_gemm(n: int) -> float:

@@ -56,6 +56,9 @@ struct GemmGroup {
   long long ldc;
   int ntasks;
   int ksplit;  // > 1: split-K, partial products are atomically added into C (beta == 1)
+  int tri;     // NN only: B is an upper-triangular block with a reciprocal diagonal
+               // (B[k][n] = 0 for k > n, 1/B[k][k] on the diagonal) -- the inverse
+               // blocks a store_inverses DPOTRF leaves in its tile's upper triangle
   int M, N, K;
   int tiles_n, tiles_per_task;
   int lower;
@@ -64,7 +67,7 @@ struct GemmGroup {
 
 constexpr int GROUP_MAX = 32;
 
-template <bool TRANS_B, int G>
+template <bool TRANS_B, int G, bool TRI>
 __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_constant__ GemmGroup<G> p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -189,6 +192,10 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
             for (int e = 0; e < 2; ++e) {
               const int k = 4 * t + 2 * h + e;
               b[j][e] = ptx::lds64(bS + q * 2048 + k * 128 + (((nn >> 1) ^ (k & 7)) << 4) + (nn & 1) * 8);
+              if (TRI) {
+                const int kg = kt * BK + k, ng = n0 + n;
+                b[j][e] = kg > ng ? 0.0 : (kg == ng ? 1.0 / b[j][e] : b[j][e]);
+              }
             }
           }
         }
@@ -374,14 +381,14 @@ int tiles_per_cta(int total) {
   return total >= 2 * num_sms() ? 2 : 1;
 }
 
-template <bool TB, int G>
+template <bool TB, int G, bool TRI = false>
 cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double alpha, double beta, bool lower,
-                           cudaStream_t stream) {
+                           bool tri, cudaStream_t stream) {
   static bool attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_set[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(dgemm_dmma_kernel<TB, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(dgemm_dmma_kernel<TB, G, TRI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set[dev & 63] = true;
@@ -401,6 +408,7 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
   p.alpha = alpha;
   p.beta = beta;
   p.lower = lower ? 1 : 0;
+  p.tri = tri ? 1 : 0;
   const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
   p.tiles_n = tn;
   p.tiles_per_task = lower ? tm * (tm + 1) / 2 : tm * tn;
@@ -419,14 +427,14 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
   const int per = tiles_per_cta(total);
   const int grid = (total + per - 1) / per;
   count_launch();
-  dgemm_dmma_kernel<TB, G><<<grid, THREADS, SMEM_BYTES, stream>>>(p);
+  dgemm_dmma_kernel<TB, G, TRI><<<grid, THREADS, SMEM_BYTES, stream>>>(p);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_dgemm_group(const GemmDesc* d, int n, int M, int N, int K, double alpha, double beta,
-                               bool trans_b, bool lower, cudaStream_t stream) {
+                               bool trans_b, bool lower, cudaStream_t stream, bool tri) {
   if (M <= 0 || N <= 0 || n <= 0) return cudaSuccess;
   if (K <= 0) return cudaErrorInvalidValue;
   for (int i = 0; i < n; ++i) {
@@ -439,11 +447,13 @@ cudaError_t launch_dgemm_group(const GemmDesc* d, int n, int M, int N, int K, do
     const int m = n - i0 < GROUP_MAX ? n - i0 : GROUP_MAX;
     cudaError_t e;
     if (m == 1)
-      e = trans_b ? launch_group_t<true, 1>(d + i0, 1, M, N, K, alpha, beta, lower, stream)
-                  : launch_group_t<false, 1>(d + i0, 1, M, N, K, alpha, beta, lower, stream);
+      e = trans_b ? launch_group_t<true, 1>(d + i0, 1, M, N, K, alpha, beta, lower, false, stream)
+                  : (tri ? launch_group_t<false, 1, true>(d + i0, 1, M, N, K, alpha, beta, lower, true, stream)
+                         : launch_group_t<false, 1>(d + i0, 1, M, N, K, alpha, beta, lower, false, stream));
     else
-      e = trans_b ? launch_group_t<true, GROUP_MAX>(d + i0, m, M, N, K, alpha, beta, lower, stream)
-                  : launch_group_t<false, GROUP_MAX>(d + i0, m, M, N, K, alpha, beta, lower, stream);
+      e = trans_b ? launch_group_t<true, GROUP_MAX>(d + i0, m, M, N, K, alpha, beta, lower, false, stream)
+                  : (tri ? launch_group_t<false, GROUP_MAX, true>(d + i0, m, M, N, K, alpha, beta, lower, true, stream)
+                         : launch_group_t<false, GROUP_MAX>(d + i0, m, M, N, K, alpha, beta, lower, false, stream));
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

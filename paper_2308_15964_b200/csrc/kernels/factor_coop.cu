@@ -21,6 +21,8 @@
 // the POTRF tile untouched).
 #include <cooperative_groups.h>
 
+#include <vector>
+
 #include "kernels.h"
 
 namespace sfx {
@@ -242,7 +244,7 @@ __device__ __forceinline__ void store_tile(double* dst, long long ld, const doub
 }
 
 // factor the diagonal block kb in place (lower), inverse^T (K-major) to ws
-__device__ void factor_block(Smem& s, double* A, long long lda, int kb, double* ws, int* info) {
+__device__ void factor_block(Smem& s, double* A, long long lda, int kb, double* ws, int* info, int store_inv) {
   const int tid = threadIdx.x;
   double* Akk = A + (kb * T) * lda + kb * T;
   load_N(s.c, Akk, lda);
@@ -254,16 +256,20 @@ __device__ void factor_block(Smem& s, double* A, long long lda, int kb, double* 
     if (k <= i) Akk[i * lda + k] = s.c[i][k];
   }
   inv_lower64(s);
-  for (int e = tid; e < T * T; e += THREADS) ws[e] = s.b[e >> 6][e & 63];
+  for (int e = tid; e < T * T; e += THREADS) {
+    const int r = e >> 6, c = e & 63;
+    ws[e] = s.b[r][c];
+    if (store_inv && r < c) Akk[r * lda + c] = s.b[r][c];  // inv(L_kk)[c][r] in the strict upper triangle
+  }
   __syncthreads();
 }
 
 __global__ void __launch_bounds__(THREADS) potrf_coop_kernel(double* A, long long lda, int nb, unsigned int* bar,
-                                                              double* ws, int* info) {
+                                                              double* ws, int* info, int store_inv) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x;
-  if (blockIdx.x == 0) factor_block(s, A, lda, 0, ws, info);
+  if (blockIdx.x == 0) factor_block(s, A, lda, 0, ws, info, store_inv);
   grid_barrier(bar);
   for (int kb = 0; kb + 1 < nb; ++kb) {
     // ---- panel: A_ik <- A_ik inv(L_kk)^T ----
@@ -313,7 +319,7 @@ __global__ void __launch_bounds__(THREADS) potrf_coop_kernel(double* A, long lon
       store_tile(Aij, lda, acc, ib == jb, nullptr);
       if (w == 0) {
         __syncthreads();
-        factor_block(s, A, lda, kb + 1, ws, info);
+        factor_block(s, A, lda, kb + 1, ws, info, store_inv);
       }
     }
     grid_barrier(bar);
@@ -430,12 +436,14 @@ size_t coop_workspace_bytes(int n) { return 256 + static_cast<size_t>((n + T - 1
 
 bool coop_supported(int M, int n) { return n % T == 0 && M % T == 0 && n >= T && n <= 4096; }
 
-cudaError_t launch_dpotrf_coop(double* A, long long lda, int n, int* info, void* workspace, cudaStream_t s) {
+cudaError_t launch_dpotrf_coop(double* A, long long lda, int n, int* info, void* workspace, cudaStream_t s,
+                               bool store_inverses) {
   if (!set_smem_attrs()) return cudaErrorInvalidValue;
   unsigned int* bar = static_cast<unsigned int*>(workspace);
   double* ws = reinterpret_cast<double*>(static_cast<char*>(workspace) + 256);
   int nb = n / T;
-  void* args[] = {&A, &lda, &nb, &bar, &ws, &info};
+  int store = store_inverses ? 1 : 0;
+  void* args[] = {&A, &lda, &nb, &bar, &ws, &info, &store};
   count_launch();
   return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(potrf_coop_kernel), dim3(COOP_GRID), dim3(THREADS), args,
                                      SMEM, s);
@@ -469,6 +477,32 @@ cudaError_t launch_dtrsm_coop_group(const TrsmDesc* d, int ntasks, int M, int n,
     count_launch();
     cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(trsm_coop_kernel), dim3(grid), dim3(THREADS),
                                                 args, SMEM, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_dtrsm_inv_group(const TrsmDesc* d, int ntasks, int M, int n, cudaStream_t s) {
+  // Right-looking blocked TRSM on the DMMA GEMM kernel; the 64x64 diagonal
+  // inverses come precomputed in L's upper triangle (store_inverses POTRF).
+  const int nb = n / T;
+  std::vector<GemmDesc> solve(ntasks), update(ntasks);
+  for (int kb = 0; kb < nb; ++kb) {
+    for (int i = 0; i < ntasks; ++i) {
+      const double* Lkk = d[i].L + (kb * T) * d[i].ldl + kb * T;
+      double* Bk = d[i].B + kb * T;
+      // X_kb = B_kb * inv(L_kk)^T : NN with B-operand[k][n] = inv[n][k] = Lkk_upper[k][n]
+      solve[i] = GemmDesc{Bk, d[i].ldb, Lkk, d[i].ldl, Bk, d[i].ldb};
+    }
+    cudaError_t e = launch_dgemm_group(solve.data(), ntasks, M, T, T, 1.0, 0.0, false, false, s, true);
+    if (e != cudaSuccess) return e;
+    const int rest = n - (kb + 1) * T;
+    if (rest <= 0) break;
+    for (int i = 0; i < ntasks; ++i) {
+      const double* Ljk = d[i].L + ((kb + 1) * T) * d[i].ldl + kb * T;  // rows kb+1.. of column block kb
+      update[i] = GemmDesc{d[i].B + kb * T, d[i].ldb, Ljk, d[i].ldl, d[i].B + (kb + 1) * T, d[i].ldb};
+    }
+    e = launch_dgemm_group(update.data(), ntasks, M, rest, T, -1.0, 1.0, true, false, s);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -15,6 +15,13 @@ inline void count_launch() { g_kernel_launches.fetch_add(1, std::memory_order_re
 bool make_tmap_f64_2d(CUtensorMap* tm, const double* base, uint64_t inner, uint64_t outer, uint64_t ld,
                       uint32_t box_inner, uint32_t box_outer, bool swizzle128);
 
+struct TrsmDesc {
+  const double* L;
+  long long ldl;
+  double* B;
+  long long ldb;
+};
+
 struct GemmDesc {
   const double* A;
   long long lda;
@@ -26,7 +33,13 @@ struct GemmDesc {
 
 // n independent same-shape GEMMs in grouped launches (up to 32 per launch)
 cudaError_t launch_dgemm_group(const GemmDesc* d, int n, int M, int N, int K, double alpha, double beta,
-                               bool trans_b, bool lower, cudaStream_t stream);
+                               bool trans_b, bool lower, cudaStream_t stream, bool tri = false);
+
+// X L^T = B for every task, L's 64x64 diagonal blocks carrying their inverses
+// (transposed, strict upper) in the upper triangle: for each 64-column panel,
+// X_kb = B_kb * inv(L_kk)^T (triangular NN DMMA GEMM, in place) then
+// B_j -= X_kb L_{j,kb}^T for the columns right of it (NT DMMA GEMM), all grouped
+cudaError_t launch_dtrsm_inv_group(const TrsmDesc* d, int ntasks, int M, int n, cudaStream_t s);
 
 // C = beta*C + alpha*A*op(B); op(B) = B^T ([N x K] storage) if trans_b else B ([K x N]).
 // lower: only row >= col of C is computed/stored (square C).
@@ -36,15 +49,12 @@ cudaError_t launch_dgemm(const double* A, long long lda, const double* B, long l
 
 // cooperative (single-launch) factorization kernels, n and M multiples of 64;
 // workspace: per-stream scratch whose first 256 bytes are zero-initialised barrier words
-struct TrsmDesc {
-  const double* L;
-  long long ldl;
-  double* B;
-  long long ldb;
-};
 size_t coop_workspace_bytes(int n);
 bool coop_supported(int M, int n);
-cudaError_t launch_dpotrf_coop(double* A, long long lda, int n, int* info, void* workspace, cudaStream_t s);
+// store_inverses: also leave inv(L_jj)^T of every 64x64 diagonal block in that
+// block's strict upper triangle (consumed by launch_dtrsm_inv_group)
+cudaError_t launch_dpotrf_coop(double* A, long long lda, int n, int* info, void* workspace, cudaStream_t s,
+                               bool store_inverses = false);
 cudaError_t launch_dtrsm_coop_group(const TrsmDesc* d, int ntasks, int M, int n, void* workspace, size_t ws_bytes,
                                     cudaStream_t s);
 

@@ -91,6 +91,7 @@ class CudaBackend : public Backend {
     }
     // peer access to every device initialised before this one (both ways)
     for (int o = 0; o < d; ++o) {
+      if (devs_[o]->ordinal == D.ordinal) continue;  // two logical devices on one GPU: plain device copies
       int can = 0;
       cudaDeviceCanAccessPeer(&can, D.ordinal, devs_[o]->ordinal);
       if (can) {
@@ -255,7 +256,11 @@ class CudaBackend : public Backend {
                          static_cast<int>(o[1].rows), static_cast<int>(o[0].cols), op.fp[0], op.fp[1], true, true, s);
         break;
       case SFX_OP_DTRSM:
-        if (devs_[d]->scratch[stream] && coop_supported(static_cast<int>(o[1].rows), static_cast<int>(o[1].cols))) {
+        if (op.ip[0] && coop_supported(static_cast<int>(o[1].rows), static_cast<int>(o[1].cols))) {
+          TrsmDesc td{f64(o[0]), o[0].ld, f64(o[1]), o[1].ld};
+          e = launch_dtrsm_inv_group(&td, 1, static_cast<int>(o[1].rows), static_cast<int>(o[1].cols), s);
+        } else if (devs_[d]->scratch[stream] &&
+                   coop_supported(static_cast<int>(o[1].rows), static_cast<int>(o[1].cols))) {
           TrsmDesc td{f64(o[0]), o[0].ld, f64(o[1]), o[1].ld};
           e = launch_dtrsm_coop_group(&td, 1, static_cast<int>(o[1].rows), static_cast<int>(o[1].cols),
                                       devs_[d]->scratch[stream], kScratchBytes, s);
@@ -267,7 +272,7 @@ class CudaBackend : public Backend {
       case SFX_OP_DPOTRF:
         if (devs_[d]->scratch[stream] && coop_supported(static_cast<int>(o[0].rows), static_cast<int>(o[0].rows)))
           e = launch_dpotrf_coop(f64(o[0]), o[0].ld, static_cast<int>(o[0].rows), devs_[d]->info,
-                                 devs_[d]->scratch[stream], s);
+                                 devs_[d]->scratch[stream], s, op.ip[0] != 0);
         else
           e = launch_dpotrf(f64(o[0]), o[0].ld, static_cast<int>(o[0].rows), devs_[d]->info, s);
         break;
@@ -309,6 +314,15 @@ class CudaBackend : public Backend {
                                     static_cast<int>(o[2].cols), static_cast<int>(o[0].cols), f.fp[0], f.fp[1],
                                     f.ip[0] != 0, false, devs_[d]->streams[stream]);
       return cuda_err(e, "grouped dgemm launch", err);
+    }
+    if (ops.size() > 1 && f.op == SFX_OP_DTRSM && f.ip[0]) {
+      std::vector<TrsmDesc> td(ops.size());
+      for (size_t i = 0; i < ops.size(); ++i)
+        td[i] = TrsmDesc{static_cast<const double*>(ops[i].o[0].dptr), ops[i].o[0].ld,
+                         static_cast<double*>(ops[i].o[1].dptr), ops[i].o[1].ld};
+      cudaError_t e = launch_dtrsm_inv_group(td.data(), static_cast<int>(td.size()), static_cast<int>(f.o[1].rows),
+                                             static_cast<int>(f.o[1].cols), devs_[d]->streams[stream]);
+      return cuda_err(e, "grouped dtrsm (inverse blocks) launch", err);
     }
     if (ops.size() > 1 && f.op == SFX_OP_DTRSM && devs_[d]->scratch[stream]) {
       std::vector<TrsmDesc> td(ops.size());

@@ -935,8 +935,8 @@ int Runtime::issue(int d, int s, const std::vector<Task*>& group, std::vector<Ac
 bool Runtime::is_coop(const Task* t) const {
   if (ncoop_ == 0) return false;
   if (t->op == SFX_OP_DPOTRF) return t->acc[0].h->rows % 64 == 0 && t->acc[0].h->rows <= 4096;
-  if (t->op == SFX_OP_DTRSM)
-    return t->acc[0].h->rows % 64 == 0 && t->acc[0].h->rows <= 4096 && t->acc[1].h->rows % 64 == 0;
+  if (t->op == SFX_OP_DTRSM)  // the inverse-block variant runs as ordinary DMMA GEMM launches
+    return !t->ip[0] && t->acc[0].h->rows % 64 == 0 && t->acc[0].h->rows <= 4096 && t->acc[1].h->rows % 64 == 0;
   return false;
 }
 
@@ -944,8 +944,8 @@ bool Runtime::groupable(const Task* t) const {
   // only ops with a grouped kernel (one launch for the whole group) or trivial
   // generators: grouping anything else would serialise independent tasks on one stream
   switch (t->op) {
-    case SFX_OP_DTRSM:
-      return group_max_ > 1 && is_coop(t);  // grouped cooperative TRSM
+    case SFX_OP_DTRSM:  // grouped cooperative TRSM, or grouped inverse-block GEMM sweeps
+      return group_max_ > 1 && (is_coop(t) || (t->ip[0] && t->acc[0].h->rows % 64 == 0));
     case SFX_OP_DGEMM:
     case SFX_OP_DSYRK:
     case SFX_OP_FILL_UNIFORM:
@@ -960,8 +960,9 @@ bool Runtime::groupable(const Task* t) const {
 
 bool Runtime::same_signature(const Task* a, const Task* b) const {
   if (a->op != b->op || a->acc.size() != b->acc.size()) return false;
+  const bool ip_matters = a->op == SFX_OP_DGEMM || a->op == SFX_OP_DTRSM || a->op == SFX_OP_DPOTRF;
   for (int k = 0; k < 4; ++k)
-    if (a->fp[k] != b->fp[k] || (a->op == SFX_OP_DGEMM && a->ip[k] != b->ip[k])) return false;
+    if (a->fp[k] != b->fp[k] || (ip_matters && a->ip[k] != b->ip[k])) return false;
   for (size_t k = 0; k < a->acc.size(); ++k) {
     const Handle* x = a->acc[k].h;
     const Handle* y = b->acc[k].h;

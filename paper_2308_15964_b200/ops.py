@@ -15,7 +15,9 @@ Operand conventions (tiles are 2-D row-major float64 arrays):
   dsyrk(alpha, beta)            A(r), C(w): lower(C) = beta*C + alpha*A*A^T
   syrk_sub                      lower(C) -= A @ A.T
   dtrsm()                       L(r), B(w): B = B * L^-T  (right, lower, trans)
-  dpotrf()                      A(w): lower(A) = chol(A)
+  dpotrf()                      A(w): lower(A) = chol(A) (upper untouched, LAPACK 'L')
+  dpotrf(store_inverses=True)   + inv(L_jj)^T of each 64x64 diagonal block in its strict upper
+  dtrsm(inverse_blocks=True)    B = B * L^-T using those blocks (DMMA GEMM sweeps)
   p2p_pair(eps2)                P_i(r), P_j(r), F_i(cw), F_j(cw)
   p2p_self(eps2)                P_i(r), F_i(cw)
   fill_uniform/fill_spd/fill_particles/zero   generators (write one tile)
@@ -57,12 +59,18 @@ def dsyrk(alpha: float = -1.0, beta: float = 1.0) -> Op:
     return Op("dsyrk", N.OP_DSYRK, (alpha, beta))
 
 
-def dtrsm() -> Op:
-    return Op("dtrsm", N.OP_DTRSM)
+def dtrsm(inverse_blocks: bool = False) -> Op:
+    """B = B L^-T.  ``inverse_blocks``: L's tile comes from ``dpotrf(store_inverses=True)``
+    and carries the inverses of its 64x64 diagonal blocks in its upper triangle, so the
+    solve runs as DMMA GEMM sweeps (x inverse block, then trailing update)."""
+    return Op("dtrsm_inv" if inverse_blocks else "dtrsm", N.OP_DTRSM, iparam=(1 if inverse_blocks else 0,))
 
 
-def dpotrf() -> Op:
-    return Op("dpotrf", N.OP_DPOTRF)
+def dpotrf(store_inverses: bool = False) -> Op:
+    """Lower Cholesky in place.  Default: LAPACK 'L' semantics (upper triangle untouched).
+    ``store_inverses``: the strict upper triangle of each 64x64 diagonal block receives
+    inv(L_jj)^T (for ``dtrsm(inverse_blocks=True)``); the factor L is identical."""
+    return Op("dpotrf_inv" if store_inverses else "dpotrf", N.OP_DPOTRF, iparam=(1 if store_inverses else 0,))
 
 
 def p2p_pair(eps2: float = 1e-9) -> Op:
@@ -109,3 +117,5 @@ gemm_nt_sub = dgemm(-1.0, 1.0, True)
 syrk_sub = dsyrk(-1.0, 1.0)
 trsm = dtrsm()
 potrf = dpotrf()
+trsm_inv = dtrsm(inverse_blocks=True)
+potrf_inv = dpotrf(store_inverses=True)

@@ -162,3 +162,28 @@ def test_particles_match_oracle(gpu_engine):
         denom = mag.sum(axis=1)
         dF = np.sqrt(((got[:3] - w[:3]) ** 2).sum(axis=0))
         assert (dF / denom).max() <= 1e-12
+
+
+@pytest.mark.parametrize("b", [256, 1024])
+def test_dpotrf_store_inverses_and_trsm_inverse_blocks(gpu_engine, b):
+    A0 = inputs.spd_tile(51, 0, 0, b, b, b)
+    A = A0.copy()
+    B0 = inputs.uniform_tile(52, 0, 0, b, b, b)
+    X = B0.copy()
+    def run(g):
+        g.task(sf.write(A), device=sf.ops.potrf_inv)
+        g.task(sf.read(A), sf.write(X), device=sf.ops.trsm_inv)
+    _run(gpu_engine, run)
+    want = A0.copy()
+    bodies.potrf_inv(want)
+    L = np.tril(A)
+    assert np.linalg.norm(A0 - L @ L.T) / np.linalg.norm(A0) <= 1e-12
+    # the strict upper triangle of every 64x64 diagonal block holds inv(L_jj)^T
+    for j0 in range(0, b, 64):
+        blk, wblk = A[j0:j0 + 64, j0:j0 + 64], want[j0:j0 + 64, j0:j0 + 64]
+        iu = np.triu_indices(64, 1)
+        assert np.abs(blk[iu] - wblk[iu]).max() <= 1e-12 * np.abs(wblk[iu]).max()
+    Xw = B0.copy()
+    bodies.trsm(np.tril(want), Xw)
+    assert np.linalg.norm(X - Xw) / np.linalg.norm(Xw) <= 1e-12
+    assert np.linalg.norm(X @ L.T - B0) / (np.linalg.norm(L) * np.linalg.norm(X)) <= 1e-13
