@@ -145,6 +145,7 @@ typedef struct sfx_dev_stats {
    * stream work outside it, releasing successors; completion-thread time;
    * number of launch groups */
   uint64_t t_plan_ns, t_issue_ns, t_release_ns, t_complete_ns, groups;
+  uint64_t prefetches; /* host->device copies staged ahead of the reading task */
 } sfx_dev_stats;
 
 typedef struct sfx_event {
@@ -201,8 +202,12 @@ int sfx_edges(sfx_runtime* rt, uint32_t gid, uint64_t* src, uint64_t* dst, uint6
 int sfx_violations(sfx_runtime* rt, uint64_t* n);
 
 /* tuning knobs: "group_max" (ready same-shape tasks fused into one grouped
- * launch, default 32; 1 disables grouping) and "window" (max in-flight tasks
- * per device) */
+ * launch, default 32; 1 disables grouping), "window" (max in-flight tasks per
+ * device), "groups_per_stream" (launches queued per stream, default 2),
+ * "urgent_priority" (priority from which tasks use the high-priority streams,
+ * default 1000000), "prefetch" (0/1: stage queued tasks' host operands while
+ * all streams are busy, default 1 on CUDA), "prefetch_depth" (queued tasks
+ * looked at, default 64) */
 int sfx_set_option(sfx_runtime* rt, const char* key, int64_t value);
 
 /* pinned host memory (cudaHostAlloc; aligned malloc in sim) for tiles */

@@ -87,7 +87,7 @@ class DevStats(ctypes.Structure):
         "bytes_to_device", "copies_to_device", "bytes_from_device", "copies_from_device",
         "bytes_p2p_in", "copies_p2p_in", "hits", "misses", "evictions", "writebacks",
         "blocks", "bytes_in_use", "capacity", "tasks_executed", "kernel_launches", "stream_waits",
-        "t_plan_ns", "t_issue_ns", "t_release_ns", "t_complete_ns", "groups")]
+        "t_plan_ns", "t_issue_ns", "t_release_ns", "t_complete_ns", "groups", "prefetches")]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

@@ -53,7 +53,8 @@ class CudaBackend : public Backend {
   }
   bool is_sim() const override { return false; }
 
-  int init_device(int d, int, int nstreams, int nurgent, int ncoop, uint64_t bytes, std::string& err) override {
+  int init_device(int d, int, int nstreams, int nurgent, int ncoop, int nprefetch, uint64_t bytes,
+                  std::string& err) override {
     Dev& D = *devs_[d];
     cudaError_t e = cudaSetDevice(D.ordinal);
     if (e) return cuda_err(e, "cudaSetDevice", err);
@@ -77,13 +78,13 @@ class CudaBackend : public Backend {
     cudaMemset(D.info, 0, sizeof(int));
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    const int total = nstreams + nurgent + ncoop;
+    const int total = nstreams + nurgent + ncoop + nprefetch;
     D.streams.resize(total);
     D.scratch.assign(total, nullptr);
     for (int s = 0; s < total; ++s) {
       e = cudaStreamCreateWithPriority(&D.streams[s], cudaStreamNonBlocking, s < nstreams ? least : greatest);
       if (e) return cuda_err(e, "cudaStreamCreate", err);
-      if (s >= nstreams + nurgent) {  // cooperative-kernel streams: barrier words + inverse blocks
+      if (s >= nstreams + nurgent && s < nstreams + nurgent + ncoop) {  // cooperative-kernel streams
         e = cudaMalloc(&D.scratch[s], kScratchBytes);
         if (e) return cuda_err(e, "scratch cudaMalloc", err);
         cudaMemset(D.scratch[s], 0, kScratchBytes);

@@ -29,7 +29,7 @@ class SimBackend : public Backend {
   explicit SimBackend(int ndev) : arenas_(ndev, nullptr), caps_(ndev, 0) {}
   ~SimBackend() override { shutdown(); }
   bool is_sim() const override { return true; }
-  int init_device(int d, int, int, int, int, uint64_t bytes, std::string& err) override {
+  int init_device(int d, int, int, int, int, int, uint64_t bytes, std::string& err) override {
     if (!bytes) bytes = 16ull << 20;  // reference default device_memory (engine.py:180)
     const uint64_t alloc = (bytes + 63) / 64 * 64;
     arenas_[d] = static_cast<uint8_t*>(aligned_alloc(64, alloc));

@@ -89,10 +89,13 @@ int Runtime::init(const uint64_t* arena_bytes, std::string& err) {
     auto dev = std::make_unique<Device>();
     dev->index = d;
     dev->queue.prio = sched_ == SFX_SCHED_PRIO;
-    if (be_->is_sim()) ncoop_ = 0;
-    dev->stream_inflight.assign(nstreams_ + nurgent_ + ncoop_, 0);
-    dev->stream_groups.assign(nstreams_ + nurgent_ + ncoop_, 0);
-    int rc = be_->init_device(d, d, nstreams_, nurgent_, ncoop_, arena_bytes ? arena_bytes[d] : 0, err);
+    if (be_->is_sim()) {
+      ncoop_ = 0;
+      prefetch_ = false;  // keeps the simulator's LRU behaviour identical to the reference
+    }
+    dev->stream_inflight.assign(nstreams_ + nurgent_ + ncoop_ + 1, 0);
+    dev->stream_groups.assign(nstreams_ + nurgent_ + ncoop_ + 1, 0);
+    int rc = be_->init_device(d, d, nstreams_, nurgent_, ncoop_, 1, arena_bytes ? arena_bytes[d] : 0, err);
     if (rc) return rc;
     dev->capacity = be_->arena_capacity(d);
     dev->free_bytes = dev->capacity;
@@ -543,6 +546,7 @@ void Runtime::push_ready(Task* t, int wid) {
   t->t_push = now_ns();
   record(graphs_[t->gid].get(), SFX_EV_PUSH, t->t_push, wid, t->tid);
   devs_[d]->queue.push(t);
+  devs_[d]->prefetch_pending = true;
   devs_[d]->exec_cv.notify_one();
 }
 
@@ -649,6 +653,10 @@ void Runtime::drop_block(Block* b, bool write_back, std::vector<Action>* acts, i
     D.stats.writebacks += 1;
   }
   if (h->dirty_dev == b->dev) h->dirty_dev = -1;
+  if (b->prefetched) {
+    b->prefetched = false;
+    b->pins -= 1;
+  }
   b->valid = false;
   b->dirty = false;
   h->blocks[b->dev] = nullptr;
@@ -723,7 +731,10 @@ int Runtime::ensure_block(int d, int s, Handle* h, std::vector<Action>& acts, st
     D.blocks[h->hid] = b;
     D.stats.blocks += 1;
   }
-  b->pins += 1;
+  if (b->prefetched)
+    b->prefetched = false;  // the prefetch's pin becomes this task's pin
+  else
+    b->pins += 1;
   tmp_pins.push_back(b);
   *out = b;
   return 0;
@@ -1061,6 +1072,62 @@ void Runtime::poison(int code, const std::string& msg) {
   done_cv_.notify_all();
 }
 
+int Runtime::plan_prefetch(int d, std::vector<Action>& acts) {
+  Device& D = *devs_[d];
+  const int s = pf_stream();
+  int issued = 0, seen = 0;
+  auto consider = [&](Task* t) {
+    if (t->op == SFX_OP_FLUSH) return;
+    for (auto& a : t->acc) {
+      Handle* h = a.h;
+      if (h->blocks[d] || !h->host_valid || h->dirty_dev >= 0) continue;
+      const uint64_t size = std::max<uint64_t>((h->bytes + align_ - 1) / align_ * align_, align_);
+      if (D.free_bytes < size + D.capacity / 8) return;
+      uint64_t off;
+      if (!alloc_space(d, size, &off)) return;
+      Block* b = new Block();
+      b->h = h;
+      b->dev = d;
+      b->off = off;
+      b->size = size;
+      b->pins = 1;
+      b->prefetched = true;
+      b->valid = true;
+      b->stamp = ++D.clock;
+      h->blocks[d] = b;
+      D.blocks[h->hid] = b;
+      D.stats.blocks += 1;
+      if (h->host_ready && !h->host_ready->complete) acts.push_back(Action{Action::WAIT, h->host_ready});
+      Action cp{Action::H2D, nullptr};
+      cp.host = h->host;
+      cp.dst_off = off;
+      cp.n = h->bytes;
+      acts.push_back(cp);
+      SyncP cs = new_sync(d, s, false);
+      acts.push_back(Action{Action::RECORD, cs});
+      b->ready = cs;
+      D.stats.bytes_to_device += h->bytes;
+      D.stats.copies_to_device += 1;
+      D.stats.prefetches += 1;
+      ++issued;
+    }
+  };
+  if (!D.queue.prio) {
+    for (Task* t : D.queue.fifo) {
+      if (++seen > prefetch_depth_) break;
+      consider(t);
+    }
+  } else {
+    std::vector<Task*> top(D.queue.heap);
+    std::sort(top.begin(), top.end(), [](const Task* a, const Task* b) { return heap_less(b, a); });
+    for (Task* t : top) {
+      if (++seen > prefetch_depth_) break;
+      consider(t);
+    }
+  }
+  return issued;
+}
+
 void Runtime::exec_loop(int d) {
   be_->bind_thread(d);
   Device& D = *devs_[d];
@@ -1087,11 +1154,29 @@ void Runtime::exec_loop(int d) {
       }
       return free_in(0, nstreams_);
     };
+    auto runnable = [&] {
+      return !paused_ && !fail_code_ && D.queue.size() > 0 && D.ninflight < static_cast<int>(window_) &&
+             free_stream(D.queue.peek()) >= 0;
+    };
     D.exec_cv.wait(lk, [&] {
-      return stopping_ || (!paused_ && !fail_code_ && D.queue.size() > 0 &&
-                           D.ninflight < static_cast<int>(window_) && free_stream(D.queue.peek()) >= 0);
+      return stopping_ || runnable() || (prefetch_ && D.prefetch_pending && !paused_ && !fail_code_);
     });
     if (stopping_) return;
+    if (!runnable()) {
+      // every stream is busy: stage operands of queued tasks meanwhile
+      D.prefetch_pending = false;
+      std::vector<Action> pacts;
+      if (plan_prefetch(d, pacts) > 0) {
+        lk.unlock();
+        std::string perr;
+        std::vector<Task*> none;
+        std::vector<OpLaunch> noops;
+        int prc = issue(d, pf_stream(), none, pacts, noops, perr);
+        lk.lock();
+        if (prc) poison(SFX_ERR_CUDA, perr);
+      }
+      continue;
+    }
     const int64_t t_busy0 = now_ns();
     // pop the head task, plus (grouped launch) the following ready tasks of the
     // same op and operand shapes -- up to group_max_, never two commutative
@@ -1427,6 +1512,10 @@ int Runtime::set_option(const std::string& key, int64_t value) {
     for (auto& d : devs_) d->exec_cv.notify_all();
   } else if (key == "urgent_priority") {
     urgent_priority_ = value;
+  } else if (key == "prefetch") {
+    prefetch_ = value != 0 && !be_->is_sim();
+  } else if (key == "prefetch_depth") {
+    prefetch_depth_ = static_cast<int>(std::max<int64_t>(0, value));
   } else if (key == "window") {
     window_ = static_cast<uint32_t>(std::max<int64_t>(1, value));
     for (auto& d : devs_) d->exec_cv.notify_all();

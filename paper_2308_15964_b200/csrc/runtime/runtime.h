@@ -82,6 +82,7 @@ struct Block {
   uint64_t stamp = 0;
   int pins = 0;
   bool valid = false, dirty = false, zombie = false;
+  bool prefetched = false;  // holds one pin for a not-yet-launched reader (prefetch)
   SyncP ready;  // contents valid once this completes (null: valid now)
 };
 
@@ -165,8 +166,8 @@ class Backend {
   virtual bool is_sim() const = 0;
   // nstreams normal-priority streams, then nurgent highest-priority streams, then
   // ncoop highest-priority streams reserved for cooperative (grid-barrier) kernels
-  virtual int init_device(int d, int ordinal, int nstreams, int nurgent, int ncoop, uint64_t arena_bytes,
-                          std::string& err) = 0;
+  virtual int init_device(int d, int ordinal, int nstreams, int nurgent, int ncoop, int nprefetch,
+                          uint64_t arena_bytes, std::string& err) = 0;
   virtual void bind_thread(int d) = 0;
   virtual uint64_t arena_capacity(int d) = 0;
   virtual void* arena_ptr(int d, uint64_t off) = 0;
@@ -234,6 +235,7 @@ struct Device {
   std::condition_variable exec_cv, comp_cv;
   std::thread exec_thread, comp_thread;
   sfx_dev_stats stats{};
+  bool prefetch_pending = false;  // ready queue changed since the last prefetch pass
 };
 
 class Runtime {
@@ -306,6 +308,13 @@ class Runtime {
   // co-resident, so their grid barriers can never starve each other)
   int ncoop_ = 2;
   bool is_coop(const Task* t) const;
+  // Prefetch: while every stream is busy, the executor stages host-resident
+  // operands of tasks waiting in its queue on a dedicated copy stream, so PCIe
+  // transfers overlap compute (never evicts; keeps capacity/8 free).
+  bool prefetch_ = true;
+  int prefetch_depth_ = 64;
+  int pf_stream() const { return nstreams_ + nurgent_ + ncoop_; }
+  int plan_prefetch(int d, std::vector<Action>& acts);
   uint64_t align_;
   bool trace_;
   std::mutex mu_;
