@@ -98,18 +98,26 @@ def _emit(graph, fast):
     return None
 
 
-def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: bool = True):
-    """C += A B over tiles, loop order i, j, k."""
+def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: bool = True,
+                priorities: bool = False):
+    """C += A B over tiles, loop order i, j, k.
+
+    ``priorities``: block row i gets priority nt - i, so with the priority
+    scheduler the rows of C finish one after another (a few rows in flight)
+    instead of every chain advancing in lock-step -- staging of A/C rows and the
+    flush of finished C tiles then overlap the remaining compute.
+    """
     nt = A.nt
     batch = _emit(graph, fast)
     for i in range(nt):
         for j in range(nt):
+            prio = nt - i if priorities else 0
             for k in range(nt):
                 acc = (read(A[i, k]), read(B[k, j]), write(C[i, j]))
                 if batch:
-                    batch.add(ops.gemm_nn, acc, 0, "gemm")
+                    batch.add(ops.gemm_nn, acc, prio, "gemm")
                 else:
-                    graph.task(*acc, device=ops.gemm_nn, name="gemm")
+                    graph.task(*acc, device=ops.gemm_nn, priority=prio, name="gemm")
     return batch.submit() if batch else None
 
 
