@@ -398,3 +398,61 @@ def test_cell_semantics():
         f.value = 1
     b = sf.Cell(True)
     assert b.value is True
+
+
+def test_cholesky_priorities_match_oracle_program():
+    from paper_2308_15964_b200.algorithms import cholesky_priorities as P
+
+    for nt in (2, 5, 8):
+        prog = programs.cholesky_program(nt)
+        mine = []
+        for k in range(nt):
+            mine.append(P(nt, "potrf", k))
+            for i in range(k + 1, nt):
+                mine.append(P(nt, "trsm", k, i))
+            for i in range(k + 1, nt):
+                mine.append(P(nt, "syrk", k, i))
+                for j in range(k + 1, i):
+                    mine.append(P(nt, "gemm", k, i, j))
+        assert mine == [p for _, _, p in prog]
+
+
+def test_block_cyclic_owner_computes_on_simulated_devices():
+    """Every task runs on the device that owns (home) the tile it writes; reads
+    of remote tiles arrive peer-to-peer; the dependency edges are the oracle's."""
+    from paper_2308_15964_b200 import algorithms as alg
+
+    nt, ndev = 6, 4
+    eng = sim_engine(devices=ndev, streams=2)
+    try:
+        g = sf.TaskGraph().compute_on(eng)
+        tiles = {(i, j): np.zeros(4) for i in range(nt) for j in range(i + 1)}
+        P, Q = alg.grid_shape(ndev)
+        owner = {ij: (ij[0] % P) * Q + (ij[1] % Q) for ij in tiles}
+        for ij, t in tiles.items():
+            g.place(t, owner[ij])
+        prog = programs.cholesky_program(nt)
+        tids, out_tile = [], {}
+        for kind, acc, prio in prog:
+            specs = [{"read": sf.read, "write": sf.write}[m](tiles[key[1:]]) for m, key in acc]
+            t = g.task(*specs, device=sf.ops.noop, priority=prio, name=kind)
+            tids.append(t.task_id)
+            out_tile[t.task_id] = [key[1:] for m, key in acc if m == "write"][0]
+        assert g.wait_all(timeout=60)
+        k = eng.streams_per_device
+        streams = k + (max(2, k // 4) if k >= 2 else 0)  # normal + urgent streams per device (sim: no coop)
+        pops = {tid: wid for kind, _, wid, tid, _ in g.trace.export_events() if kind == "Pop"}
+        for tid in tids:
+            dev = pops[tid] // streams
+            assert dev == owner[out_tile[tid]], (tid, dev, owner[out_tile[tid]])
+        assert sum(eng.stats(d)["copies_p2p_in"] for d in range(ndev)) > 0
+        want = stf_edges(prog)
+        assert edge_indices(g, tids) == sorted(want)
+    finally:
+        eng.stop()
+
+
+def stf_edges(prog):
+    from oracle import stf
+
+    return stf.static_successor_edges(programs.program_accesses(prog))
