@@ -433,11 +433,12 @@ def test_block_cyclic_owner_computes_on_simulated_devices():
             g.place(t, owner[ij])
         prog = programs.cholesky_program(nt)
         tids, out_tile = [], {}
-        for kind, acc, prio in prog:
-            specs = [{"read": sf.read, "write": sf.write}[m](tiles[key[1:]]) for m, key in acc]
-            t = g.task(*specs, device=sf.ops.noop, priority=prio, name=kind)
-            tids.append(t.task_id)
-            out_tile[t.task_id] = [key[1:] for m, key in acc if m == "write"][0]
+        with g.gated():  # static slot layout, comparable with the oracle's edges
+            for kind, acc, prio in prog:
+                specs = [{"read": sf.read, "write": sf.write}[m](tiles[key[1:]]) for m, key in acc]
+                t = g.task(*specs, device=sf.ops.noop, priority=prio, name=kind)
+                tids.append(t.task_id)
+                out_tile[t.task_id] = [key[1:] for m, key in acc if m == "write"][0]
         assert g.wait_all(timeout=60)
         k = eng.streams_per_device
         streams = k + (max(2, k // 4) if k >= 2 else 0)  # normal + urgent streams per device (sim: no coop)
