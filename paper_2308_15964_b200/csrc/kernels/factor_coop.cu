@@ -32,7 +32,7 @@ constexpr int T = 64;       // block size
 constexpr int P = T + 2;    // shared pitch (doubles): 528 B, 16-byte aligned rows
 constexpr int THREADS = 256;
 constexpr int COOP_GRID = 64;
-constexpr int SMEM = 3 * T * P * 8 + 2 * T * 8 + T * 8;
+constexpr int SMEM = 3 * T * P * 8 + 2 * T * 8 + T * 8 + 4 * 16 * 17 * 8 + 16;
 
 struct Smem {
   double a[T][P];  // K-major operand A (a[k][m])
@@ -40,6 +40,8 @@ struct Smem {
   double c[T][P];  // scratch / row-major tile
   double col[2][T];
   double piv[T];
+  double dinv[4][16][17];  // inverses of the four 16x16 diagonal sub-blocks
+  int bad;
 };
 
 // Sense-free grid barrier: counter returns to 0, generation only grows.
@@ -114,118 +116,230 @@ __device__ __forceinline__ void mm_nt(double acc[4][4], const double (*AT)[P], c
   }
 }
 
-// In-place lower Cholesky of s.c (row-major 64x64, lower part valid) and
-// s.b <- inv(L)^T stored K-major for mm_nt (s.b[k][n] = inv(L)[n][k]).
-// Returns false (all threads) if a pivot is not positive.
-__device__ bool potrf_inv64(Smem& s) {
+// ---- blocked 64x64 Cholesky + inverse: 16-wide sub-blocks factored and inverted
+//      by single warps (only __syncwarp), panel/trailing/inverse assembly by the
+//      whole CTA: ~20 CTA barriers per 64 block instead of ~130 ----
+
+// 1/sqrt(d) to ~1 ulp: MUFU approximation + two Newton steps (no slow-path
+// branch, no IEEE division on the dependent chain)
+__device__ __forceinline__ double rsqrt_refined(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  const double h = 0.5 * d;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+
+// warp: X = inv(L) column by column, right-looking: lane n holds column n of X
+// in x[]; after x[q] is final every later row k gets acc_k -= L[k][q] x[q].  The
+// dependent chain per step is one multiply + one fma (the shuffles of L[k][q]
+// do not depend on x and issue early).  rinv[q] = 1 / L[q][q].
+__device__ __forceinline__ void warp_trinv16(const double (&r)[16], const double (&rinv)[16], int n,
+                                             double (&x)[16]) {
+#pragma unroll
+  for (int q = 0; q < 16; ++q) x[q] = (q == n) ? 1.0 : 0.0;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    x[q] *= rinv[q];  // rows q < n stay exactly 0
+#pragma unroll
+    for (int k = 1; k < 16; ++k) {
+      if (k > q) {
+        const double lkq = __shfl_sync(0xffffffffu, r[q], k);  // L[k][q] from lane k
+        x[k] = fma(-lkq, x[q], x[k]);
+      }
+    }
+  }
+}
+
+// warp: in-place lower Cholesky of the 16x16 block c[o..o+16)^2 (Schur complement)
+// and its inverse into x.  Lane i (< 16) keeps row i in registers; columns are
+// broadcast with shuffles, so the 16 dependent steps need no shared-memory
+// round trips.  Every lane computes every pivot's 1/sqrt, so the inverse needs
+// no division at all.
+__device__ __forceinline__ void warp_potrf_inv16(double (*c)[P], int o, double (*x)[17], int* bad) {
+  const int lane = threadIdx.x & 31;
+  const int i = lane & 15;
+  double r[16], rinv[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) r[k] = (k <= i) ? c[o + i][o + k] : 0.0;
+  bool ok = true;
+#pragma unroll 16
+  for (int j = 0; j < 16; ++j) {
+    const double d = __shfl_sync(0xffffffffu, r[j], j);  // pivot (Schur complement) from lane j
+    ok &= d > 0.0;
+    const double rs = rsqrt_refined(d);
+    rinv[j] = rs;
+    // scale column j below the diagonal, then the rank-1 update of the trailing rows.
+    // selects, not `if (i == j) r[j] = ..`: equality propagation would turn that
+    // into r[i] (a dynamic index) and push r[] to local memory
+    const double rj = r[j];
+    r[j] = (i > j) ? rj * rs : ((i == j) ? d * rs : rj);
+    // fixed trip counts (k > j tested inside) so both loops unroll fully and
+    // r[] stays in registers; the test is warp-uniform, the shuffle is safe
+#pragma unroll
+    for (int k = 1; k < 16; ++k) {
+      if (k > j) {
+        const double lkj = __shfl_sync(0xffffffffu, r[j], k);  // L[k][j] from lane k
+        if (i >= k) r[k] = fma(-r[j], lkj, r[k]);
+      }
+    }
+  }
+  if (!ok && lane == 0) *bad = 1;
+  if (lane < 16) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k <= i) c[o + i][o + k] = r[k];
+  }
+  double xs[16];
+  warp_trinv16(r, rinv, i, xs);
+  if (lane < 16) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) x[q][i] = xs[q];
+  }
+  __syncwarp();
+}
+
+// warp: inverse of an already-factored lower 16x16 block (lane n: column n)
+__device__ __forceinline__ void warp_inv16(const double (*c)[P], int o, double (*x)[17]) {
+  const int lane = threadIdx.x & 31;
+  const int i = lane & 15;
+  double r[16], rinv[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) r[k] = (k <= i) ? c[o + i][o + k] : 0.0;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) rinv[q] = 1.0 / __shfl_sync(0xffffffffu, r[q], q);  // independent: ILP
+  double xs[16];
+  warp_trinv16(r, rinv, i, xs);
+  if (lane < 16) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) x[q][i] = xs[q];
+  }
+  __syncwarp();
+}
+
+// CTA: full inverse of the lower 64x64 L in s.c from the four 16x16 diagonal
+// inverses in s.dinv: X_pq = -D_p^{-1} sum_{q<=r<p} L_pr X_rq, block row by
+// block row.  Result: s.b[k][n] = inv(L)[n][k] (K-major operand for mm_nt);
+// s.a is scratch (row-major X).
+__device__ void assemble_inv64(Smem& s) {
   const int tid = threadIdx.x;
-  const int ti = tid >> 4, tk = tid & 15;
-  const int R = ti * 4, C = tk * 4;
-  const bool active = tk <= ti;
-  double a[4][4];
+  for (int e = tid; e < T * T; e += THREADS) {
+    const int i = e >> 6, n = e & 63;
+    const int p = i >> 4, q = n >> 4;
+    s.a[i][n] = (p == q) ? s.dinv[p][i & 15][n & 15] : 0.0;
+  }
+  __syncthreads();
+  for (int p = 1; p < 4; ++p) {
+    // T_pq = sum_{r=q}^{p-1} L_pr X_rq for every q < p (kept in registers, <= 3 per thread)
+    double t[3];
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) a[r][c] = (active && C + c <= R + r) ? s.c[R + r][C + c] : 0.0;
-  for (int j = 0; j < T; ++j) {
-    const int buf = j & 1;
-    if (active && tk == (j >> 2)) {
-      const int jj = j & 3;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) s.col[buf][R + r] = jj == 0 ? a[r][0] : jj == 1 ? a[r][1] : jj == 2 ? a[r][2] : a[r][3];
+    for (int u = 0; u < 3; ++u) {  // static register indices (no local-memory array)
+      const int e = tid + u * THREADS;
+      t[u] = 0.0;
+      if (e < p * 256) {
+        const int q = e >> 8, ii = (e >> 4) & 15, nn = e & 15;
+        const int i = 16 * p + ii, n = 16 * q + nn;
+        double acc = 0.0;
+        for (int k = 16 * q; k < 16 * p; ++k) acc = fma(s.c[i][k], s.a[k][n], acc);
+        t[u] = acc;
+      }
     }
     __syncthreads();
-    const double piv = s.col[buf][j];
-    if (tid == 0) s.piv[j] = piv;
-    if (active && C + 3 > j) {
-      const double inv = 1.0 / piv;
-      double cr[4], cc[4];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) cr[r] = s.col[buf][R + r] * inv;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) cc[c] = s.col[buf][C + c];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (C + c > j && R + r >= C + c) a[r][c] = fma(-cr[r], cc[c], a[r][c]);
+    for (int u = 0; u < 3; ++u) {  // park T in the (still zero) X_pq slots
+      const int e = tid + u * THREADS;
+      if (e < p * 256) s.a[16 * p + ((e >> 4) & 15)][16 * (e >> 8) + (e & 15)] = t[u];
     }
-  }
-  __syncthreads();
-  bool ok = true;
-  for (int j = 0; j < T; ++j) ok &= s.piv[j] > 0.0;
-  if (tid < T) s.col[0][tid] = sqrt(s.piv[tid]);  // sqrt(pivot) once per column
-  __syncthreads();
-  // L[i][k] = a / sqrt(piv_k), L[i][i] = sqrt(piv_i); zero above the diagonal
-  if (active) {
+    __syncthreads();
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int i = R + r, k = C + c;
-        if (k < i) s.c[i][k] = a[r][c] / s.col[0][k];
-        else if (k == i) s.c[i][k] = s.col[0][i];
-        else s.c[i][k] = 0.0;
+    for (int u = 0; u < 3; ++u) {  // X_pq = -D_p^{-1} T_pq
+      const int e = tid + u * THREADS;
+      if (e < p * 256) {
+        const int q = e >> 8, ii = (e >> 4) & 15, nn = e & 15;
+        double acc = 0.0;
+        for (int k = 0; k <= ii; ++k) acc = fma(s.dinv[p][ii][k], s.a[16 * p + k][16 * q + nn], acc);
+        t[u] = -acc;
       }
-  } else {
+    }
+    __syncthreads();
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) s.c[R + r][C + c] = 0.0;
+    for (int u = 0; u < 3; ++u) {
+      const int e = tid + u * THREADS;
+      if (e < p * 256) s.a[16 * p + ((e >> 4) & 15)][16 * (e >> 8) + (e & 15)] = t[u];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < T * T; e += THREADS) {
+    const int r = e >> 6, c = e & 63;
+    s.b[r][c] = s.a[c][r];  // b[k][n] = inv[n][k]
   }
   __syncthreads();
+}
+
+// CTA: s.c (row-major, lower part = SPD block) <- L (upper zeroed); s.b <- inv(L)^T
+// K-major.  Returns false if a pivot was not positive.
+__device__ bool factor64(Smem& s) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) s.bad = 0;
+  for (int e = tid; e < T * T; e += THREADS) {
+    const int i = e >> 6, k = e & 63;
+    if (k > i) s.c[i][k] = 0.0;
+  }
+  __syncthreads();
+  for (int p = 0; p < 4; ++p) {
+    const int o = 16 * p;
+    if (warp == 0) warp_potrf_inv16(s.c, o, s.dinv[p], &s.bad);
+    __syncthreads();
+    if (p == 3) break;
+    // panel rows below: c[r][o..o+16) <- c[r][o..o+16) * D_p^{-T}
+    const int rows = T - o - 16;
+    double v[3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int e = tid + u * THREADS;
+      v[u] = 0.0;
+      if (e < rows * 16) {
+        const int r = o + 16 + (e >> 4), q = e & 15;
+        double acc = 0.0;
+        for (int k = 0; k <= q; ++k) acc = fma(s.c[r][o + k], s.dinv[p][q][k], acc);
+        v[u] = acc;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int e = tid + u * THREADS;
+      if (e < rows * 16) s.c[o + 16 + (e >> 4)][o + (e & 15)] = v[u];
+    }
+    __syncthreads();
+    // trailing lower update: c[i][k] -= sum_q c[i][o+q] c[k][o+q], o+16 <= k <= i < 64
+    for (int e = tid; e < rows * rows; e += THREADS) {
+      const int i = o + 16 + e / rows, k = o + 16 + e % rows;
+      if (k > i) continue;
+      double acc = s.c[i][k];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc = fma(-s.c[i][o + q], s.c[k][o + q], acc);
+      s.c[i][k] = acc;
+    }
+    __syncthreads();
+  }
+  const bool ok = s.bad == 0;
+  assemble_inv64(s);
   return ok;
 }
 
-// s.b[k][n] = inv(L)[n][k] from a lower-triangular L in s.c (row-major).
-// X = inv(L) solves L X = I row by row: X[i][:] = (e_i - sum_{r<i} L[i][r] X[r][:]) / L[i][i].
-// Right-looking over all 256 threads: each owns a 4x4 patch of the running sums
-// acc[r][n] = sum_{q<i} L[r][q] X[q][n]; at step i the owners of row i finish it,
-// broadcast it through a double-buffered row, and everyone applies the rank-1
-// update -- one barrier and <= 16 FMAs per thread per step.
-__device__ void inv_lower64(Smem& s) {
-  const int tid = threadIdx.x;
-  const int ti = tid >> 4, tk = tid & 15;
-  const int R = ti * 4, C = tk * 4;
-  double acc[4][4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-  for (int i = 0; i < T; ++i) {
-    const int buf = i & 1;
-    if (ti == (i >> 2)) {
-      const int ii = i & 3;
-      const double d = s.c[i][i];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const double a = ii == 0 ? acc[0][c] : ii == 1 ? acc[1][c] : ii == 2 ? acc[2][c] : acc[3][c];
-        const int n = C + c;
-        const double x = n <= i ? ((n == i ? 1.0 : 0.0) - a) / d : 0.0;
-        s.col[buf][n] = x;       // row i of X
-        s.a[n][i] = x;           // K-major copy: a[n][i] = X[i][n] = inv[i][n]
-      }
-    }
-    __syncthreads();
-    if (R + 3 > i) {
-      double xr[4], lr[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) xr[c] = s.col[buf][C + c];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) lr[r] = (R + r > i) ? s.c[R + r][i] : 0.0;
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = fma(lr[r], xr[c], acc[r][c]);
-    }
-  }
-  __syncthreads();
-  // b[k][n] = inv[n][k]: s.a[n][i] holds inv[i][n], i.e. a[x][y] = inv[y][x] -> b = a
+// CTA: inverse of an already-factored lower 64x64 L in s.c (upper part ignored)
+__device__ void inv64_blocked(Smem& s) {
+  const int tid = threadIdx.x, warp = tid >> 5;
   for (int e = tid; e < T * T; e += THREADS) {
-    const int r = e >> 6, c = e & 63;
-    s.b[r][c] = s.a[r][c];
+    const int i = e >> 6, k = e & 63;
+    if (k > i) s.c[i][k] = 0.0;
   }
   __syncthreads();
+  if (warp < 4) warp_inv16(s.c, 16 * warp, s.dinv[warp]);
+  __syncthreads();
+  assemble_inv64(s);
 }
 
 __device__ __forceinline__ void store_tile(double* dst, long long ld, const double acc[4][4], bool lower_only,
@@ -249,13 +363,12 @@ __device__ void factor_block(Smem& s, double* A, long long lda, int kb, double* 
   double* Akk = A + (kb * T) * lda + kb * T;
   load_N(s.c, Akk, lda);
   __syncthreads();
-  const bool ok = potrf_inv64(s);
+  const bool ok = factor64(s);
   if (!ok && tid == 0 && info) atomicCAS(info, 0, kb * T + 1);
   for (int e = tid; e < T * T; e += THREADS) {  // L back, original upper triangle kept
     const int i = e >> 6, k = e & 63;
     if (k <= i) Akk[i * lda + k] = s.c[i][k];
   }
-  inv_lower64(s);
   for (int e = tid; e < T * T; e += THREADS) {
     const int r = e >> 6, c = e & 63;
     ws[e] = s.b[r][c];
@@ -357,7 +470,7 @@ __global__ void __launch_bounds__(THREADS) trsm_coop_kernel(const __grid_constan
       s.c[i][k] = k <= i ? Ljj[i * g.ldl + k] : 0.0;
     }
     __syncthreads();
-    inv_lower64(s);
+    inv64_blocked(s);
     double* out = g.ws + static_cast<long long>(w) * T * T;
     for (int e = tid; e < T * T; e += THREADS) out[e] = s.b[e >> 6][e & 63];
     __syncthreads();
