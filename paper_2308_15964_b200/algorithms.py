@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _native as N
 from . import ops
-from .access import commutative_write, read, write
+from .access import AccessMode, commutative_write, read, write
 from .memory import pinned_empty
 
 
@@ -66,30 +66,85 @@ class TiledMatrix:
 
 
 class _Batch:
-    """Accumulates task descriptors and submits them in one native call."""
+    """Accumulates task descriptors and submits them in native calls.
+
+    ``add`` takes one task (access specs); ``add_many`` takes a regular block of
+    tasks as arrays (one row of handle ids per task), built with numpy so that
+    the host cost per task is a few ns.  ``flush`` submits what is pending, so
+    long loops can hand work to the executors chunk by chunk while the rest is
+    still being built (insertion overlaps execution; program order is kept).
+    """
 
     def __init__(self, graph):
         self.g = graph
-        self.codes, self.fp, self.ip, self.prio, self.nacc, self.hids, self.modes, self.names = ([] for _ in range(8))
+        self._chunks = []  # (codes, fp, ip, prio, nacc, hids, modes, name-or-list)
+        self._single = None
+        self._tids = []
+
+    def _single_lists(self):
+        if self._single is None:
+            self._single = tuple([] for _ in range(8))
+        return self._single
 
     def add(self, op, accesses, priority=0, name=None):
-        self.codes.append(op.code)
-        self.fp.append(op.fparam)
-        self.ip.append(op.iparam)
-        self.prio.append(priority)
-        self.nacc.append(len(accesses))
+        codes, fp, ip, prio, nacc, hids, modes, names = self._single_lists()
+        codes.append(op.code)
+        fp.append(op.fparam)
+        ip.append(op.iparam)
+        prio.append(priority)
+        nacc.append(len(accesses))
         for spec in accesses:
-            self.hids.append(self.g.hid_of(spec.obj))
-            self.modes.append(spec.mode.code)
-        self.names.append(name)
+            hids.append(self.g.hid_of(spec.obj))
+            modes.append(spec.mode.code)
+        names.append(name)
+
+    def _close_single(self):
+        if self._single is not None and self._single[0]:
+            codes, fp, ip, prio, nacc, hids, modes, names = self._single
+            self._chunks.append((np.array(codes, np.uint32), np.array(fp, np.float64), np.array(ip, np.int64),
+                                 np.array(prio, np.int32), np.array(nacc, np.uint32), np.array(hids, np.uint64),
+                                 np.array(modes, np.uint32), names))
+        self._single = None
+
+    def add_many(self, op, hids, modes, priority=0, name=None):
+        """``hids``: (n, k) handle ids, row t = task t's accesses in declaration
+        order; ``modes``: the k access mode codes; ``priority``: scalar or (n,)."""
+        self._close_single()
+        hids = np.ascontiguousarray(hids, dtype=np.uint64)
+        n, k = hids.shape
+        if n == 0:
+            return
+        self._chunks.append((np.full(n, op.code, np.uint32), np.broadcast_to(np.array(op.fparam), (n, 4)),
+                             np.broadcast_to(np.array(op.iparam, np.int64), (n, 4)),
+                             np.broadcast_to(np.asarray(priority, np.int32), (n,)), np.full(n, k, np.uint32),
+                             hids.reshape(-1), np.tile(np.asarray(modes, np.uint32), n), name))
+
+    def flush(self):
+        self._close_single()
+        if not self._chunks:
+            return
+        ch, self._chunks = self._chunks, []
+        cat = [np.concatenate([c[f] for c in ch]) for f in range(7)]
+        names = ch[0][7] if len(ch) == 1 else None  # a block name (str) or per-task list
+        if len(ch) > 1 and any(c[7] is not None for c in ch):
+            names = []
+            for c in ch:
+                names.extend(c[7] if isinstance(c[7], list) else [c[7]] * len(c[0]))
+        self._tids.append(self.g.submit_arrays(*cat, names=names))
 
     def submit(self):
-        if not self.codes:
+        self.flush()
+        if not self._tids:
             return np.zeros(0, np.uint64)
-        return self.g.submit_arrays(np.array(self.codes, np.uint32), np.array(self.fp, np.float64),
-                                    np.array(self.ip, np.int64), np.array(self.prio, np.int32),
-                                    np.array(self.nacc, np.uint32), np.array(self.hids, np.uint64),
-                                    np.array(self.modes, np.uint32), names=self.names)
+        return np.concatenate(self._tids)
+
+
+def _hid_grid(graph, M):
+    """Handle ids of M's tiles as an (nt, nt) array (0 where a lower matrix has no tile)."""
+    H = np.zeros((M.nt, M.nt), np.uint64)
+    for (i, j), t in M.tiles.items():
+        H[i, j] = graph.hid_of(t)
+    return H
 
 
 def _emit(graph, fast):
@@ -108,17 +163,26 @@ def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: boo
     flush of finished C tiles then overlap the remaining compute.
     """
     nt = A.nt
-    batch = _emit(graph, fast)
+    if not fast:
+        for i in range(nt):
+            for j in range(nt):
+                prio = nt - i if priorities else 0
+                for k in range(nt):
+                    graph.task(read(A[i, k]), read(B[k, j]), write(C[i, j]), device=ops.gemm_nn,
+                               priority=prio, name="gemm")
+        return None
+    # same (i, j, k) task sequence, built as arrays and submitted one block row
+    # of C at a time so the executors start while later rows are being built
+    HA, HB, HC = _hid_grid(graph, A), _hid_grid(graph, B), _hid_grid(graph, C)
+    modes = (AccessMode.READ.code, AccessMode.READ.code, AccessMode.WRITE.code)
+    batch = _Batch(graph)
+    jj, kk = np.meshgrid(np.arange(nt), np.arange(nt), indexing="ij")
+    jj, kk = jj.reshape(-1), kk.reshape(-1)
     for i in range(nt):
-        for j in range(nt):
-            prio = nt - i if priorities else 0
-            for k in range(nt):
-                acc = (read(A[i, k]), read(B[k, j]), write(C[i, j]))
-                if batch:
-                    batch.add(ops.gemm_nn, acc, prio, "gemm")
-                else:
-                    graph.task(*acc, device=ops.gemm_nn, priority=prio, name="gemm")
-    return batch.submit() if batch else None
+        hids = np.stack([HA[i, kk], HB[kk, jj], HC[i, jj]], axis=1)
+        batch.add_many(ops.gemm_nn, hids, modes, nt - i if priorities else 0, "gemm")
+        batch.flush()
+    return batch.submit()
 
 
 URGENT = 1_000_000  # runtime default "urgent_priority": launched on high-priority CUDA streams
@@ -172,28 +236,35 @@ def insert_cholesky(graph, A: TiledMatrix, fast: bool = True, priorities: bool =
             emit(ops.syrk_sub, (read(A[i, k]), write(A[i, i])), P("syrk", k, i), "syrk")
             for j in range(k + 1, i):
                 emit(ops.gemm_nt_sub, (read(A[i, k]), read(A[j, k]), write(A[i, j])), P("gemm", k, i, j), "gemm")
+        if batch:
+            batch.flush()  # hand step k to the executors while step k+1 is built
     return batch.submit() if batch else None
 
 
 def insert_particles(graph, P: list, F: list, eps2: float = 1e-9, fast: bool = True):
     """All-pairs interactions between particle groups, commutative accumulation into F."""
     ng = len(P)
-    batch = _emit(graph, fast)
     self_op, pair_op = ops.p2p_self(eps2), ops.p2p_pair(eps2)
-    for g in range(ng):
-        acc = (read(P[g]), commutative_write(F[g]))
-        if batch:
-            batch.add(self_op, acc, 0, "p2p_self")
-        else:
-            graph.task(*acc, device=self_op, name="p2p_self")
-    for i in range(ng):
-        for j in range(i + 1, ng):
-            acc = (read(P[i]), read(P[j]), commutative_write(F[i]), commutative_write(F[j]))
-            if batch:
-                batch.add(pair_op, acc, 0, "p2p_pair")
-            else:
-                graph.task(*acc, device=pair_op, name="p2p_pair")
-    return batch.submit() if batch else None
+    if not fast:
+        for g in range(ng):
+            graph.task(read(P[g]), commutative_write(F[g]), device=self_op, name="p2p_self")
+        for i in range(ng):
+            for j in range(i + 1, ng):
+                graph.task(read(P[i]), read(P[j]), commutative_write(F[i]), commutative_write(F[j]),
+                           device=pair_op, name="p2p_pair")
+        return None
+    HP = np.array([graph.hid_of(p) for p in P], np.uint64)
+    HF = np.array([graph.hid_of(f) for f in F], np.uint64)
+    R, CW = AccessMode.READ.code, AccessMode.COMMUTATIVE_WRITE.code
+    batch = _Batch(graph)
+    batch.add_many(self_op, np.stack([HP, HF], axis=1), (R, CW), 0, "p2p_self")
+    batch.flush()
+    ii, jj = np.triu_indices(ng, 1)  # (i, j) pairs in loop order
+    pairs = np.stack([HP[ii], HP[jj], HF[ii], HF[jj]], axis=1)
+    for c0 in range(0, len(pairs), 4096):  # chunks: execution starts while the rest is submitted
+        batch.add_many(pair_op, pairs[c0:c0 + 4096], (R, R, CW, CW), 0, "p2p_pair")
+        batch.flush()
+    return batch.submit()
 
 
 def insert_fill_uniform(graph, M: TiledMatrix, seed: int):

@@ -172,7 +172,9 @@ class TaskGraph:
         self._entries = {}  # id(obj) -> _Entry
         self._by_hid = {}
         self._names = {}
+        self._name_ranges = []  # (first tid, count, name) of array submissions
         self._tids = []
+        self._tid_ranges = []   # (first tid, count) of array submissions
         self._inserter_ident = None
         self._batch = None
         self._desc_buf = ctypes.create_string_buffer(96)
@@ -318,11 +320,13 @@ class TaskGraph:
         acc["hid"] = acc_hids
         acc["mode"] = acc_modes
         N.check(N.lib.sfx_submit(self._h, n, descs.ctypes.data, acc.ctypes.data if len(acc) else None), self._h)
-        self._tids.extend(int(t) for t in tids)
-        if names is not None:
-            for t, nm in zip(tids, names):
+        self._tid_ranges.append((first, n))
+        if isinstance(names, str):  # one name for the whole block
+            self._name_ranges.append((first, n, names))
+        elif names is not None:
+            for t, nm in zip(tids.tolist(), names):
                 if nm is not None:
-                    self._names[int(t)] = nm
+                    self._names[t] = nm
         return tids
 
     @contextlib.contextmanager
@@ -420,10 +424,18 @@ class TaskGraph:
 
     # -- export -----------------------------------------------------------------
     def _label(self, tid) -> str:
-        return self._names.get(tid) or f"task{tid}"
+        nm = self._names.get(tid)
+        if nm is None:
+            for first, n, rn in self._name_ranges:
+                if first <= tid < first + n:
+                    return rn
+        return nm or f"task{tid}"
 
     def all_task_ids(self) -> list:
-        return list(self._tids)
+        ids = list(self._tids)
+        for first, n in self._tid_ranges:
+            ids.extend(range(first, first + n))
+        return sorted(ids)
 
     def edges(self) -> list:
         """Successor edges (src tid, dst tid, hid), one per handle pair (trace.py:94-102)."""
