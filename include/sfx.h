@@ -68,6 +68,8 @@ extern "C" {
                               tile ops are refused with SFX_ERR_UNSUPPORTED       */
 #define SFX_FLAG_TRACE 2u  /* record Push/Pop/Start/End (CUDA-event timestamps)     */
 #define SFX_FLAG_PAUSED 4u /* start with executors held (gated insertion)           */
+#define SFX_FLAG_KTIME 8u  /* time every launch group on its stream (CUDA events):
+                              sfx_dev_stats.timed_* (bench roofline)              */
 
 /* ---- schedulers (scheduler.py:66-126) ---- */
 #define SFX_SCHED_FIFO 0
@@ -146,6 +148,12 @@ typedef struct sfx_dev_stats {
    * number of launch groups */
   uint64_t t_plan_ns, t_issue_ns, t_release_ns, t_complete_ns, groups;
   uint64_t prefetches; /* host->device copies staged ahead of the reading task */
+  /* SFX_FLAG_KTIME (or TRACE): launch groups timed start->end with CUDA events
+   * recorded on the launching stream (after its stream waits), the tasks they
+   * carried, the summed group durations and the union of the group intervals
+   * (device time with at least one timed group running; folded in when
+   * sfx_stats is called) */
+  uint64_t timed_groups, timed_tasks, timed_ns, busy_ns;
 } sfx_dev_stats;
 
 typedef struct sfx_event {

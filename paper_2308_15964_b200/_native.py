@@ -38,6 +38,7 @@ READ, WRITE, ATOMIC_WRITE, COMMUTATIVE_WRITE, MAYBE_WRITE = 0, 1, 2, 3, 4
 FLAG_SIM = 1
 FLAG_TRACE = 2
 FLAG_PAUSED = 4
+FLAG_KTIME = 8
 
 SCHED_FIFO, SCHED_PRIO = 0, 1
 
@@ -87,7 +88,8 @@ class DevStats(ctypes.Structure):
         "bytes_to_device", "copies_to_device", "bytes_from_device", "copies_from_device",
         "bytes_p2p_in", "copies_p2p_in", "hits", "misses", "evictions", "writebacks",
         "blocks", "bytes_in_use", "capacity", "tasks_executed", "kernel_launches", "stream_waits",
-        "t_plan_ns", "t_issue_ns", "t_release_ns", "t_complete_ns", "groups", "prefetches")]
+        "t_plan_ns", "t_issue_ns", "t_release_ns", "t_complete_ns", "groups", "prefetches",
+        "timed_groups", "timed_tasks", "timed_ns", "busy_ns")]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

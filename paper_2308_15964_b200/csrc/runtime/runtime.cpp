@@ -79,7 +79,8 @@ Runtime::Runtime(Backend* be, int ndev, int nstreams, uint32_t sched, uint32_t f
       flags_(flags),
       window_(window ? window : 4096u),
       align_(align),
-      trace_((flags & SFX_FLAG_TRACE) != 0) {
+      trace_((flags & SFX_FLAG_TRACE) != 0),
+      ktime_((flags & (SFX_FLAG_TRACE | SFX_FLAG_KTIME)) != 0) {
   paused_ = (flags & SFX_FLAG_PAUSED) != 0;
   nurgent_ = nstreams >= 2 ? std::max(2, nstreams / 4) : 0;
 }
@@ -768,8 +769,8 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
     }
   }
   if (!t->end) {
-    t->end = new_sync(d, s, trace_);
-    if (trace_) t->start = new_sync(d, s, true);
+    t->end = new_sync(d, s, ktime_);
+    if (ktime_) t->start = new_sync(d, s, true);
   }
   for (const SyncP& w : t->waits) wait_on(w);
   for (auto& a : t->acc)
@@ -1040,6 +1041,18 @@ void Runtime::complete(Task* t) {
   t->copy_syncs.clear();
   t->waits.clear();
   Graph* g = graphs_[t->gid].get();
+  if (ktime_ && t->start && t->end) {
+    D.stats.timed_tasks += 1;
+    if (!t->end->group_timed) {
+      t->end->group_timed = true;
+      const int64_t t0 = be_->event_time_ns(t->dev, t->start->event);
+      const int64_t t1 = be_->event_time_ns(t->dev, t->end->event);
+      const int64_t dt = t1 - t0;
+      if (dt > 0) D.kintervals.emplace_back(t0, t1);
+      D.stats.timed_groups += 1;
+      D.stats.timed_ns += dt > 0 ? static_cast<uint64_t>(dt) : 0;
+    }
+  }
   if (trace_ && t->start && t->end) {
     t->t_start = be_->event_time_ns(t->dev, t->start->event);
     t->t_end = be_->event_time_ns(t->dev, t->end->event);
@@ -1199,8 +1212,8 @@ void Runtime::exec_loop(int d) {
       }
     }
     const int s = free_stream(first);
-    SyncP gend = new_sync(d, s, trace_);
-    SyncP gstart = trace_ ? new_sync(d, s, true) : nullptr;
+    SyncP gend = new_sync(d, s, ktime_);
+    SyncP gstart = ktime_ ? new_sync(d, s, true) : nullptr;
     const int64_t tpop = now_ns();
     for (Task* t : group) {
       t->state = SFX_STATE_EXECUTING;
@@ -1409,7 +1422,23 @@ int Runtime::stats(int dev, sfx_dev_stats* out) {
     last_error = "bad device index";
     return SFX_ERR_CONFIG;
   }
-  *out = devs_[dev]->stats;
+  Device& D = *devs_[dev];
+  if (!D.kintervals.empty()) {
+    // union of the timed launch-group intervals (overlapping groups on
+    // different streams count once)
+    std::sort(D.kintervals.begin(), D.kintervals.end());
+    int64_t cs = D.kintervals[0].first, ce = D.kintervals[0].second;
+    for (auto& iv : D.kintervals) {
+      if (iv.first > ce) {
+        D.stats.busy_ns += static_cast<uint64_t>(ce - cs);
+        cs = iv.first;
+      }
+      ce = std::max(ce, iv.second);
+    }
+    D.stats.busy_ns += static_cast<uint64_t>(ce - cs);
+    D.kintervals.clear();
+  }
+  *out = D.stats;
   if (!be_->is_sim()) out->kernel_launches = be_->kernel_launches();  // process-wide kernel count
   return SFX_OK;
 }

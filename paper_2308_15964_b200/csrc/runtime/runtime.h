@@ -62,6 +62,7 @@ struct Sync {
   std::atomic<bool> recorded{false};
   bool complete = false;       // guarded by the runtime mutex
   bool group_counted = false;  // launch group already retired from its stream
+  bool group_timed = false;    // launch group duration already accumulated (KTIME)
   ~Sync();
 };
 using SyncP = std::shared_ptr<Sync>;
@@ -235,6 +236,7 @@ struct Device {
   std::condition_variable exec_cv, comp_cv;
   std::thread exec_thread, comp_thread;
   sfx_dev_stats stats{};
+  std::vector<std::pair<int64_t, int64_t>> kintervals;  // KTIME group [start, end] not yet folded into busy_ns
   bool prefetch_pending = false;  // ready queue changed since the last prefetch pass
 };
 
@@ -317,6 +319,7 @@ class Runtime {
   int plan_prefetch(int d, std::vector<Action>& acts);
   uint64_t align_;
   bool trace_;
+  bool ktime_;  // trace_ || SFX_FLAG_KTIME: every launch group gets a timing start event
   std::mutex mu_;
   std::condition_variable done_cv_;
   std::vector<std::unique_ptr<Device>> devs_;

@@ -72,7 +72,7 @@ class ComputeEngine:
 
     def __init__(self, team, scheduler=None, device_memory=None, *, backend: str = "cuda",
                  trace: bool = True, window: int = 0, ordinals=None, arena_align: int = 0,
-                 group_max: int = 32):
+                 group_max: int = 32, kernel_timing: bool = False):
         if isinstance(team, (list, tuple)):
             team = WorkerTeam(team)
         devices = team.device_indexes()
@@ -89,6 +89,8 @@ class ComputeEngine:
         self.policy = native_policy(scheduler)
         self.trace_enabled = trace
         flags = N.FLAG_TRACE if trace else 0
+        if kernel_timing:
+            flags |= N.FLAG_KTIME  # stats(): timed_groups / timed_tasks / timed_ns
         if backend == "sim":
             flags |= N.FLAG_SIM
         if arena_align:
