@@ -87,6 +87,10 @@ extern "C" {
                                   (tests/conftest.py:87-124): iparam = {kind, a, b}   */
 #define SFX_OP_BYTES_ADD 3     /* bytes[off:off+len] += delta (mod 256): iparam={off,len,delta} */
 #define SFX_OP_FLUSH 4         /* runtime-internal host flush (write or read mode)    */
+#define SFX_OP_ADD_I64 5       /* every operand (int64 cells): += iparam[0] with device
+                                  atomics.  Like P2P_PAIR/P2P_SELF it accumulates
+                                  atomically, so its commutative members of one group run
+                                  concurrently on one device (shared guard)            */
 #define SFX_OP_DGEMM 10        /* C = beta*C + alpha*A*op(B); fparam={alpha,beta}, iparam[0]=trans_b */
 #define SFX_OP_DSYRK 11        /* C = beta*C + alpha*A*A^T, lower; fparam={alpha,beta} */
 #define SFX_OP_DTRSM 12        /* B = B * L^-T  (right, lower, transposed, non-unit)   */

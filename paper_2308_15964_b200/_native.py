@@ -49,6 +49,7 @@ OP_SPIN = 1
 OP_CELL = 2
 OP_BYTES_ADD = 3
 OP_FLUSH = 4
+OP_ADD_I64 = 5
 OP_DGEMM = 10
 OP_DSYRK = 11
 OP_DTRSM = 12

@@ -60,6 +60,20 @@ cudaError_t launch_dtrsm_coop_group(const TrsmDesc* d, int ntasks, int M, int n,
 
 cudaError_t launch_dtrsm(const double* L, long long ldl, double* B, long long ldb, int M, int n, cudaStream_t s);
 cudaError_t launch_dpotrf(double* A, long long lda, int n, int* info, cudaStream_t s);
+struct P2PDesc {
+  const double* Pi;
+  long long ldpi;
+  int ni;
+  const double* Pj;
+  long long ldpj;
+  int nj;
+  double* Fi;
+  long long ldfi;
+  double* Fj;
+  long long ldfj;
+};
+// grouped launch: tasks of one op (pair or self), one kernel per 32 tasks
+cudaError_t launch_p2p_group(const P2PDesc* d, int ntasks, bool self, double eps2, cudaStream_t s);
 cudaError_t launch_p2p(const double* Pi, long long ldpi, int ni, const double* Pj, long long ldpj, int nj, double* Fi,
                        long long ldfi, double* Fj, long long ldfj, bool self, double eps2, cudaStream_t s);
 
@@ -70,6 +84,7 @@ cudaError_t launch_fill_spd(double* a, long long rows, long long cols, long long
 cudaError_t launch_fill_particles(double* p, long long n, long long ld, long long seed, long long first,
                                   cudaStream_t s);
 cudaError_t launch_spin(long long ns, cudaStream_t s);
+cudaError_t launch_add_i64(long long* const* cells, int n, long long delta, cudaStream_t s);
 cudaError_t launch_cell(long long* target, const long long* const* reads, int nreads, long long kind, long long a,
                         long long b, cudaStream_t s);
 cudaError_t launch_bytes_add(unsigned char* p, long long off, long long len, long long delta, cudaStream_t s);

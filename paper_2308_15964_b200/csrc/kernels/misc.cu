@@ -152,6 +152,30 @@ cudaError_t launch_fill_particles(double* p, long long n, long long ld, long lon
   return cudaGetLastError();
 }
 
+namespace {
+struct AddI64Args {
+  long long* cells[8];
+  int n;
+  long long delta;
+};
+// SFX_OP_ADD_I64: device-atomic accumulation (members of one commutative group
+// may run concurrently, runtime.h accumulates_atomically)
+__global__ void add_i64_kernel(AddI64Args a) {
+  if (threadIdx.x < a.n)
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.cells[threadIdx.x]), static_cast<unsigned long long>(a.delta));
+}
+}  // namespace
+
+cudaError_t launch_add_i64(long long* const* cells, int n, long long delta, cudaStream_t s) {
+  AddI64Args a{};
+  a.n = n < 8 ? n : 8;
+  for (int k = 0; k < a.n; ++k) a.cells[k] = cells[k];
+  a.delta = delta;
+  count_launch();
+  add_i64_kernel<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_spin(long long ns, cudaStream_t s) {
   count_launch();
   spin_kernel<<<1, 32, 0, s>>>(ns);

@@ -5,141 +5,272 @@
 //   r2   = |x_a - x_b|^2 + eps2
 //   pot_a += q_b / r
 //   F_a  += q_a q_b (x_a - x_b) / r^3
-// A pair task (i, j) evaluates both directions (targets in i from sources in
-// j, and targets in j from sources in i) in one launch: every ORDERED
-// interaction is evaluated exactly once, which is the unit of the metric
-// (N(N-1) ordered interactions, 20 flop each by convention).
-// The self task (i, i) skips a == b.
+// (oracle/bodies.py _one_side / p2p_pair / p2p_self).  A pair task (i, j)
+// owes every ORDERED interaction between the two groups (both directions),
+// a self task every ordered pair a != b inside one group: N(N-1) in total,
+// the unit of the metric.
 //
-// Layout/roofline choices: one thread owns TPT targets in registers; source
-// tiles are staged in shared memory with coalesced loads and read back as
-// broadcasts (every lane reads the same source), so the inner loop is pure
-// FP64 pipe work: 3 DADD + 3 DFMA (r2) + MUFU.RSQ64H + 8 (Newton) + 3 DMUL +
-// 1 DADD + 3 DFMA = 21 FP64 ops per ordered interaction.
-// Commutative accumulation into F is exclusive per handle (the runtime chains
-// members of a commutative group), so the epilogue is a plain read-add-write.
+// Mutual evaluation.  Both directions of a pair share dx, r2 and 1/r, so the
+// kernel evaluates each UNORDERED pair once and applies it to both sides:
+//   u = 1/r, pa = q_a u, pb = q_b u, s = pa pb u  (= q_a q_b / r^3)
+//   pot_a += pb, pot_b += pa, F_a += s d, F_b -= s d       (d = x_a - x_b)
+// = 3 DADD + 3 DFMA (r2) + MUFU.RSQ64H + 5 (one 3rd-order refinement step,
+// full double) + 4 DMUL + 2 DADD + 6 DFMA = 23 FP64 ops per unordered pair,
+// 11.5 per ordered interaction (the one-directional formulation needs 21).
 //
-// Oracle: oracle/bodies.py p2p_pair / p2p_self.
+// Layout (warp-shuffle rotation).  A CTA owns a 512-target block of side a
+// and a 512-source block of side b; each of its 4 warps holds 128 targets in
+// registers (TPT = 4 per lane, with their accumulators).  The b block is
+// walked in chunks of 64: every lane loads SPT = 2 sources (coalesced) and
+// zeroes their accumulators, then the warp does 32 rotation steps: evaluate
+// the lane's 4 x 2 pairs, pass the 2 sources and their accumulators to the
+// next lane (__shfl_sync).  After 32 steps every source has met all 128
+// targets of the warp and is back on its home lane with its accumulated
+// contributions; the 4 warps' partials are summed in shared memory and added
+// to F_b with one FP64 atomic per component.  Targets flush their
+// accumulators with FP64 atomics at the end.  Because every update of F is a
+// device atomic, other CTAs of the same task and other tasks of the same
+// commutative group may add into the same accumulators concurrently: the
+// runtime takes these ops' commutative guards in shared mode
+// (runtime.h accumulates_atomically) and groups up to 32 same-shape tasks
+// into one launch (launch_p2p_group).
+//
+// Self task: the blocks (ba, bb) with bb >= ba of one group; on diagonal
+// blocks only pairs with index(b) > index(a) count, so each unordered pair is
+// evaluated once (the mask costs one compare + select, diagonal blocks only).
+// Padding lanes (past n) carry q = 0 and a far-away position, contributing 0.
 #include "kernels.h"
 
 namespace sfx {
 namespace {
 
-constexpr int THREADS = 128;
-constexpr int TPT = 2;     // targets per thread (ILP + one smem broadcast per 2 interactions)
-constexpr int TILE = 256;  // sources staged per shared-memory round
-constexpr int SPLIT_SRC = 1024;  // sources per block: a task spreads over (targets/256) x (sources/1024) blocks
+constexpr int THREADS = 128;           // 4 warps
+constexpr int TPT = 4;                 // targets per lane
+constexpr int SPT = 2;                 // sources per lane per chunk
+constexpr int BLK = 32 * TPT * (THREADS / 32);  // 512: targets per CTA = sources per CTA
+constexpr int CHUNK = 32 * SPT;        // 64 sources per rotation round
+constexpr double FAR = 1e100;          // padding position (r2 ~ 1e200: finite, u ~ 1e-100)
 
-// 1/sqrt(x) for normal x > 0 (r2 >= eps2 > 0 here): the MUFU.RSQ64H seed
-// (~23 bits) refined by two Newton steps (~46 -> full double).  4 FP64 ops per
-// step, no special-case slow path (CUDA's rsqrt(double) branches to one).
-__device__ __forceinline__ double rsqrt_nr(double x) {
+// 1/sqrt(x), x > 0 normal: MUFU.RSQ64H seed refined by one third-order step
+// y' = y + y e (1/2 + 3/8 e), e = 1 - x y^2 (error ~ (5/16) e^3: full double
+// for a seed good to ~2^-22).  5 FP64 ops, no slow path.
+__device__ __forceinline__ double rsqrt_fast(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x * y, y, 1.0);
-  y = fma(0.5 * y, e, y);
-  e = fma(-x * y, y, 1.0);
-  y = fma(0.5 * y, e, y);
-  return y;
+  const double e = fma(-x * y, y, 1.0);
+  const double c = fma(0.375, e, 0.5);
+  return fma(y * e, c, y);
 }
 
-struct P2PSide {
-  const double* tgt;  // 4 x nt (ld)
-  const double* src;  // 4 x ns (ld)
-  double* acc;        // 4 x nt (ld)
-  long long ld_t, ld_s, ld_a;
-  int nt, ns;
-  int self;  // exclude a == b
+struct P2PArgs {
+  const double* pa;  // 4 x na (ld_pa)
+  const double* pb;  // 4 x nb (ld_pb)
+  double* fa;
+  double* fb;
+  long long ld_pa, ld_pb, ld_fa, ld_fb;
+  int na, nb;
+  int nblk_a, nblk_b;  // blocks of BLK along a and b
+  double eps2;
 };
 
-__global__ void __launch_bounds__(THREADS) p2p_kernel(P2PSide s0, P2PSide s1, int blocks0, double eps2) {
-  __shared__ double4 sp[TILE];
-  const bool second = blockIdx.x >= blocks0;
-  const P2PSide& S = second ? s1 : s0;
-  const int blk_lin = second ? blockIdx.x - blocks0 : blockIdx.x;
-  const int nsplit = (S.ns + SPLIT_SRC - 1) / SPLIT_SRC;
-  const int blk = blk_lin / nsplit, split = blk_lin - blk * nsplit;
-  const int j_begin = split * SPLIT_SRC, j_end = min(S.ns, j_begin + SPLIT_SRC);
-  const int base = blk * THREADS * TPT;
-  double xi[TPT], yi[TPT], zi[TPT];
-  double ax[TPT], ay[TPT], az[TPT], ap[TPT];
-  int ti[TPT];
+template <bool DIAG>
+__device__ __forceinline__ void pair_step(const double (&xa)[TPT], const double (&ya)[TPT], const double (&za)[TPT],
+                                          const double (&qa)[TPT], double (&fxa)[TPT], double (&fya)[TPT],
+                                          double (&fza)[TPT], double (&pta)[TPT], const int (&ia)[TPT],
+                                          double (&xb)[SPT], double (&yb)[SPT], double (&zb)[SPT],
+                                          double (&qb)[SPT], double (&fxb)[SPT], double (&fyb)[SPT],
+                                          double (&fzb)[SPT], double (&ptb)[SPT], const int (&ib)[SPT], double eps2) {
 #pragma unroll
-  for (int u = 0; u < TPT; ++u) {
-    ti[u] = base + u * THREADS + threadIdx.x;
-    const int t = ti[u] < S.nt ? ti[u] : 0;
-    xi[u] = S.tgt[t];
-    yi[u] = S.tgt[S.ld_t + t];
-    zi[u] = S.tgt[2 * S.ld_t + t];
-    ax[u] = ay[u] = az[u] = ap[u] = 0.0;
-  }
-  for (int j0 = j_begin; j0 < j_end; j0 += TILE) {
-    __syncthreads();
-    for (int k = threadIdx.x; k < TILE; k += THREADS) {
-      const int j = j0 + k;
-      double4 v;
-      if (j < j_end) {
-        v.x = S.src[j];
-        v.y = S.src[S.ld_s + j];
-        v.z = S.src[2 * S.ld_s + j];
-        v.w = S.src[3 * S.ld_s + j];
-      } else {
-        v.x = v.y = v.z = 0.0;
-        v.w = 0.0;  // zero charge: contributes nothing
-      }
-      sp[k] = v;
-    }
-    __syncthreads();
-    const int jn = min(TILE, j_end - j0);
-#pragma unroll 4
-    for (int k = 0; k < jn; ++k) {
-      const double4 p = sp[k];
+  for (int v = 0; v < SPT; ++v) {
 #pragma unroll
-      for (int u = 0; u < TPT; ++u) {
-        const double dx = xi[u] - p.x, dy = yi[u] - p.y, dz = zi[u] - p.z;
-        const double r2 = fma(dx, dx, fma(dy, dy, fma(dz, dz, eps2)));
-        double inv = rsqrt_nr(r2);
-        if (S.self && j0 + k == ti[u]) inv = 0.0;
-        const double qi = p.w * inv;        // q_b / r
-        const double s3 = qi * inv * inv;   // q_b / r^3
-        ap[u] += qi;
-        ax[u] = fma(s3, dx, ax[u]);
-        ay[u] = fma(s3, dy, ay[u]);
-        az[u] = fma(s3, dz, az[u]);
-      }
+    for (int u = 0; u < TPT; ++u) {
+      const double dx = xa[u] - xb[v], dy = ya[u] - yb[v], dz = za[u] - zb[v];
+      const double r2 = fma(dx, dx, fma(dy, dy, fma(dz, dz, eps2)));
+      double w = rsqrt_fast(r2);
+      if (DIAG) w = ib[v] > ia[u] ? w : 0.0;
+      const double pa_ = qa[u] * w, pb_ = qb[v] * w;
+      const double s = pa_ * pb_ * w;
+      pta[u] += pb_;
+      ptb[v] += pa_;
+      fxa[u] = fma(s, dx, fxa[u]);
+      fya[u] = fma(s, dy, fya[u]);
+      fza[u] = fma(s, dz, fza[u]);
+      fxb[v] = fma(-s, dx, fxb[v]);
+      fyb[v] = fma(-s, dy, fyb[v]);
+      fzb[v] = fma(-s, dz, fzb[v]);
     }
   }
+}
+
+template <bool DIAG>
+__device__ __forceinline__ void run_block(const P2PArgs& A, int ba, int bb, double (*red)[4][CHUNK]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double xa[TPT], ya[TPT], za[TPT], qa[TPT], fxa[TPT], fya[TPT], fza[TPT], pta[TPT];
+  int ia[TPT];
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
-    const int t = ti[u];
-    if (t >= S.nt) continue;
-    // source splits of one task add into the same targets: FP64 atomics
-    // (the runtime already keeps different tasks of a commutative group apart)
-    const double qa = S.tgt[3 * S.ld_t + t];
-    atomicAdd(&S.acc[t], qa * ax[u]);
-    atomicAdd(&S.acc[S.ld_a + t], qa * ay[u]);
-    atomicAdd(&S.acc[2 * S.ld_a + t], qa * az[u]);
-    atomicAdd(&S.acc[3 * S.ld_a + t], ap[u]);
+    ia[u] = ba * BLK + warp * (32 * TPT) + u * 32 + lane;
+    const bool ok = ia[u] < A.na;
+    const int t = ok ? ia[u] : 0;
+    xa[u] = ok ? A.pa[t] : FAR;
+    ya[u] = ok ? A.pa[A.ld_pa + t] : FAR;
+    za[u] = ok ? A.pa[2 * A.ld_pa + t] : FAR;
+    qa[u] = ok ? A.pa[3 * A.ld_pa + t] : 0.0;
+    fxa[u] = fya[u] = fza[u] = pta[u] = 0.0;
   }
+  const int b_end = min(A.nb, (bb + 1) * BLK);
+  for (int c0 = bb * BLK; c0 < b_end; c0 += CHUNK) {
+    double xb[SPT], yb[SPT], zb[SPT], qb[SPT], fxb[SPT], fyb[SPT], fzb[SPT], ptb[SPT];
+    int ib[SPT];
+#pragma unroll
+    for (int v = 0; v < SPT; ++v) {
+      ib[v] = c0 + v * 32 + lane;
+      const bool ok = ib[v] < b_end;
+      const int t = ok ? ib[v] : 0;
+      xb[v] = ok ? A.pb[t] : -FAR;
+      yb[v] = ok ? A.pb[A.ld_pb + t] : -FAR;
+      zb[v] = ok ? A.pb[2 * A.ld_pb + t] : -FAR;
+      qb[v] = ok ? A.pb[3 * A.ld_pb + t] : 0.0;
+      fxb[v] = fyb[v] = fzb[v] = ptb[v] = 0.0;
+    }
+    const int src = (lane + 1) & 31;
+#pragma unroll 1
+    for (int r = 0; r < 32; ++r) {
+      pair_step<DIAG>(xa, ya, za, qa, fxa, fya, fza, pta, ia, xb, yb, zb, qb, fxb, fyb, fzb, ptb, ib, A.eps2);
+#pragma unroll
+      for (int v = 0; v < SPT; ++v) {
+        xb[v] = __shfl_sync(0xffffffffu, xb[v], src);
+        yb[v] = __shfl_sync(0xffffffffu, yb[v], src);
+        zb[v] = __shfl_sync(0xffffffffu, zb[v], src);
+        qb[v] = __shfl_sync(0xffffffffu, qb[v], src);
+        fxb[v] = __shfl_sync(0xffffffffu, fxb[v], src);
+        fyb[v] = __shfl_sync(0xffffffffu, fyb[v], src);
+        fzb[v] = __shfl_sync(0xffffffffu, fzb[v], src);
+        ptb[v] = __shfl_sync(0xffffffffu, ptb[v], src);
+        if (DIAG) ib[v] = __shfl_sync(0xffffffffu, ib[v], src);
+      }
+    }
+    // 32 rotations: every source is home again.  Sum the 4 warps' partials.
+#pragma unroll
+    for (int v = 0; v < SPT; ++v) {
+      red[warp][0][v * 32 + lane] = fxb[v];
+      red[warp][1][v * 32 + lane] = fyb[v];
+      red[warp][2][v * 32 + lane] = fzb[v];
+      red[warp][3][v * 32 + lane] = ptb[v];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 4 * CHUNK; e += THREADS) {
+      const int comp = e / CHUNK, k = e - comp * CHUNK;
+      const int j = c0 + k;
+      if (j < b_end) {
+        const double sum = (red[0][comp][k] + red[1][comp][k]) + (red[2][comp][k] + red[3][comp][k]);
+        atomicAdd(&A.fb[comp * A.ld_fb + j], sum);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < TPT; ++u) {
+    const int t = ia[u];
+    if (t >= A.na) continue;
+    atomicAdd(&A.fa[t], fxa[u]);
+    atomicAdd(&A.fa[A.ld_fa + t], fya[u]);
+    atomicAdd(&A.fa[2 * A.ld_fa + t], fza[u]);
+    atomicAdd(&A.fa[3 * A.ld_fa + t], pta[u]);
+  }
+}
+
+constexpr int MAX_GROUP = 32;
+
+// One launch for up to MAX_GROUP tasks of the same op (grouped by the
+// runtime's executor like the DGEMMs): task k owns CTAs [first[k], first[k+1]).
+// Pair task: nblk_a * nblk_b CTAs; self task (SELF): the nblk (nblk + 1) / 2
+// blocks ba <= bb of one group.
+struct P2PGroup {
+  P2PArgs t[MAX_GROUP];
+  int first[MAX_GROUP + 1];
+  int n;
+};
+
+template <bool SELF>
+__global__ void __launch_bounds__(THREADS) p2p_mutual_kernel(const __grid_constant__ P2PGroup G) {
+  __shared__ double red[THREADS / 32][4][CHUNK];
+  int k = 0;
+  while (k + 1 < G.n && static_cast<int>(blockIdx.x) >= G.first[k + 1]) ++k;
+  const P2PArgs& A = G.t[k];
+  int lin = blockIdx.x - G.first[k];
+  int ba, bb;
+  if (SELF) {
+    ba = 0;
+    while (lin >= A.nblk_a - ba) {
+      lin -= A.nblk_a - ba;
+      ++ba;
+    }
+    bb = ba + lin;
+  } else {
+    ba = lin / A.nblk_b;
+    bb = lin - ba * A.nblk_b;
+  }
+  if (SELF && ba == bb)
+    run_block<true>(A, ba, bb, red);
+  else
+    run_block<false>(A, ba, bb, red);
 }
 
 }  // namespace
 
+cudaError_t launch_p2p_group(const P2PDesc* d, int ntasks, bool self, double eps2, cudaStream_t s) {
+  for (int c0 = 0; c0 < ntasks; c0 += MAX_GROUP) {
+    P2PGroup G{};
+    G.n = 0;
+    int blocks = 0;
+    for (int k = c0; k < ntasks && k < c0 + MAX_GROUP; ++k) {
+      const P2PDesc& x = d[k];
+      if (x.ni <= 0 || (!self && x.nj <= 0)) continue;
+      P2PArgs& a = G.t[G.n];
+      a.pa = x.Pi;
+      a.fa = x.Fi;
+      a.ld_pa = x.ldpi;
+      a.ld_fa = x.ldfi;
+      a.na = x.ni;
+      a.nblk_a = (x.ni + BLK - 1) / BLK;
+      a.eps2 = eps2;
+      if (self) {
+        a.pb = x.Pi;
+        a.fb = x.Fi;
+        a.ld_pb = x.ldpi;
+        a.ld_fb = x.ldfi;
+        a.nb = x.ni;
+        a.nblk_b = a.nblk_a;
+      } else {
+        a.pb = x.Pj;
+        a.fb = x.Fj;
+        a.ld_pb = x.ldpj;
+        a.ld_fb = x.ldfj;
+        a.nb = x.nj;
+        a.nblk_b = (x.nj + BLK - 1) / BLK;
+      }
+      G.first[G.n] = blocks;
+      blocks += self ? a.nblk_a * (a.nblk_a + 1) / 2 : a.nblk_a * a.nblk_b;
+      ++G.n;
+    }
+    if (!G.n) continue;
+    G.first[G.n] = blocks;
+    count_launch();
+    if (self)
+      p2p_mutual_kernel<true><<<blocks, THREADS, 0, s>>>(G);
+    else
+      p2p_mutual_kernel<false><<<blocks, THREADS, 0, s>>>(G);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t launch_p2p(const double* Pi, long long ldpi, int ni, const double* Pj, long long ldpj, int nj, double* Fi,
                        long long ldfi, double* Fj, long long ldfj, bool self, double eps2, cudaStream_t s) {
-  const int per_block = THREADS * TPT;
-  P2PSide a{Pi, self ? Pi : Pj, Fi, ldpi, self ? ldpi : ldpj, ldfi, ni, self ? ni : nj, self ? 1 : 0};
-  const int b0 = (ni + per_block - 1) / per_block * ((a.ns + SPLIT_SRC - 1) / SPLIT_SRC);
-  if (self) {
-    count_launch();
-    p2p_kernel<<<b0, THREADS, 0, s>>>(a, a, b0, eps2);
-  } else {
-    P2PSide b{Pj, Pi, Fj, ldpj, ldpi, ldfj, nj, ni, 0};
-    const int b1 = (nj + per_block - 1) / per_block * ((b.ns + SPLIT_SRC - 1) / SPLIT_SRC);
-    count_launch();
-    p2p_kernel<<<b0 + b1, THREADS, 0, s>>>(a, b, b0, eps2);
-  }
-  return cudaGetLastError();
+  P2PDesc d{Pi, ldpi, ni, Pj, ldpj, nj, Fi, ldfi, Fj, ldfj};
+  return launch_p2p_group(&d, 1, self, eps2, s);
 }
 
 }  // namespace sfx

@@ -199,6 +199,7 @@ class CudaBackend : public Backend {
       case SFX_OP_SPIN:
       case SFX_OP_CELL:
       case SFX_OP_BYTES_ADD:
+      case SFX_OP_ADD_I64:
       case SFX_OP_FLUSH:
       case SFX_OP_ZERO:
       case SFX_OP_DGEMM:
@@ -231,6 +232,12 @@ class CudaBackend : public Backend {
       case SFX_OP_BYTES_ADD:
         e = launch_bytes_add(static_cast<unsigned char*>(o[0].dptr), op.ip[0], op.ip[1], op.ip[2], s);
         break;
+      case SFX_OP_ADD_I64: {
+        long long* cells[8];
+        for (int k = 0; k < op.n; ++k) cells[k] = static_cast<long long*>(o[k].dptr);
+        e = launch_add_i64(cells, op.n, op.ip[0], s);
+        break;
+      }
       case SFX_OP_CELL: {
         const long long* reads[7];
         for (int k = 1; k < op.n; ++k) reads[k - 1] = static_cast<const long long*>(o[k].dptr);
@@ -315,6 +322,22 @@ class CudaBackend : public Backend {
                                     static_cast<int>(o[2].cols), static_cast<int>(o[0].cols), f.fp[0], f.fp[1],
                                     f.ip[0] != 0, false, devs_[d]->streams[stream]);
       return cuda_err(e, "grouped dgemm launch", err);
+    }
+    if (ops.size() > 1 && (f.op == SFX_OP_P2P_PAIR || f.op == SFX_OP_P2P_SELF)) {
+      const bool self = f.op == SFX_OP_P2P_SELF;
+      std::vector<P2PDesc> pd(ops.size());
+      for (size_t i = 0; i < ops.size(); ++i) {
+        const Operand* o = ops[i].o;
+        auto f64p = [](const Operand& x) { return static_cast<double*>(x.dptr); };
+        if (self)
+          pd[i] = P2PDesc{f64p(o[0]), o[0].ld, static_cast<int>(o[0].cols), nullptr, 0, 0, f64p(o[1]), o[1].ld,
+                          nullptr, 0};
+        else
+          pd[i] = P2PDesc{f64p(o[0]), o[0].ld, static_cast<int>(o[0].cols), f64p(o[1]), o[1].ld,
+                          static_cast<int>(o[1].cols), f64p(o[2]), o[2].ld, f64p(o[3]), o[3].ld};
+      }
+      cudaError_t e = launch_p2p_group(pd.data(), static_cast<int>(pd.size()), self, f.fp[0], devs_[d]->streams[stream]);
+      return cuda_err(e, "grouped p2p launch", err);
     }
     if (ops.size() > 1 && f.op == SFX_OP_DTRSM && f.ip[0]) {
       std::vector<TrsmDesc> td(ops.size());

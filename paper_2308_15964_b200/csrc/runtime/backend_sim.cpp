@@ -71,6 +71,7 @@ class SimBackend : public Backend {
       case SFX_OP_SPIN:
       case SFX_OP_CELL:
       case SFX_OP_BYTES_ADD:
+      case SFX_OP_ADD_I64:
       case SFX_OP_FLUSH:
       case SFX_OP_ZERO:
         return true;
@@ -90,6 +91,10 @@ class SimBackend : public Backend {
       }
       case SFX_OP_ZERO:
         memset(op.o[0].dptr, 0, op.o[0].bytes);
+        return SFX_OK;
+      case SFX_OP_ADD_I64:
+        for (int k = 0; k < op.n; ++k)
+          __atomic_fetch_add(static_cast<int64_t*>(op.o[k].dptr), op.ip[0], __ATOMIC_RELAXED);
         return SFX_OK;
       case SFX_OP_BYTES_ADD: {
         uint8_t* p = static_cast<uint8_t*>(op.o[0].dptr);

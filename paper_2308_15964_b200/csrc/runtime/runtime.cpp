@@ -312,6 +312,17 @@ int Runtime::validate(const sfx_task_desc& d, const sfx_access* acc, std::string
           return SFX_ERR_CONFIG;
         }
       return 0;
+    case SFX_OP_ADD_I64:
+      if (d.n_access < 1 || d.n_access > 8) {
+        err = "add_i64 takes 1 to 8 int64 cells";
+        return SFX_ERR_CONFIG;
+      }
+      for (uint32_t k = 0; k < d.n_access; ++k)
+        if (hs[k]->bytes < 8 || !mode_writes(acc[k].mode)) {
+          err = "add_i64 operands must be written 8-byte int64 cells";
+          return SFX_ERR_CONFIG;
+        }
+      return 0;
     case SFX_OP_BYTES_ADD:
       if (!need(1) || !writes(0)) return SFX_ERR_CONFIG;
       if (d.iparam[0] < 0 || d.iparam[1] < 0 || static_cast<uint64_t>(d.iparam[0] + d.iparam[1]) > hs[0]->bytes) {
@@ -451,6 +462,7 @@ int Runtime::submit(uint32_t n, const sfx_task_desc* descs, const sfx_access* ac
     for (auto& a : t->acc)
       if (a.mode == SFX_COMMUTATIVE_WRITE) t->commute.push_back(a.h);
     std::sort(t->commute.begin(), t->commute.end(), [](const Handle* x, const Handle* y) { return x->hid < y->hid; });
+    t->commute_shared = accumulates_atomically(t->op);
     Graph* g = graphs_[d.graph].get();
     g->tasks.push_back(t);
     g->inserted += 1;
@@ -878,7 +890,7 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
     b->dirty = true;
     h->dirty_dev = d;
     h->host_valid = false;
-    if (m == SFX_COMMUTATIVE_WRITE) h->commute_last = t->end;
+    if (m == SFX_COMMUTATIVE_WRITE && !t->commute_shared) h->commute_last = t->end;
     if (m == SFX_WRITE || m == SFX_MAYBE_WRITE) b->ready = t->end;
   }
 
@@ -964,6 +976,8 @@ bool Runtime::groupable(const Task* t) const {
     case SFX_OP_FILL_SPD:
     case SFX_OP_FILL_PARTICLES:
     case SFX_OP_ZERO:
+    case SFX_OP_P2P_PAIR:  // grouped mutual P2P kernel; commutative guards in shared mode
+    case SFX_OP_P2P_SELF:
       return group_max_ > 1;
     default:
       return false;
@@ -986,21 +1000,40 @@ bool Runtime::same_signature(const Task* a, const Task* b) const {
 }
 
 bool Runtime::acquire_commute(Task* t) {
-  // all-or-nothing in hid order; on failure the task parks on the busy handle
+  // all-or-nothing in hid order; on failure the task parks on the busy handle.
+  // Shared mode (the op accumulates into its commutative operands with device
+  // atomics, so any interleaving is one of the orders commutativity allows):
+  // members of a group run concurrently as long as they are on the same device
+  // and no exclusive member holds the handle.
   for (Handle* h : t->commute) {
-    if (h->commute_owner && h->commute_owner != t) {
+    const bool busy = t->commute_shared
+                          ? (h->commute_owner != nullptr || (h->shared_users > 0 && h->shared_dev != t->dev))
+                          : ((h->commute_owner && h->commute_owner != t) || h->shared_users > 0);
+    if (busy) {
       h->commute_waiters.push_back(t);
       return false;
     }
   }
-  for (Handle* h : t->commute) h->commute_owner = t;
+  for (Handle* h : t->commute) {
+    if (t->commute_shared) {
+      h->shared_users += 1;
+      h->shared_dev = t->dev;
+    } else {
+      h->commute_owner = t;
+    }
+  }
   return true;
 }
 
 void Runtime::release_commute(Task* t) {
   for (Handle* h : t->commute) {
-    if (h->commute_owner != t) continue;
-    h->commute_owner = nullptr;
+    if (t->commute_shared) {
+      if (--h->shared_users > 0) continue;
+      h->shared_dev = -1;
+    } else {
+      if (h->commute_owner != t) continue;
+      h->commute_owner = nullptr;
+    }
     // wake the parked members in FIFO order; each re-enters its device queue
     while (!h->commute_waiters.empty()) {
       Task* w = h->commute_waiters.front();
@@ -1011,12 +1044,13 @@ void Runtime::release_commute(Task* t) {
 }
 
 bool Runtime::commute_conflict(const std::vector<Task*>& group, const Task* t) const {
-  // members of one commutative group must never run concurrently on the same handle
+  // members of one commutative group must never run concurrently on the same
+  // handle -- unless all of them accumulate atomically (shared guard)
   for (const Access& a : t->acc) {
     if (a.mode != SFX_COMMUTATIVE_WRITE) continue;
     for (const Task* g : group)
       for (const Access& b : g->acc)
-        if (b.h == a.h) return true;
+        if (b.h == a.h && !(t->commute_shared && g->commute_shared)) return true;
   }
   return false;
 }
@@ -1244,8 +1278,13 @@ void Runtime::exec_loop(int d) {
           t->end.reset();
           t->start.reset();
           t->state = SFX_STATE_READY;
-          for (Handle* h : t->commute)
-            if (h->commute_owner == t) h->commute_owner = nullptr;
+          if (t->commute_shared) {
+            for (Handle* h : t->commute)
+              if (--h->shared_users == 0) h->shared_dev = -1;
+          } else {
+            for (Handle* h : t->commute)
+              if (h->commute_owner == t) h->commute_owner = nullptr;
+          }
           D.queue.push_front(t);
         }
         group.resize(planned);

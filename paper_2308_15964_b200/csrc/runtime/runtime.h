@@ -48,6 +48,12 @@ inline Cat category_of(uint32_t mode) {
   }
 }
 inline bool mode_writes(uint32_t m) { return m != SFX_READ; }
+// ops whose writes to commutative operands are device-atomic accumulations:
+// concurrent members of a commutative group give one of the results a serial
+// order would (up to FP rounding), so their guard is taken in shared mode
+inline bool accumulates_atomically(uint32_t op) {
+  return op == SFX_OP_P2P_PAIR || op == SFX_OP_P2P_SELF || op == SFX_OP_ADD_I64;
+}
 
 class Backend;
 
@@ -106,6 +112,10 @@ struct Handle {
   // of being re-offered (no quadratic re-offer scan, handles.py:317-328)
   Task* commute_owner = nullptr;
   std::deque<Task*> commute_waiters;
+  // shared mode (ops that accumulate with device atomics, accumulates_atomically):
+  // members run concurrently on ONE device; exclusive members wait for them all
+  int shared_users = 0;
+  int shared_dev = -1;
   int group_dev = -1;   // device of the active atomic/commutative group
   int home = -1;        // owner hint (2-D block-cyclic distribution)
 };
@@ -134,6 +144,7 @@ struct Task {
   std::vector<SyncP> copy_syncs;  // copies issued on this task's stream
   int64_t t_push = 0, t_pop = 0, t_start = 0, t_end = 0;
   std::vector<Handle*> commute;  // commutative handles sorted by hid (graph.py:150-157)
+  bool commute_shared = false;   // op accumulates with device atomics: guard in shared mode
 };
 
 struct Operand {

@@ -111,6 +111,13 @@ def bytes_add(off: int, length: int, delta: int) -> Op:
     return Op("bytes_add", N.OP_BYTES_ADD, iparam=(off, length, delta))
 
 
+def add_i64(delta: int) -> Op:
+    """Every operand (an int64 cell) += delta with device atomics.  An op that
+    accumulates atomically: its commutative_write members of one group run
+    concurrently on one device (shared guard; the P2P ops behave the same)."""
+    return Op("add_i64", N.OP_ADD_I64, iparam=(int(delta),))
+
+
 noop = Op("noop", N.OP_NOOP)
 gemm_nn = dgemm(1.0, 1.0, False)
 gemm_nt_sub = dgemm(-1.0, 1.0, True)

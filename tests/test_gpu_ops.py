@@ -187,3 +187,54 @@ def test_dpotrf_store_inverses_and_trsm_inverse_blocks(gpu_engine, b):
     bodies.trsm(np.tril(want), Xw)
     assert np.linalg.norm(X - Xw) / np.linalg.norm(Xw) <= 1e-12
     assert np.linalg.norm(X @ L.T - B0) / (np.linalg.norm(L) * np.linalg.norm(X)) <= 1e-13
+
+
+@pytest.mark.parametrize("sizes", [(300, 77, 1), (513, 1024, 64)])
+def test_particles_ragged_groups(gpu_engine, sizes):
+    """Group sizes that are not multiples of the kernel's 512-particle blocks or
+    64-source chunks (padding lanes), including a one-particle group."""
+    rng = np.random.default_rng(sum(sizes))
+    P = [sf.pinned_empty((4, n)) for n in sizes]
+    F = [sf.pinned_zeros((4, n)) for n in sizes]
+    for p in P:
+        p[:3] = rng.random((3, p.shape[1]))
+        p[3] = 0.5 + 0.5 * rng.random(p.shape[1])
+    want = [np.zeros_like(f) for f in F]
+    for i in range(len(sizes)):
+        bodies.p2p_self(P[i], want[i])
+        for j in range(i + 1, len(sizes)):
+            bodies.p2p_pair(P[i], P[j], want[i], want[j])
+    _run(gpu_engine, lambda g: alg.insert_particles(g, P, F))
+    for got, w in zip(F, want):
+        pot_rel = np.abs(got[3] - w[3]) / np.abs(w[3])
+        assert pot_rel.max() <= 1e-10, pot_rel.max()
+        scale = np.abs(w[:3]).max()
+        assert np.abs(got[:3] - w[:3]).max() <= 1e-11 * scale
+
+
+def test_shared_commutative_members_on_gpu(gpu_engine):
+    """add_i64 members of commutative groups run concurrently on the streams
+    (shared guard), interleaved with exclusive members and plain writes: the
+    cells equal a serial execution."""
+    import random
+    rng = random.Random(11)
+    n = 5
+    g = sf.TaskGraph().compute_on(gpu_engine)
+    cells = [sf.Cell(0) for _ in range(n)]
+    want = [0] * n
+    for step in range(400):
+        i, j = rng.sample(range(n), 2)
+        if step % 80 == 79:
+            g.task(sf.write(cells[i]), sf.read(cells[j]), device=sf.ops.cell("write", 2, 1))
+            want[i] = (2 * want[i] + 1 + want[j]) % 10000019
+        elif rng.random() < 0.2:
+            g.task(sf.commutative_write(cells[i]), device=sf.ops.cell("commute", 1, 3))
+            want[i] = (want[i] + 3) % 10000019
+        else:
+            d = rng.randrange(1, 100)
+            g.task(sf.commutative_write(cells[i]), sf.commutative_write(cells[j]), device=sf.ops.add_i64(d))
+            want[i] += d
+            want[j] += d
+    g.flush_all(keep_device=False)
+    assert g.wait_all(timeout=60)
+    assert [c.value for c in cells] == want

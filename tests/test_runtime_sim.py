@@ -457,3 +457,37 @@ def stf_edges(prog):
     from oracle import stf
 
     return stf.static_successor_edges(programs.program_accesses(prog))
+
+
+@pytest.mark.parametrize("devices,streams", [(1, 4), (2, 3)])
+def test_shared_commutative_guard_mixed_with_exclusive_members(devices, streams):
+    """Ops that accumulate with device atomics (add_i64, the P2P ops) take the
+    commutative guard in shared mode; exclusive members of the same group (cell
+    'commute') still exclude them.  Values equal a serial execution, and the
+    commutative groups still produce no edges among their members."""
+    rng = random.Random(7)
+    n = 6
+    eng = sim_engine(devices, streams)
+    try:
+        g = sf.TaskGraph().compute_on(eng)
+        cells = [sf.Cell(0) for _ in range(n)]
+        want = [0] * n
+        for step in range(300):
+            i, j = rng.sample(range(n), 2)
+            if step % 50 == 49:  # a plain write closes the groups of cell i
+                g.task(sf.write(cells[i]), sf.read(cells[j]), device=sf.ops.cell("write", 2, 1))
+                want[i] = (2 * want[i] + 1 + want[j]) % 10000019  # reference tests/conftest.py:22
+            elif rng.random() < 0.2:
+                g.task(sf.commutative_write(cells[i]), device=sf.ops.cell("commute", 1, 3))
+                want[i] = (want[i] + 3) % 10000019
+            else:
+                d = rng.randrange(1, 100)
+                g.task(sf.commutative_write(cells[i]), sf.commutative_write(cells[j]), device=sf.ops.add_i64(d))
+                want[i] += d
+                want[j] += d
+        assert g.wait_all(timeout=60)
+        g.flush_all(keep_device=False)
+        assert g.wait_all(timeout=60)
+    finally:
+        eng.stop()
+    assert [c.value for c in cells] == want
