@@ -384,7 +384,8 @@ def secondary(sf, alg, dev, args, peak_tf):
     eng.stop()
     del M
     # C4: particles 2^20 in 256 groups, one evaluation
-    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, args.streams), trace=False, ordinals=[dev])
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, args.streams), trace=False, ordinals=[dev],
+                           kernel_timing=True)
     ng, per = 256, 4096
     P = [sf.pinned_empty((4, per)) for _ in range(ng)]
     F = [sf.pinned_empty((4, per)) for _ in range(ng)]
@@ -393,18 +394,36 @@ def secondary(sf, alg, dev, args, peak_tf):
     for f in F:
         g.task(sf.write(f), device=sf.ops.zero())
     g.wait_all()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    alg.insert_particles(g, P, F)
-    g.wait_all()
-    e1.record()
-    torch.cuda.synchronize()
-    t = e0.elapsed_time(e1) / 1e3
+    ts = []
+    for rep in range(3):
+        torch.cuda.synchronize()
+        s0 = eng.stats(0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        alg.insert_particles(g, P, F)
+        g.wait_all()
+        e1.record()
+        torch.cuda.synchronize()
+        s1 = eng.stats(0)
+        if rep:
+            ts.append(e0.elapsed_time(e1) / 1e3)
+    t = statistics.mean(ts)
     inter = alg.interactions(ng * per)
+    dfma_tf = sf.fp64_dfma_peak(dev)
+    # mutual kernel: 23 FP64 instructions per unordered pair = 2 ordered interactions
+    # (csrc/kernels/particles.cu); FP64-pipe bound = (DFMA peak / 2 flop) instr/s / 11.5
+    bound = dfma_tf * 1e12 / 2 / 11.5
+    busy = (s1["busy_ns"] - s0["busy_ns"]) * 1e-9
     out["particles_C4"] = {"particles": ng * per, "groups": ng, "tasks": 32896, "seconds": t,
                            "interactions_per_s": inter / t,
-                           "gflops_20flop_convention": inter * alg.FLOP_PER_INTERACTION / t / 1e9}
+                           "gflops_20flop_convention": inter * alg.FLOP_PER_INTERACTION / t / 1e9,
+                           "roofline": {"bound": "fp64 pipe (DFMA/DMUL/DADD)", "unit": "interactions/s",
+                                        "achieved": inter / busy if busy else None,
+                                        "peak": bound, "frac": inter / busy / bound if busy else None,
+                                        "dfma_peak_tflops": dfma_tf,
+                                        "fp64_instr_per_interaction": 11.5,
+                                        "kernel_share_of_step": busy / t,
+                                        "launches": s1["timed_groups"] - s0["timed_groups"]}}
     eng.stop()
     # runtime overhead per task: reference protocol (src/bench.py:67-117), T chains x N tasks, D = 0
     eng = sf.create_engine(sf.WorkerTeam.of_devices(1, 4), trace=False, ordinals=[dev])

@@ -228,6 +228,9 @@ int sfx_host_free(void* p, int sim);
 
 /* FP64 DMMA throughput microbenchmark on a device (roofline denominator) */
 int sfx_fp64_peak(int ordinal, double* tflops, double* sm_mhz);
+/* FP64 pipe (DFMA, 2 flop per FMA) throughput microbenchmark: the roofline
+ * denominator of the particle kernel, whose work is DFMA/DMUL/DADD */
+int sfx_fp64_dfma_peak(int ordinal, double* tflops);
 
 #ifdef __cplusplus
 }

@@ -137,6 +137,7 @@ def _load():
         "sfx_host_alloc": ([u64, ctypes.c_int, ctypes.POINTER(P)], ctypes.c_int),
         "sfx_host_free": ([P, ctypes.c_int], ctypes.c_int),
         "sfx_fp64_peak": ([ctypes.c_int, ctypes.POINTER(dbl), ctypes.POINTER(dbl)], ctypes.c_int),
+        "sfx_fp64_dfma_peak": ([ctypes.c_int, ctypes.POINTER(dbl)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -153,7 +154,7 @@ EXPORTED = ("sfx_abi_version", "sfx_device_count", "sfx_create", "sfx_destroy", 
             "sfx_submit", "sfx_pause", "sfx_resume", "sfx_wait_all", "sfx_wait_task",
             "sfx_task_state", "sfx_flush", "sfx_stats", "sfx_resident", "sfx_block_state",
             "sfx_trace", "sfx_edges", "sfx_violations", "sfx_set_option", "sfx_host_alloc", "sfx_host_free",
-            "sfx_fp64_peak")
+            "sfx_fp64_peak", "sfx_fp64_dfma_peak")
 
 _ERRORS = {
     ERR_CONFIG: ConfigurationError,

@@ -226,4 +226,20 @@ int sfx_fp64_peak(int ordinal, double* tflops, double* sm_mhz) {
   return SFX_OK;
 }
 
+int sfx_fp64_dfma_peak(int ordinal, double* tflops) {
+  int have = 0;
+  sfx_device_count(&have);
+  if (ordinal < 0 || ordinal >= have) {
+    g_err = "no such CUDA device";
+    return SFX_ERR_CUDA;
+  }
+  cudaSetDevice(ordinal);
+  cudaError_t e = sfx::fp64_dfma_peak(20000, tflops);
+  if (e != cudaSuccess) {
+    g_err = cudaGetErrorString(e);
+    return SFX_ERR_CUDA;
+  }
+  return SFX_OK;
+}
+
 }  // extern "C"

@@ -33,20 +33,25 @@
 namespace sfx {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4;
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3;
 constexpr int CONSUMER_WARPS = 8;
 // one producer warpgroup (4 warps, one elected TMA lane) + two DMMA warpgroups;
 // setmaxnreg moves registers from the producer to the consumers (40 / 232).
 constexpr int THREADS = (CONSUMER_WARPS + 4) * 32;
 constexpr int A_STAGE = BM * BK * 8;  // 16 KiB
 constexpr int B_STAGE = BN * BK * 8;  // 16 KiB
-constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 2 * STAGES * 8 + 1024;
+// C prefetch buffer: the producer TMA-loads the next epilogue's C tile (8 boxes
+// of 16 x 128 doubles, 128B swizzle) while the consumers are still in the
+// mainloop, so the epilogue reads C from shared memory instead of waiting on HBM
+constexpr int C_BUF = BM * BN * 8;  // 128 KiB
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + C_BUF + 2 * STAGES * 8 + 16 + 1024;
+static_assert(SMEM_BYTES <= 232448, "dynamic shared memory per CTA");
 
 // One launch covers G independent tile tasks of identical shape (grouped
 // launch): CTA blockIdx.x -> (task, output tile).  Each task carries its own
 // TMA descriptors in the (large, __grid_constant__) parameter block.
 struct alignas(64) GemmOperands {
-  CUtensorMap a, b;
+  CUtensorMap a, b, c;  // c: only when GemmGroup::cpref
   double* C;
 };
 
@@ -62,6 +67,7 @@ struct GemmGroup {
   int M, N, K;
   int tiles_n, tiles_per_task;
   int lower;
+  int cpref;  // C tiles of interior output tiles are prefetched by TMA (beta != 0, ksplit == 1, !lower)
   double alpha, beta;
 };
 
@@ -73,8 +79,11 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+  uint8_t* sC = sB + STAGES * B_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sC + C_BUF);
   uint64_t* empty = full + STAGES;
+  uint64_t* cfull = empty + STAGES;
+  uint64_t* cempty = cfull + 1;
 
   const int total = p.ntasks * p.tiles_per_task * p.ksplit;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -108,6 +117,8 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], CONSUMER_WARPS * 32);
     }
+    ptx::mbar_init(cfull, 1);
+    ptx::mbar_init(cempty, CONSUMER_WARPS * 32);
     ptx::fence_mbar_init();
   }
   __syncthreads();
@@ -118,7 +129,7 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
     // tile's operands stream in while the consumers finish the current one.
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     if (warp == CONSUMER_WARPS && lane == 0) {
-      int it = 0;
+      int it = 0, cn = 0;
       for (int lin = blockIdx.x; lin < total; lin += gridDim.x) {
         int task, m0, n0, kt0, kt1;
         coords(lin, task, m0, n0, kt0, kt1);
@@ -139,6 +150,16 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
               ptx::tma_load_2d(sB + s * B_STAGE + q * 2048, tmB, n0 + 16 * q, kt * BK, &full[s]);
           }
         }
+        // this tile's C, once the previous epilogue released the buffer; it lands
+        // while the consumers work through the last STAGES k-steps
+        if (p.cpref && m0 + BM <= p.M && n0 + BN <= p.N) {
+          if (cn > 0) ptx::mbar_wait(cempty, (cn - 1) & 1);
+          ptx::mbar_arrive_expect_tx(cfull, C_BUF);
+          const CUtensorMap* tmC = &p.t[task].c;
+#pragma unroll
+          for (int q = 0; q < BN / 16; ++q) ptx::tma_load_2d(sC + q * (BM * 128), tmC, n0 + 16 * q, m0, cfull);
+          ++cn;
+        }
       }
     }
     return;
@@ -148,7 +169,7 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
   asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
   const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warp grid, warp tile 64 x 32
   const int g = lane >> 2, t = lane & 3;
-  int it = 0;
+  int it = 0, cn = 0;
   for (int lin = blockIdx.x; lin < total; lin += gridDim.x) {
     int task, m0, n0, kt0, kt1;
     coords(lin, task, m0, n0, kt0, kt1);
@@ -230,6 +251,29 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
       continue;
     }
     const bool interior = !p.lower && m0 + BM <= p.M && n0 + BN <= p.N;
+    if (interior && p.cpref) {
+      // C from the prefetch buffer: element (r, c) of the tile sits in box q = c / 16
+      // at r * 128 + (((c % 16) / 2) ^ (r % 8)) * 16 + (c % 2) * 8 -- a warp's 32
+      // 16-byte reads cover every 128-byte row segment once (4 wavefronts, no conflict)
+      ptx::mbar_wait(cfull, cn & 1);
+      const uint32_t cS = ptx::smem_u32(sC);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = wm * 64 + 8 * i + g;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = wn * 32 + 8 * j + 2 * t;
+          const double2 cv = ptx::lds128(cS + (c >> 4) * (BM * 128) + r * 128 + ((((c & 15) >> 1) ^ g) << 4));
+          double2 v;
+          v.x = fma(p.beta, cv.x, p.alpha * acc[i][j][0]);
+          v.y = fma(p.beta, cv.y, p.alpha * acc[i][j][1]);
+          *reinterpret_cast<double2*>(Cbase + static_cast<long long>(m0 + r) * p.ldc + n0 + c) = v;
+        }
+      }
+      ptx::mbar_arrive(cempty);  // this thread's reads of the buffer are done
+      ++cn;
+      continue;
+    }
     if (interior) {
 #pragma unroll
       for (int half = 0; half < 4; ++half) {  // 4 x 8 fragments: loads in flight together, no spills
@@ -401,6 +445,8 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
     if (!ok) return cudaErrorInvalidValue;
     p.t[i].C = d[i].C;
   }
+  // split-K decided below; the C prefetch needs beta != 0, no split and a full tile
+  const bool want_cpref = beta != 0.0 && !lower && M >= BM && N >= BN;
   p.ldc = d[0].ldc;
   p.M = M;
   p.N = N;
@@ -420,6 +466,10 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
     const int tiles = p.tiles_per_task * n, ksteps = (K + BK - 1) / BK;
     while (tiles * p.ksplit * 2 <= num_sms() && ksteps / (p.ksplit * 2) >= 8) p.ksplit *= 2;
   }
+  p.cpref = want_cpref && p.ksplit == 1 ? 1 : 0;
+  if (p.cpref)
+    for (int i = 0; i < n; ++i)
+      if (!make_tmap_f64_2d(&p.t[i].c, d[i].C, N, M, d[i].ldc, 16, BM, true)) return cudaErrorInvalidValue;
   const int total = p.tiles_per_task * n * p.ksplit;
   // persistent CTAs, at most tiles_per_cta() output tiles each: the operand
   // ring streams the next tile during the epilogue, while SMs still free up

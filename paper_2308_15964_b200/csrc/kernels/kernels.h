@@ -89,5 +89,6 @@ cudaError_t launch_cell(long long* target, const long long* const* reads, int nr
                         long long b, cudaStream_t s);
 cudaError_t launch_bytes_add(unsigned char* p, long long off, long long len, long long delta, cudaStream_t s);
 cudaError_t fp64_dmma_peak(int iters, double* tflops);
+cudaError_t fp64_dfma_peak(int iters, double* tflops);
 
 }  // namespace sfx

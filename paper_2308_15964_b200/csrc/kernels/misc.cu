@@ -122,6 +122,22 @@ __global__ void dmma_peak_kernel(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+// FP64 pipe (DFMA) peak: 8 independent FMA chains per thread
+__global__ void dfma_peak_kernel(double* out, int iters) {
+  double a = 1.0 - threadIdx.x * 1e-9, b = 1e-9 * blockIdx.x;
+  double c[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i] = i * 1e-3;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i] = fma(c[i], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i];
+  if (s == 12345.678) out[0] = s;
+}
+
 inline unsigned grid_for(long long n, int bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
 
 }  // namespace
@@ -201,6 +217,33 @@ cudaError_t launch_bytes_add(unsigned char* p, long long off, long long len, lon
   count_launch();
   bytes_add_kernel<<<grid_for(len, 256), 256, 0, s>>>(p, off, len, delta);
   return cudaGetLastError();
+}
+
+cudaError_t fp64_dfma_peak(int iters, double* tflops) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* out;
+  cudaError_t e = cudaMalloc(&out, 8);
+  if (e) return e;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int threads = 512, blocks = 4 * sms;
+  count_launch();
+  dfma_peak_kernel<<<blocks, threads>>>(out, 100);  // warm-up
+  cudaEventRecord(e0);
+  count_launch();
+  dfma_peak_kernel<<<blocks, threads>>>(out, iters);
+  cudaEventRecord(e1);
+  e = cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *tflops = 2.0 * 8 * static_cast<double>(iters) * blocks * threads / (ms * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return e ? e : cudaGetLastError();
 }
 
 cudaError_t fp64_dmma_peak(int iters, double* tflops) {

@@ -206,4 +206,11 @@ def fp64_peak(ordinal: int = 0):
     return t.value, mhz.value
 
 
+def fp64_dfma_peak(ordinal: int = 0) -> float:
+    """Measured FP64 pipe (DFMA) peak in TFLOP/s (2 flop per FMA)."""
+    t = ctypes.c_double(0)
+    N.check(N.lib.sfx_fp64_dfma_peak(ordinal, ctypes.byref(t)))
+    return t.value
+
+
 HOST_KIND = HOST
