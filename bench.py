@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--streams", type=int, default=16)
     ap.add_argument("--group", type=int, default=32)
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--e2e-row-priorities", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -266,7 +267,9 @@ def main_ours(args, dist):
 
     # ---- e2e: host-resident inputs through the public API ----
     def e2e_step():
-        alg.insert_gemm(g, A, B, C)
+        # block-row priorities: rows of C finish one after another, so their flush
+        # (D2H) and the next rows' staging (H2D) overlap the remaining compute
+        alg.insert_gemm(g, A, B, C, priorities=args.e2e_row_priorities)
         for t in C.tiles.values():
             g.flush_to_host(t)                      # C back to the host (write-mode flush)
         for M in (A, B):
