@@ -48,9 +48,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--workload", choices=("gemm", "cholesky"), default="gemm",
+    ap.add_argument("--workload", choices=("gemm", "cholesky", "particles"), default="gemm",
                     help="gemm: C2 tiled DGEMM (default, BASELINE configs[1]); cholesky: tiled Cholesky over "
-                         "all --gpus GPUs from one runtime (C3 at n=32768/1024, C5 at n=65536/1024)")
+                         "all --gpus GPUs from one runtime (C3 at n=32768/1024, C5 at n=65536/1024); "
+                         "particles: C4 (2^20 particles, 256 groups) over all --gpus GPUs from one runtime")
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--b", type=int, default=None)
     ap.add_argument("--streams", type=int, default=16)
@@ -521,6 +522,70 @@ def main_cholesky(args, dist):
     dist.barrier()
 
 
+def main_particles(args, dist):
+    """C4 over all GPUs of the node from ONE runtime (rank 0): pair tasks dealt to the
+    GPUs, per-GPU partial accumulators, one dacc reduction per group."""
+    import torch
+
+    import paper_2308_15964_b200 as sf
+    from paper_2308_15964_b200 import algorithms as alg
+
+    ndev = max(args.gpus, dist.world)
+    if dist.rank != 0:
+        dist.barrier()
+        return
+    ng, per = 256, 4096
+    dfma_tf = sf.fp64_dfma_peak(0)
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(ndev, args.streams), trace=False, ordinals=list(range(ndev)),
+                           group_max=args.group)
+    P = [sf.pinned_empty((4, per)) for _ in range(ng)]
+    F = [sf.pinned_empty((4, per)) for _ in range(ng)]
+    g = sf.TaskGraph().compute_on(eng)
+    alg.insert_fill_particles(g, P, 4)
+    g.wait_all()
+    parts = None
+    times = []
+    clocks = ClockSampler(0)
+    for rep in range(args.warmup + args.steps):
+        for f in F:
+            g.task(sf.write(f), device=sf.ops.zero())
+        g.wait_all()
+        for d in range(ndev):
+            torch.cuda.synchronize(d)
+        if rep == args.warmup:
+            clocks.start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        parts = alg.insert_particles(g, P, F, partials=parts)
+        g.wait_all()
+        e1.record()
+        torch.cuda.synchronize()
+        if rep >= args.warmup:
+            times.append(e0.elapsed_time(e1) / 1e3)
+    clk = clocks.stop()
+    stats = [eng.stats(d) for d in range(ndev)]
+    eng.stop()
+    t = statistics.mean(times)
+    inter = alg.interactions(ng * per)
+    bound = ndev * dfma_tf * 1e12 / 2 / 11.5
+    line = {
+        "metric": "particle interactions/s (C4, FP64)", "value": inter / t, "unit": "interactions/s",
+        "n_gpus": ndev, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (positions uniform in the unit cube, charges in [0.5, 1], generated on device)",
+        "config": {"workload": f"particles {ng * per} in {ng} groups, 32896 tasks, {ndev} GPU(s) from one runtime",
+                   "parallelism": "pair tasks in balanced blocks per GPU, per-GPU partial accumulators, "
+                                  "dacc reduction (peer pulls)", "l2": "one evaluation per step"},
+        "clocks": clk,
+        "roofline": {"bound": "fp64 pipe", "achieved": inter / t, "peak": bound, "unit": "interactions/s",
+                     "frac": inter / t / bound, "dfma_peak_tflops_per_gpu": dfma_tf},
+        "p2p_bytes": sum(s["bytes_p2p_in"] for s in stats),
+        "gpu_launches": stats[0]["kernel_launches"],
+    }
+    print(json.dumps(line), flush=True)
+    dist.barrier()
+
+
 def main():
     args = parse()
     dist = Dist()
@@ -530,6 +595,8 @@ def main():
     dist.init("nccl")
     if args.workload == "cholesky":
         main_cholesky(args, dist)
+    elif args.workload == "particles":
+        main_particles(args, dist)
     else:
         args.n, args.b = args.n or 16384, args.b or 512
         main_ours(args, dist)

@@ -101,6 +101,8 @@ extern "C" {
 #define SFX_OP_FILL_SPD 31     /* A = (R+R^T)/2 + n*I tile: iparam={seed,row0,col0,n}    */
 #define SFX_OP_FILL_PARTICLES 32 /* P (4 x n SoA x,y,z,q): iparam={seed,first_particle}  */
 #define SFX_OP_ZERO 33         /* A = 0                                                  */
+#define SFX_OP_DACC 34         /* A += B1 + ... + Bk (FP64, same rows x cols, k = 1..7):
+                                  the reduction of per-GPU partial accumulators        */
 
 /* ---- trace event kinds (trace.py:14-21) ---- */
 #define SFX_EV_PUSH 0

@@ -60,6 +60,7 @@ OP_FILL_UNIFORM = 30
 OP_FILL_SPD = 31
 OP_FILL_PARTICLES = 32
 OP_ZERO = 33
+OP_DACC = 34
 
 EV_PUSH, EV_POP, EV_START, EV_END, EV_STAGE_BEGIN, EV_STAGE_END = range(6)
 EV_NAMES = {EV_PUSH: "Push", EV_POP: "Pop", EV_START: "TaskStart", EV_END: "TaskEnd",

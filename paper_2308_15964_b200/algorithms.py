@@ -275,10 +275,27 @@ def insert_cholesky(graph, A: TiledMatrix, fast: bool = True, priorities="auto",
     return batch.submit() if batch else None
 
 
-def insert_particles(graph, P: list, F: list, eps2: float = 1e-9, fast: bool = True):
-    """All-pairs interactions between particle groups, commutative accumulation into F."""
+def insert_particles(graph, P: list, F: list, eps2: float = 1e-9, fast: bool = True, devices=None,
+                     partials=None):
+    """All-pairs interactions between particle groups, commutative accumulation into F.
+
+    On one GPU every task accumulates into F directly (commutative groups, shared
+    guards: the kernel's updates are device atomics).  With ``devices`` > 1 (default:
+    the engine's device count) the program follows SURVEY.md §8e: device d > 0 gets
+    private zeroed partial accumulators Fd[g] (homed on d), the pair tasks are dealt
+    to the devices in balanced contiguous blocks (positions replicate lazily by
+    peer pulls, 128 KiB per group), device 0 accumulates into F itself, and one
+    ``dacc`` task per group adds the partials into F[g] (peer pulls of 128 KiB per
+    partial).  Returns the list of partial accumulators (keep them alive until
+    wait_all) or None.
+    """
     ng = len(P)
     self_op, pair_op = ops.p2p_self(eps2), ops.p2p_pair(eps2)
+    if devices is None:
+        eng = getattr(graph, "engine", None)
+        devices = getattr(eng, "ndev", 1) if eng is not None else 1
+    if devices > 1:
+        return _insert_particles_multi(graph, P, F, self_op, pair_op, min(devices, 8), partials)
     if not fast:
         for g in range(ng):
             graph.task(read(P[g]), commutative_write(F[g]), device=self_op, name="p2p_self")
@@ -299,6 +316,39 @@ def insert_particles(graph, P: list, F: list, eps2: float = 1e-9, fast: bool = T
         batch.add_many(pair_op, pairs[c0:c0 + 4096], (R, R, CW, CW), 0, "p2p_pair")
         batch.flush()
     return batch.submit()
+
+
+def _insert_particles_multi(graph, P, F, self_op, pair_op, ndev, partials=None):
+    ng = len(P)
+    for f in F:
+        graph.place(f, 0)
+    if partials is None or len(partials) != ndev - 1:
+        partials = [[pinned_empty(f.shape, np.float64) for f in F] for _ in range(1, ndev)]
+    for d, Fd in enumerate(partials, start=1):
+        for f in Fd:
+            graph.place(f, d)
+            graph.task(write(f), device=ops.zero(), name="zero_partial")
+    acc = [F] + partials  # acc[d][g]: device d's accumulator of group g
+
+    HP = np.array([graph.hid_of(p) for p in P], np.uint64)
+    HF = np.array([[graph.hid_of(f) for f in acc[d]] for d in range(ndev)], np.uint64)
+    R, CW = AccessMode.READ.code, AccessMode.COMMUTATIVE_WRITE.code
+    batch = _Batch(graph)
+    # self tasks round-robin, pair tasks in contiguous balanced blocks (consecutive
+    # tasks on a device then reuse each other's source groups)
+    gg = np.arange(ng)
+    batch.add_many(self_op, np.stack([HP, HF[gg % ndev, gg]], axis=1), (R, CW), 0, "p2p_self")
+    batch.flush()
+    ii, jj = np.triu_indices(ng, 1)
+    dd = np.arange(len(ii)) * ndev // len(ii)
+    pairs = np.stack([HP[ii], HP[jj], HF[dd, ii], HF[dd, jj]], axis=1)
+    for c0 in range(0, len(pairs), 4096):
+        batch.add_many(pair_op, pairs[c0:c0 + 4096], (R, R, CW, CW), 0, "p2p_pair")
+        batch.flush()
+    batch.submit()
+    for g in range(ng):
+        graph.task(write(F[g]), *[read(acc[d][g]) for d in range(1, ndev)], device=ops.dacc(), name="reduce")
+    return partials
 
 
 def insert_fill_uniform(graph, M: TiledMatrix, seed: int):

@@ -84,6 +84,9 @@ cudaError_t launch_fill_spd(double* a, long long rows, long long cols, long long
 cudaError_t launch_fill_particles(double* p, long long n, long long ld, long long seed, long long first,
                                   cudaStream_t s);
 cudaError_t launch_spin(long long ns, cudaStream_t s);
+// A += sum of n addends (FP64 rows x cols, each with its own ld), n <= 7
+cudaError_t launch_dacc(double* a, long long lda, long long rows, long long cols, const double* const* add,
+                        const long long* ld, int n, cudaStream_t s);
 cudaError_t launch_add_i64(long long* const* cells, int n, long long delta, cudaStream_t s);
 cudaError_t launch_cell(long long* target, const long long* const* reads, int nreads, long long kind, long long a,
                         long long b, cudaStream_t s);

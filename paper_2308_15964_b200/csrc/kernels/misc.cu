@@ -182,6 +182,44 @@ __global__ void add_i64_kernel(AddI64Args a) {
 }
 }  // namespace
 
+namespace {
+struct DaccArgs {
+  double* a;
+  const double* add[7];
+  long long ld[7];
+  long long lda, rows, cols;
+  int n;
+};
+// SFX_OP_DACC: a += add_1 + ... + add_n, one element per thread (HBM-bound; the
+// addends are per-GPU partial accumulators pulled peer-to-peer before the launch)
+__global__ void dacc_kernel(DaccArgs p) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= p.rows * p.cols) return;
+  const long long r = i / p.cols, c = i - r * p.cols;
+  double v = p.a[r * p.lda + c];
+  for (int k = 0; k < p.n; ++k) v += p.add[k][r * p.ld[k] + c];
+  p.a[r * p.lda + c] = v;
+}
+}  // namespace
+
+cudaError_t launch_dacc(double* a, long long lda, long long rows, long long cols, const double* const* add,
+                        const long long* ld, int n, cudaStream_t s) {
+  DaccArgs p{};
+  p.a = a;
+  p.lda = lda;
+  p.rows = rows;
+  p.cols = cols;
+  p.n = n < 7 ? n : 7;
+  for (int k = 0; k < p.n; ++k) {
+    p.add[k] = add[k];
+    p.ld[k] = ld[k];
+  }
+  if (rows * cols <= 0) return cudaSuccess;
+  count_launch();
+  dacc_kernel<<<grid_for(rows * cols, 256), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_add_i64(long long* const* cells, int n, long long delta, cudaStream_t s) {
   AddI64Args a{};
   a.n = n < 8 ? n : 8;

@@ -200,6 +200,7 @@ class CudaBackend : public Backend {
       case SFX_OP_CELL:
       case SFX_OP_BYTES_ADD:
       case SFX_OP_ADD_I64:
+      case SFX_OP_DACC:
       case SFX_OP_FLUSH:
       case SFX_OP_ZERO:
       case SFX_OP_DGEMM:
@@ -232,6 +233,16 @@ class CudaBackend : public Backend {
       case SFX_OP_BYTES_ADD:
         e = launch_bytes_add(static_cast<unsigned char*>(o[0].dptr), op.ip[0], op.ip[1], op.ip[2], s);
         break;
+      case SFX_OP_DACC: {
+        const double* add[7];
+        long long ld[7];
+        for (int k = 1; k < op.n; ++k) {
+          add[k - 1] = f64(o[k]);
+          ld[k - 1] = o[k].ld;
+        }
+        e = launch_dacc(f64(o[0]), o[0].ld, o[0].rows, o[0].cols, add, ld, op.n - 1, s);
+        break;
+      }
       case SFX_OP_ADD_I64: {
         long long* cells[8];
         for (int k = 0; k < op.n; ++k) cells[k] = static_cast<long long*>(o[k].dptr);

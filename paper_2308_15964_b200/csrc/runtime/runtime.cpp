@@ -396,6 +396,20 @@ int Runtime::validate(const sfx_task_desc& d, const sfx_access* acc, std::string
         return SFX_ERR_CONFIG;
       }
       return 0;
+    case SFX_OP_DACC:
+      if (d.n_access < 2 || d.n_access > 8) {
+        err = "dacc takes a target plus 1 to 7 addends";
+        return SFX_ERR_CONFIG;
+      }
+      if (!writes(0)) return SFX_ERR_CONFIG;
+      for (uint32_t k = 0; k < d.n_access; ++k) {
+        if ((rc = expect_f64(hs[k], "dacc operand", err))) return rc;
+        if (hs[k]->rows != hs[0]->rows || hs[k]->cols != hs[0]->cols) {
+          err = "dacc: operands must have the same rows x cols";
+          return SFX_ERR_CONFIG;
+        }
+      }
+      return 0;
     case SFX_OP_FLUSH:
       if (!need(1)) return SFX_ERR_CONFIG;
       return 0;

@@ -97,6 +97,11 @@ def zero() -> Op:
     return Op("zero", N.OP_ZERO)
 
 
+def dacc() -> Op:
+    """A += B1 + ... + Bk (k <= 7): sums per-GPU partial accumulators into their target."""
+    return Op("dacc", N.OP_DACC)
+
+
 def spin(ns: int) -> Op:
     return Op("spin", N.OP_SPIN, iparam=(int(ns),))
 

@@ -67,3 +67,33 @@ def test_random_programs_on_two_devices():
             assert [c.value for c in cells] == p["sequential"]
     finally:
         eng.stop()
+
+
+@pytest.mark.parametrize("ndev", [2, 3])
+def test_particles_with_per_device_partials(ndev):
+    """SURVEY.md §8e for C4: pair tasks dealt to the devices, private per-device
+    accumulators, one dacc reduction per group (peer pulls) -- same result as the
+    oracle within the particle tolerances."""
+    ng, per = 6, 512
+    objs = programs.particle_operands(ng, per)
+    want = {k: v.copy() for k, v in objs.items()}
+    programs.run_on_oracle(programs.particles_program(ng), want, workers=4)
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(ndev, 3), device_memory=1 << 30, ordinals=[0] * ndev)
+    try:
+        P = [sf.pinned_empty((4, per)) for _ in range(ng)]
+        F = [sf.pinned_zeros((4, per)) for _ in range(ng)]
+        for g in range(ng):
+            P[g][...] = objs[("P", g)]
+        gr = sf.TaskGraph().compute_on(eng)
+        parts = alg.insert_particles(gr, P, F)
+        assert parts is not None and len(parts) == ndev - 1
+        gr.flush_all(keep_device=False)
+        assert gr.wait_all(timeout=120)
+        assert all(eng.stats(d)["tasks_executed"] > 0 for d in range(ndev))
+        assert sum(eng.stats(d)["bytes_p2p_in"] for d in range(ndev)) > 0
+        for g in range(ng):
+            w = want[("F", g)]
+            assert (np.abs(F[g][3] - w[3]) / np.abs(w[3])).max() <= 1e-10
+            assert np.abs(F[g][:3] - w[:3]).max() <= 1e-11 * np.abs(w[:3]).max()
+    finally:
+        eng.stop()
