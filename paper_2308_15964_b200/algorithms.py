@@ -154,10 +154,11 @@ def _emit(graph, fast):
 
 
 def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: bool = True,
-                priorities: bool = False):
+                priorities=False):
     """C += A B over tiles, loop order i, j, k.
 
-    ``priorities``: block row i gets priority nt - i, so with the priority
+    ``priorities`` (False, True or a row-block height h): block row i gets priority
+    (nt - i) // h (h = 1 for True), so with the priority
     scheduler the rows of C finish one after another (a few rows in flight)
     instead of every chain advancing in lock-step -- staging of A/C rows and the
     flush of finished C tiles then overlap the remaining compute.
@@ -166,7 +167,7 @@ def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: boo
     if not fast:
         for i in range(nt):
             for j in range(nt):
-                prio = nt - i if priorities else 0
+                prio = (nt - i) // int(priorities) if priorities else 0
                 for k in range(nt):
                     graph.task(read(A[i, k]), read(B[k, j]), write(C[i, j]), device=ops.gemm_nn,
                                priority=prio, name="gemm")
@@ -180,7 +181,7 @@ def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: boo
     jj, kk = jj.reshape(-1), kk.reshape(-1)
     for i in range(nt):
         hids = np.stack([HA[i, kk], HB[kk, jj], HC[i, jj]], axis=1)
-        batch.add_many(ops.gemm_nn, hids, modes, nt - i if priorities else 0, "gemm")
+        batch.add_many(ops.gemm_nn, hids, modes, (nt - i) // int(priorities) if priorities else 0, "gemm")
         batch.flush()
     return batch.submit()
 
