@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--b", type=int, default=None)
     ap.add_argument("--streams", type=int, default=32)
     ap.add_argument("--group", type=int, default=32)
+    ap.add_argument("--chol-group", type=int, default=8,
+                    help="launch-group size for the Cholesky legs (tools/chol_sweep.py: 8 best for b=1024)")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--e2e-row-priorities", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -368,7 +370,7 @@ def secondary(sf, alg, dev, args, peak_tf):
     out = {}
     # C3: tiled Cholesky 32768 / 1024 on one GPU
     eng = sf.create_engine(sf.WorkerTeam.of_devices(1, args.streams), scheduler="prio", trace=False,
-                           ordinals=[dev], group_max=args.group)
+                           ordinals=[dev], group_max=args.chol_group)
     n, b = 32768, 1024
     M = alg.TiledMatrix(n, b, lower=True)
     g = sf.TaskGraph().compute_on(eng)
@@ -487,7 +489,7 @@ def main_cholesky(args, dist):
     nt = n // b
     peak_tf, _ = sf.fp64_peak(0)
     eng = sf.create_engine(sf.WorkerTeam.of_devices(ndev, args.streams), scheduler="prio", trace=False,
-                           ordinals=list(range(ndev)), group_max=args.group)
+                           ordinals=list(range(ndev)), group_max=args.chol_group)
     M = alg.TiledMatrix(n, b, lower=True)
     P, Q = alg.grid_shape(ndev)
     times = []
