@@ -52,8 +52,8 @@ def parse():
                     help="gemm: C2 tiled DGEMM (default, BASELINE configs[1]); cholesky: tiled Cholesky over "
                          "all --gpus GPUs from one runtime (C3 at n=32768/1024, C5 at n=65536/1024); "
                          "particles: C4 (2^20 particles, 256 groups) over all --gpus GPUs from one runtime")
-    ap.add_argument("--n", type=int, default=None)
-    ap.add_argument("--b", type=int, default=None)
+    ap.add_argument("--n", "--matrix-n", dest="n", type=int, default=None)
+    ap.add_argument("--b", "--tile-b", dest="b", type=int, default=None)
     ap.add_argument("--streams", type=int, default=32)
     ap.add_argument("--group", type=int, default=32)
     ap.add_argument("--chol-group", type=int, default=8,
@@ -73,8 +73,10 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.backend = None
 
     def init(self, backend="nccl"):
+        self.backend = backend
         if self.world > 1:
             import torch
             import torch.distributed as dist
@@ -93,7 +95,7 @@ class Dist:
             return x
         import torch
 
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if self.backend == "nccl" else "cpu")
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
 

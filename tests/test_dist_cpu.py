@@ -1,0 +1,57 @@
+"""The N>1 launch path on CPU: torchrun with world_size 2 over gloo (127.0.0.1).
+
+bench.py's per-rank plumbing (Dist: barrier, max over ranks) and the reference
+arm's rank discipline (rank 0 alone runs and prints ONE JSON line; the other
+ranks exit 0 without work) are what the driver relies on at N > 1.
+"""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _torchrun(args, timeout=240):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port())] + args
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    return subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=timeout)
+
+
+def test_dist_max_over_ranks_gloo(tmp_path):
+    script = tmp_path / "ranks.py"
+    script.write_text(
+        "import json, os, sys\n"
+        f"sys.path.insert(0, {ROOT!r})\n"
+        "import bench\n"
+        "d = bench.Dist()\n"
+        "d.init('gloo')\n"
+        "d.barrier()\n"
+        "m = d.max(float(d.rank + 1) * 1.5)\n"
+        "print(json.dumps({'rank': d.rank, 'world': d.world, 'max': m}), flush=True)\n"
+        "d.done()\n")
+    r = _torchrun([str(script)])
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert sorted(x["rank"] for x in lines) == [0, 1]
+    assert all(x["world"] == 2 and x["max"] == 3.0 for x in lines)
+
+
+def test_reference_arm_prints_once_under_torchrun():
+    r = _torchrun(["bench.py", "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0",
+                   "--matrix-n", "1024", "--tile-b", "256", "--cpu-seconds", "0.5"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = lines[0]
+    assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "GFLOP/s"
+    assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
