@@ -87,6 +87,13 @@ extern "C" {
                                   (tests/conftest.py:87-124): iparam = {kind, a, b}   */
 #define SFX_OP_BYTES_ADD 3     /* bytes[off:off+len] += delta (mod 256): iparam={off,len,delta} */
 #define SFX_OP_FLUSH 4         /* runtime-internal host flush (write or read mode)    */
+#define SFX_OP_EXTERN 6        /* one access; executed OUTSIDE the runtime by a host agent
+                                  (inter-process send/recv/broadcast, reference
+                                  comms.py:303-483): when ready, its host buffer is made
+                                  current (read: dirty device copy fetched home; write:
+                                  device copies dropped), then the task is handed out by
+                                  sfx_extern_poll and finished by sfx_extern_done, which
+                                  releases its successors                              */
 #define SFX_OP_ADD_I64 5       /* every operand (int64 cells): += iparam[0] with device
                                   atomics.  Like P2P_PAIR/P2P_SELF it accumulates
                                   atomically, so its commutative members of one group run
@@ -223,6 +230,13 @@ int sfx_violations(sfx_runtime* rt, uint64_t* n);
  * all streams are busy, default 1 on CUDA), "prefetch_depth" (queued tasks
  * looked at, default 64) */
 int sfx_set_option(sfx_runtime* rt, const char* key, int64_t value);
+
+/* external tasks (SFX_OP_EXTERN): block up to timeout_s (< 0: forever) until at
+ * least one is ready, copy up to cap task ids to tids (*n = count; 0 on timeout
+ * or shutdown).  The agent performs the transfer on the object's host buffer and
+ * reports it with sfx_extern_done (status != 0 poisons the engine with msg). */
+int sfx_extern_poll(sfx_runtime* rt, uint64_t* tids, uint64_t cap, uint64_t* n, double timeout_s);
+int sfx_extern_done(sfx_runtime* rt, uint64_t tid, int status, const char* msg);
 
 /* pinned host memory (cudaHostAlloc; aligned malloc in sim) for tiles */
 int sfx_host_alloc(uint64_t bytes, int sim, void** out);

@@ -49,6 +49,7 @@ OP_SPIN = 1
 OP_CELL = 2
 OP_BYTES_ADD = 3
 OP_FLUSH = 4
+OP_EXTERN = 6
 OP_ADD_I64 = 5
 OP_DGEMM = 10
 OP_DSYRK = 11
@@ -139,6 +140,9 @@ def _load():
         "sfx_host_free": ([P, ctypes.c_int], ctypes.c_int),
         "sfx_fp64_peak": ([ctypes.c_int, ctypes.POINTER(dbl), ctypes.POINTER(dbl)], ctypes.c_int),
         "sfx_fp64_dfma_peak": ([ctypes.c_int, ctypes.POINTER(dbl)], ctypes.c_int),
+        "sfx_extern_poll": ([P, ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), ctypes.c_double],
+                            ctypes.c_int),
+        "sfx_extern_done": ([P, ctypes.c_uint64, ctypes.c_int, ctypes.c_char_p], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -155,7 +159,7 @@ EXPORTED = ("sfx_abi_version", "sfx_device_count", "sfx_create", "sfx_destroy", 
             "sfx_submit", "sfx_pause", "sfx_resume", "sfx_wait_all", "sfx_wait_task",
             "sfx_task_state", "sfx_flush", "sfx_stats", "sfx_resident", "sfx_block_state",
             "sfx_trace", "sfx_edges", "sfx_violations", "sfx_set_option", "sfx_host_alloc", "sfx_host_free",
-            "sfx_fp64_peak", "sfx_fp64_dfma_peak")
+            "sfx_fp64_peak", "sfx_fp64_dfma_peak", "sfx_extern_poll", "sfx_extern_done")
 
 _ERRORS = {
     ERR_CONFIG: ConfigurationError,

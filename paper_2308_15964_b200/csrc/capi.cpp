@@ -153,6 +153,14 @@ int sfx_stats(sfx_runtime* r, int dev, sfx_dev_stats* out) {
   return guarded(r, [&](sfx::Runtime& rt) { return rt.stats(dev, out); });
 }
 
+int sfx_extern_poll(sfx_runtime* r, uint64_t* tids, uint64_t cap, uint64_t* n, double timeout_s) {
+  return guarded(r, [&](sfx::Runtime& rt) { return rt.extern_poll(tids, cap, n, timeout_s); });
+}
+
+int sfx_extern_done(sfx_runtime* r, uint64_t tid, int status, const char* msg) {
+  return guarded(r, [&](sfx::Runtime& rt) { return rt.extern_done(tid, status, msg); });
+}
+
 int sfx_resident(sfx_runtime* r, int dev, uint64_t* hids, uint64_t cap, uint64_t* n) {
   return guarded(r, [&](sfx::Runtime& rt) { return rt.resident(dev, hids, cap, n); });
 }

@@ -200,6 +200,7 @@ class CudaBackend : public Backend {
       case SFX_OP_CELL:
       case SFX_OP_BYTES_ADD:
       case SFX_OP_ADD_I64:
+      case SFX_OP_EXTERN:
       case SFX_OP_DACC:
       case SFX_OP_FLUSH:
       case SFX_OP_ZERO:

@@ -121,6 +121,7 @@ Runtime::~Runtime() {
       d->comp_cv.notify_all();
     }
     done_cv_.notify_all();
+    extern_cv_.notify_all();
   }
   for (auto& d : devs_) {
     if (d->exec_thread.joinable()) d->exec_thread.join();
@@ -411,6 +412,7 @@ int Runtime::validate(const sfx_task_desc& d, const sfx_access* acc, std::string
       }
       return 0;
     case SFX_OP_FLUSH:
+    case SFX_OP_EXTERN:
       if (!need(1)) return SFX_ERR_CONFIG;
       return 0;
     default:
@@ -510,7 +512,7 @@ int Runtime::flush(uint32_t gid, uint64_t tid, uint64_t hid, int write_mode) {
 int Runtime::place(Task* t) {
   if (ndev_ == 1) return 0;
   if (t->hint >= 0) return t->hint % ndev_;
-  if (t->op == SFX_OP_FLUSH) {
+  if (t->op == SFX_OP_FLUSH || t->op == SFX_OP_EXTERN) {
     Handle* h = t->acc[0].h;
     if (h->dirty_dev >= 0) return h->dirty_dev;
     for (int e = 0; e < ndev_; ++e)
@@ -780,7 +782,7 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
   // pass 1: blocks for every operand (may evict; victims are written back)
   std::vector<Block*> pins;
   std::vector<Block*> blocks(t->acc.size(), nullptr);
-  if (t->op != SFX_OP_FLUSH) {
+  if (t->op != SFX_OP_FLUSH && t->op != SFX_OP_EXTERN) {
     for (size_t k = 0; k < t->acc.size(); ++k) {
       int rc = ensure_block(d, s, t->acc[k].h, acts, pins, &blocks[k], err);
       if (rc) {
@@ -803,6 +805,45 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
     if (a.mode == SFX_COMMUTATIVE_WRITE) wait_on(a.h->commute_last);
   if (t->start && record_start) acts.push_back(Action{Action::RECORD, t->start});
 
+  if (t->op == SFX_OP_EXTERN) {
+    // make the host buffer current for the agent: a read (send) fetches the dirty
+    // copy home and keeps device copies; a write (recv) drops every device copy
+    // (the agent overwrites the whole buffer; host_valid is set by extern_done)
+    Handle* h = t->acc[0].h;
+    if (!mode_writes(t->acc[0].mode)) {
+      if (h->dirty_dev >= 0) {
+        Block* b = h->blocks[h->dirty_dev];
+        if (h->dirty_dev != d) {
+          err = "extern task placed away from the dirty copy";
+          return SFX_ERR_INTERNAL;
+        }
+        wait_on(b->ready);
+        Action cp{Action::D2H, nullptr};
+        cp.host = h->host;
+        cp.src_off = b->off;
+        cp.n = h->bytes;
+        acts.push_back(cp);
+        b->dirty = false;
+        b->pins += 1;
+        t->pinned.push_back(b);
+        h->dirty_dev = -1;
+        h->host_valid = true;
+        h->host_ready = t->end;
+        D.stats.bytes_from_device += h->bytes;
+        D.stats.copies_from_device += 1;
+      } else {
+        wait_on(h->host_ready);
+      }
+    } else {
+      for (int e = 0; e < ndev_; ++e)
+        if (h->blocks[e]) drop_block(h->blocks[e], false, nullptr, s);
+      h->dirty_dev = -1;
+      h->host_valid = false;
+    }
+    op.op = SFX_OP_EXTERN;
+    op.n = 0;
+    return 0;
+  }
   if (t->op == SFX_OP_FLUSH) {
     // graph.py:258-260 + device.py:318-326: fetch the dirty copy home; a
     // write-mode flush then drops every device copy
@@ -958,7 +999,7 @@ int Runtime::issue(int d, int s, const std::vector<Task*>& group, std::vector<Ac
   std::vector<OpLaunch> kern;
   kern.reserve(ops.size());
   for (auto& op : ops)
-    if (op.op != SFX_OP_FLUSH && op.op != SFX_OP_NOOP) kern.push_back(op);
+    if (op.op != SFX_OP_FLUSH && op.op != SFX_OP_NOOP && op.op != SFX_OP_EXTERN) kern.push_back(op);
   if (!kern.empty()) {
     rc = be_->launch_group(d, s, kern, err);
     if (rc) return rc;
@@ -1071,7 +1112,7 @@ bool Runtime::commute_conflict(const std::vector<Task*>& group, const Task* t) c
 
 void Runtime::complete(Task* t) {
   Device& D = *devs_[t->dev];
-  if (t->end && !t->end->group_counted) {
+  if (!t->detached && t->end && !t->end->group_counted) {
     t->end->group_counted = true;
     D.stream_groups[t->stream] -= 1;
   }
@@ -1113,11 +1154,68 @@ void Runtime::complete(Task* t) {
   t->state = SFX_STATE_FINISHED;
   if (!t->commute.empty()) release_commute(t);
   g->completed += 1;
-  D.ninflight -= 1;
-  D.stream_inflight[t->stream] -= 1;
+  if (!t->detached) {
+    D.ninflight -= 1;
+    D.stream_inflight[t->stream] -= 1;
+  }
   D.stats.tasks_executed += 1;
   D.exec_cv.notify_one();
   done_cv_.notify_all();
+}
+
+void Runtime::extern_handoff(Task* t) {
+  // the stream slot is free as soon as the host copy is current: a recv may wait
+  // for its peer for a long time
+  Device& D = *devs_[t->dev];
+  if (t->end && !t->end->group_counted) {
+    t->end->group_counted = true;
+    D.stream_groups[t->stream] -= 1;
+  }
+  D.ninflight -= 1;
+  D.stream_inflight[t->stream] -= 1;
+  t->detached = true;
+  extern_ready_.push_back(t);
+  extern_cv_.notify_all();
+  D.exec_cv.notify_one();
+}
+
+int Runtime::extern_poll(uint64_t* tids, uint64_t cap, uint64_t* n, double timeout_s) {
+  std::unique_lock<std::mutex> lk(mu_);
+  auto ready = [&] { return stopping_ || fail_code_ != 0 || !extern_ready_.empty(); };
+  if (timeout_s < 0)
+    extern_cv_.wait(lk, ready);
+  else
+    extern_cv_.wait_for(lk, std::chrono::duration<double>(timeout_s), ready);
+  uint64_t k = 0;
+  while (k < cap && !extern_ready_.empty()) {
+    tids[k++] = extern_ready_.front()->tid;
+    extern_ready_.pop_front();
+  }
+  *n = k;
+  return SFX_OK;
+}
+
+int Runtime::extern_done(uint64_t tid, int status, const char* msg) {
+  std::unique_lock<std::mutex> lk(mu_);
+  auto it = tasks_by_tid_.find(tid);
+  if (it == tasks_by_tid_.end() || it->second->op != SFX_OP_EXTERN || !it->second->detached) {
+    last_error = "extern_done: not an external task handed out by sfx_extern_poll";
+    return SFX_ERR_CONFIG;
+  }
+  Task* t = it->second;
+  if (status != 0) {
+    poison(SFX_ERR_ENGINE_FAILED, msg ? msg : "external task failed");
+    return SFX_OK;
+  }
+  Handle* h = t->acc[0].h;
+  if (mode_writes(t->acc[0].mode)) {  // the agent wrote the host buffer
+    h->host_valid = true;
+    h->host_ready.reset();
+    h->dirty_dev = -1;
+  }
+  release(t);
+  complete(t);
+  return SFX_OK;
 }
 
 void Runtime::poison(int code, const std::string& msg) {
@@ -1126,6 +1224,7 @@ void Runtime::poison(int code, const std::string& msg) {
     fail_code_ = code;
     fail_msg_ = msg;
   }
+  extern_cv_.notify_all();
   for (auto& d : devs_) {
     d->exec_cv.notify_all();
     d->comp_cv.notify_all();
@@ -1369,11 +1468,16 @@ void Runtime::exec_loop(int d) {
     const int64_t t_rel0 = now_ns();
     if (be_->is_sim()) {
       for (Task* t : group) {
+        if (t->op == SFX_OP_EXTERN) {
+          extern_handoff(t);  // released by extern_done
+          continue;
+        }
         complete(t);  // synchronous device: stage_out + task_end before release
         release(t);
       }
     } else {
-      for (Task* t : group) release(t);
+      for (Task* t : group)
+        if (t->op != SFX_OP_EXTERN) release(t);  // extern: released by extern_done
       for (Task* t : group) D.inflight.push_back(t);
       D.comp_cv.notify_one();
     }
@@ -1401,6 +1505,10 @@ void Runtime::comp_loop(int d) {
     const int64_t tc0 = now_ns();
     D.inflight.pop_front();
     if (rc) poison(SFX_ERR_CUDA, err);
+    if (t->op == SFX_OP_EXTERN && !rc) {
+      extern_handoff(t);  // its host copy is current: over to the agent
+      continue;
+    }
     complete(t);
     D.stats.t_complete_ns += now_ns() - tc0;
   }

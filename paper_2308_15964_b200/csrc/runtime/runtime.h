@@ -145,6 +145,7 @@ struct Task {
   int64_t t_push = 0, t_pop = 0, t_start = 0, t_end = 0;
   std::vector<Handle*> commute;  // commutative handles sorted by hid (graph.py:150-157)
   bool commute_shared = false;   // op accumulates with device atomics: guard in shared mode
+  bool detached = false;         // SFX_OP_EXTERN handed to the host agent: stream slots freed
 };
 
 struct Operand {
@@ -269,6 +270,8 @@ class Runtime {
   int wait_task(uint64_t tid, double timeout_s);
   int task_state(uint64_t tid, int32_t* st);
   int stats(int dev, sfx_dev_stats* out);
+  int extern_poll(uint64_t* tids, uint64_t cap, uint64_t* n, double timeout_s);
+  int extern_done(uint64_t tid, int status, const char* msg);
   int resident(int dev, uint64_t* hids, uint64_t cap, uint64_t* n);
   int block_state(uint64_t hid, int dev, int32_t* st, int32_t* host_valid);
   int trace(uint32_t gid, sfx_event* buf, uint64_t cap, uint64_t* n);
@@ -333,6 +336,9 @@ class Runtime {
   bool ktime_;  // trace_ || SFX_FLAG_KTIME: every launch group gets a timing start event
   std::mutex mu_;
   std::condition_variable done_cv_;
+  std::condition_variable extern_cv_;
+  std::deque<Task*> extern_ready_;  // SFX_OP_EXTERN tasks whose host buffers are current
+  void extern_handoff(Task* t);
   std::vector<std::unique_ptr<Device>> devs_;
   std::unordered_map<uint64_t, Handle*> handles_;
   std::vector<std::unique_ptr<Handle>> handle_store_;

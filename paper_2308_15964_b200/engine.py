@@ -142,6 +142,9 @@ class ComputeEngine:
     def stop(self) -> None:
         if not self._stopped:
             self._stopped = True
+            agent = getattr(self, "_comm_agent", None)
+            if agent is not None:
+                agent.stop()
             N.lib.sfx_destroy(self._h)
             self._h = None
 

@@ -184,6 +184,31 @@ class TaskGraph:
         self.trace = TraceView(self)
         self.trace.enabled = trace
         self.speculation_enabled = False
+        self.comm = None
+
+    # -- inter-process communication (graph.py:264-284, comms.py) -------------
+    def use_comm(self, comm) -> "TaskGraph":
+        """Bind to a communicator (comms.TorchComm) for send/recv/broadcast tasks."""
+        if self.comm is not None and self.comm is not comm:
+            raise ConfigurationError("graph is already bound to a communicator")
+        self.comm = comm
+        comm.graphs.append(self)
+        return self
+
+    def send(self, obj, dest: int, tag: int) -> "TaskViewer":
+        from .comms import comm_send
+
+        return comm_send(self, obj, dest, tag)
+
+    def recv(self, obj, src: int, tag: int) -> "TaskViewer":
+        from .comms import comm_recv
+
+        return comm_recv(self, obj, src, tag)
+
+    def broadcast(self, obj, root: int) -> "TaskViewer":
+        from .comms import comm_broadcast
+
+        return comm_broadcast(self, obj, root)
 
     # -- attachment (graph.py:57-64) -----------------------------------------
     def compute_on(self, engine) -> "TaskGraph":
@@ -386,6 +411,9 @@ class TaskGraph:
         N.lib.sfx_failure(self._h, ctypes.byref(code), msg, 1024)
         text = msg.value.decode(errors="replace")
         cause = N.error_for(code.value, text)
+        agent = getattr(self.engine, "_comm_agent", None)
+        if agent is not None and agent.error is not None:
+            cause = agent.error  # a communication task failed (e.g. CommProtocolError)
         err = EngineFailedError(f"a task failed: {text}")
         err.__cause__ = cause
         return err

@@ -11,6 +11,8 @@ import socket
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -55,3 +57,30 @@ def test_reference_arm_prints_once_under_torchrun():
     line = lines[0]
     assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "GFLOP/s"
     assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_comm_tasks_between_two_processes():
+    """send / recv / broadcast tasks (reference comms.py, tests/test_comms.py) between
+    two processes, each with its own native runtime: every tier, dependency
+    ordering through a device task, FIFO matching on one tag, broadcast, a size
+    mismatch poisoning with CommProtocolError, insertion validation."""
+    r = _torchrun([os.path.join("tests", "dist", "comm_ranks.py")])
+    assert r.returncode == 0, r.stderr[-3000:]
+    out = {x["rank"]: x for x in (json.loads(l) for l in r.stdout.splitlines() if l.startswith("{"))}
+    assert set(out) == {0, 1}
+    for rank in (0, 1):
+        assert out[rank]["tiers"] == [41, "ping", 66.0]
+        assert out[rank]["dep"] == 16
+        assert out[rank]["bcast"] == 777
+        assert out[rank]["validation"] == ["config", "config", "config", "serialization"]
+    assert out[1]["fifo"] == [1, 2, 3]
+    assert out[1]["mismatch"] == "CommProtocolError"
+
+
+@pytest.mark.gpu
+def test_comm_tasks_with_gpu_engines():
+    r = _torchrun([os.path.join("tests", "dist", "comm_gpu_ranks.py")])
+    assert r.returncode == 0, r.stderr[-3000:]
+    out = {x["rank"]: x for x in (json.loads(l) for l in r.stdout.splitlines() if l.startswith("{"))}
+    assert out[0]["d2h"] >= 256 * 256 * 8  # the dirty GPU tile was fetched home before the send
+    assert out[1]["recv_exact"] and out[1]["gemm_err"] <= 1e-15
