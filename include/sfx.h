@@ -167,6 +167,9 @@ typedef struct sfx_dev_stats {
    * (device time with at least one timed group running; folded in when
    * sfx_stats is called) */
   uint64_t timed_groups, timed_tasks, timed_ns, busy_ns;
+  /* earliest group start / latest group end (CLOCK_MONOTONIC ns) among the
+   * intervals folded in by this sfx_stats call (0 if none) */
+  int64_t first_start_ns, last_end_ns;
 } sfx_dev_stats;
 
 typedef struct sfx_event {

@@ -69,6 +69,21 @@ def trsm_inv(L, B):
     trsm(np.tril(L), B)
 
 
+def potrf_fullinv(A):
+    """potrf + inv(L)^T of the whole factor in the strict upper triangle
+    (csrc/kernels/factor_inv.cu)."""
+    potrf(A)
+    n = A.shape[0]
+    inv = scipy.linalg.solve_triangular(np.tril(A), np.eye(n), lower=True, check_finite=False)
+    iu = np.triu_indices(n, 1)
+    A[iu] = inv.T[iu]
+
+
+def trsm_fullinv(L, B):
+    """Same result as trsm (B L^-T); the operand's upper triangle is ignored."""
+    trsm(np.tril(L), B)
+
+
 def _one_side(Pt, Ps, Ft, eps2, self_pair, block=512):
     """F_t += interactions on targets Pt from sources Ps."""
     nt = Pt.shape[1]
@@ -113,6 +128,8 @@ BODIES = {
     "potrf": potrf,
     "potrf_inv": potrf_inv,
     "trsm_inv": trsm_inv,
+    "potrf_fullinv": potrf_fullinv,
+    "trsm_fullinv": trsm_fullinv,
     "p2p_pair": p2p_pair,
     "p2p_self": p2p_self,
     "noop": noop,
@@ -127,4 +144,6 @@ FLOPS = {
     "potrf": lambda b: b ** 3 / 3,
     "trsm_inv": lambda b: b ** 3,
     "potrf_inv": lambda b: b ** 3 / 3,
+    "trsm_fullinv": lambda b: b ** 3,
+    "potrf_fullinv": lambda b: b ** 3 / 3,
 }

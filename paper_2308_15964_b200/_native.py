@@ -92,7 +92,8 @@ class DevStats(ctypes.Structure):
         "bytes_p2p_in", "copies_p2p_in", "hits", "misses", "evictions", "writebacks",
         "blocks", "bytes_in_use", "capacity", "tasks_executed", "kernel_launches", "stream_waits",
         "t_plan_ns", "t_issue_ns", "t_release_ns", "t_complete_ns", "groups", "prefetches",
-        "timed_groups", "timed_tasks", "timed_ns", "busy_ns")]
+        "timed_groups", "timed_tasks", "timed_ns", "busy_ns")] + [
+        ("first_start_ns", ctypes.c_int64), ("last_end_ns", ctypes.c_int64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

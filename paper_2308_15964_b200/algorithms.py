@@ -224,14 +224,24 @@ def cholesky_priorities(nt: int, kind: str, k: int, i: int = 0, j: int = 0) -> i
     return p
 
 
+def fullinv_tile(b: int) -> bool:
+    """Tile sizes the full-inverse POTRF/TRSM pair supports (64 * 2^k, 128..4096)."""
+    nb = b // 64
+    return b % 64 == 0 and 128 <= b <= 4096 and nb & (nb - 1) == 0
+
+
 def insert_cholesky(graph, A: TiledMatrix, fast: bool = True, priorities="auto",
-                    inverse_blocks: bool = True):
+                    inverse_blocks="auto"):
     """In-place right-looking tiled Cholesky of the lower tiles of A (A = L L^T).
 
-    ``inverse_blocks`` (default): POTRF also leaves the inverses of its 64x64
+    ``inverse_blocks``: True = POTRF also leaves the inverses of its 64x64
     diagonal blocks in the diagonal tile's upper triangle and every TRSM runs as
-    DMMA GEMM sweeps on them.  The factor L (lower tiles) is the same; only the
-    otherwise unused upper triangle of the diagonal tiles differs.
+    DMMA GEMM sweeps on them; "full" = POTRF leaves inv(L)^T of the whole tile
+    there and every TRSM is one parallel DMMA GEMM (the panel chain's latency:
+    TRSM 1024 770 -> ~100 us); "auto" (default) = "full" where the tile size
+    allows it, else True; False = plain substitution kernels.  The factor L
+    (lower tiles) is the same; only the otherwise unused upper triangle of the
+    diagonal tiles differs.
 
     ``priorities``: True = column priorities (cholesky_priorities), "critical" =
     critical-path tasks only, False = all 0 (FIFO readiness order), "auto" = False
@@ -247,8 +257,13 @@ def insert_cholesky(graph, A: TiledMatrix, fast: bool = True, priorities="auto",
         # owner-computes updates (untested on hardware: single-GPU boxes only).
         eng = getattr(graph, "engine", None)
         priorities = bool(eng is not None and getattr(eng, "ndev", 1) > 1)
-    potrf_op = ops.potrf_inv if inverse_blocks else ops.potrf
-    trsm_op = ops.trsm_inv if inverse_blocks else ops.trsm
+    if inverse_blocks == "auto":
+        inverse_blocks = "full" if fullinv_tile(A.b) else True
+    if inverse_blocks == "full":
+        potrf_op, trsm_op = ops.potrf_fullinv, ops.trsm_fullinv
+    else:
+        potrf_op = ops.potrf_inv if inverse_blocks else ops.potrf
+        trsm_op = ops.trsm_inv if inverse_blocks else ops.trsm
     if priorities == "critical":
         P = lambda *a: cholesky_priorities_critical(nt, *a)  # noqa: E731
     elif priorities:

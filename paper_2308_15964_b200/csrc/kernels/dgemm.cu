@@ -110,6 +110,10 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
     }
     m0 = bm * BM;
     n0 = bn * BN;
+    if (TRI) {  // upper-triangular B: k-tiles below the diagonal are zero, skip them
+      kt1 = min(kt1, (n0 + BN + BK - 1) / BK);
+      if (kt1 < kt0) kt1 = kt0;
+    }
   };
 
   if (threadIdx.x == 0) {

@@ -55,6 +55,14 @@ bool coop_supported(int M, int n);
 // block's strict upper triangle (consumed by launch_dtrsm_inv_group)
 cudaError_t launch_dpotrf_coop(double* A, long long lda, int n, int* info, void* workspace, cudaStream_t s,
                                bool store_inverses = false);
+// full triangular inverse (factor_inv.cu): DPOTRF leaving inv(L)^T in the strict
+// upper triangle (n = 64 * 2^k, n >= 128), and DTRSM as one TRI-masked DGEMM
+bool fullinv_supported(int n);
+size_t fullinv_workspace_bytes(int n);
+cudaError_t launch_dpotrf_fullinv(double* A, long long lda, int n, int* info, void* workspace, size_t ws_bytes,
+                                  cudaStream_t s);
+cudaError_t launch_dtrsm_fullinv(const double* L, long long ldl, double* B, long long ldb, int M, int n, void* scratch,
+                                 size_t bytes, cudaStream_t s);
 cudaError_t launch_dtrsm_coop_group(const TrsmDesc* d, int ntasks, int M, int n, void* workspace, size_t ws_bytes,
                                     cudaStream_t s);
 

@@ -37,7 +37,31 @@ class CudaBackend : public Backend {
     int* info = nullptr;
     bool ready = false;
     std::vector<void*> scratch;  // per stream (cooperative streams only)
+    // per stream, allocated on first use (stream-ordered): TRSM with the full
+    // inverse computes X = B W^T out of place before copying it back
+    std::vector<void*> tscratch;
+    std::vector<size_t> tscratch_bytes;
   };
+
+  void* trsm_scratch(int d, int stream, size_t need) {
+    Dev& D = *devs_[d];
+    if (D.tscratch.size() < D.streams.size()) {
+      D.tscratch.resize(D.streams.size(), nullptr);
+      D.tscratch_bytes.resize(D.streams.size(), 0);
+    }
+    if (D.tscratch_bytes[stream] < need) {
+      if (D.tscratch[stream]) cudaFreeAsync(D.tscratch[stream], D.streams[stream]);
+      D.tscratch[stream] = nullptr;
+      D.tscratch_bytes[stream] = 0;
+      if (cudaMallocAsync(&D.tscratch[stream], need, D.streams[stream]) != cudaSuccess) {
+        cudaGetLastError();
+        D.tscratch[stream] = nullptr;
+        return nullptr;
+      }
+      D.tscratch_bytes[stream] = need;
+    }
+    return D.tscratch[stream];
+  }
   static constexpr size_t kScratchBytes = 64ull << 20;
 
  public:
@@ -276,7 +300,16 @@ class CudaBackend : public Backend {
                          static_cast<int>(o[1].rows), static_cast<int>(o[0].cols), op.fp[0], op.fp[1], true, true, s);
         break;
       case SFX_OP_DTRSM:
-        if (op.ip[0] && coop_supported(static_cast<int>(o[1].rows), static_cast<int>(o[1].cols))) {
+        if (op.ip[0] == 2) {
+          const size_t need = static_cast<size_t>(o[1].rows) * o[1].cols * 8;
+          void* sc = trsm_scratch(d, stream, need);
+          if (!sc) {
+            err = "trsm scratch allocation failed";
+            return SFX_ERR_CUDA;
+          }
+          e = launch_dtrsm_fullinv(f64(o[0]), o[0].ld, f64(o[1]), o[1].ld, static_cast<int>(o[1].rows),
+                                   static_cast<int>(o[1].cols), sc, need, s);
+        } else if (op.ip[0] && coop_supported(static_cast<int>(o[1].rows), static_cast<int>(o[1].cols))) {
           TrsmDesc td{f64(o[0]), o[0].ld, f64(o[1]), o[1].ld};
           e = launch_dtrsm_inv_group(&td, 1, static_cast<int>(o[1].rows), static_cast<int>(o[1].cols), s);
         } else if (devs_[d]->scratch[stream] &&
@@ -290,7 +323,10 @@ class CudaBackend : public Backend {
         }
         break;
       case SFX_OP_DPOTRF:
-        if (devs_[d]->scratch[stream] && coop_supported(static_cast<int>(o[0].rows), static_cast<int>(o[0].rows)))
+        if (op.ip[0] == 2 && devs_[d]->scratch[stream] && fullinv_supported(static_cast<int>(o[0].rows)))
+          e = launch_dpotrf_fullinv(f64(o[0]), o[0].ld, static_cast<int>(o[0].rows), devs_[d]->info,
+                                    devs_[d]->scratch[stream], kScratchBytes, s);
+        else if (devs_[d]->scratch[stream] && coop_supported(static_cast<int>(o[0].rows), static_cast<int>(o[0].rows)))
           e = launch_dpotrf_coop(f64(o[0]), o[0].ld, static_cast<int>(o[0].rows), devs_[d]->info,
                                  devs_[d]->scratch[stream], s, op.ip[0] != 0);
         else
@@ -403,6 +439,9 @@ class CudaBackend : public Backend {
       for (void* p : D.scratch)
         if (p) cudaFree(p);
       D.scratch.clear();
+      for (void* p : D.tscratch)
+        if (p) cudaFree(p);
+      D.tscratch.clear();
       D.arena = nullptr;
       D.ready = false;
     }

@@ -246,6 +246,14 @@ int Runtime::unreg(uint64_t hid) {
 
 // ------------------------------------------------------------- insertion
 
+// DPOTRF / DTRSM with the full triangular inverse (factor_inv.cu): exact doubling
+// over 64-blocks, and small enough for the cooperative factorization
+static bool fullinv_size(int64_t n) {
+  if (n < 128 || n > 4096 || n % 64) return false;
+  const int64_t nb = n / 64;
+  return (nb & (nb - 1)) == 0;
+}
+
 static int expect_f64(const Handle* h, const char* what, std::string& err) {
   if (h->dtype != SFX_DTYPE_F64 || h->rows <= 0 || h->cols <= 0 || h->ld < h->cols ||
       h->bytes < static_cast<uint64_t>((h->rows - 1) * h->ld + h->cols) * 8) {
@@ -369,12 +377,20 @@ int Runtime::validate(const sfx_task_desc& d, const sfx_access* acc, std::string
         err = "dtrsm: L must be square with B's column count";
         return SFX_ERR_CONFIG;
       }
+      if (d.iparam[0] == 2 && !fullinv_size(hs[0]->rows)) {
+        err = "dtrsm (full inverse): L must be 64 * 2^k with 128 <= n <= 4096";
+        return SFX_ERR_CONFIG;
+      }
       return 0;
     case SFX_OP_DPOTRF:
       if (!need(1) || !writes(0)) return SFX_ERR_CONFIG;
       if ((rc = expect_f64(hs[0], "A", err))) return rc;
       if (hs[0]->rows != hs[0]->cols) {
         err = "dpotrf: A must be square";
+        return SFX_ERR_CONFIG;
+      }
+      if (d.iparam[0] == 2 && !fullinv_size(hs[0]->rows)) {
+        err = "dpotrf (full inverse): A must be 64 * 2^k with 128 <= n <= 4096";
         return SFX_ERR_CONFIG;
       }
       return 0;
@@ -1024,6 +1040,7 @@ bool Runtime::groupable(const Task* t) const {
   // generators: grouping anything else would serialise independent tasks on one stream
   switch (t->op) {
     case SFX_OP_DTRSM:  // grouped cooperative TRSM, or grouped inverse-block GEMM sweeps
+      if (t->ip[0] == 2) return false;  // full inverse: one parallel DGEMM per task, own scratch
       return group_max_ > 1 && (is_coop(t) || (t->ip[0] && t->acc[0].h->rows % 64 == 0));
     case SFX_OP_DGEMM:
     case SFX_OP_DSYRK:
@@ -1584,10 +1601,14 @@ int Runtime::stats(int dev, sfx_dev_stats* out) {
     return SFX_ERR_CONFIG;
   }
   Device& D = *devs_[dev];
+  D.stats.first_start_ns = 0;
+  D.stats.last_end_ns = 0;
   if (!D.kintervals.empty()) {
     // union of the timed launch-group intervals (overlapping groups on
     // different streams count once)
     std::sort(D.kintervals.begin(), D.kintervals.end());
+    D.stats.first_start_ns = D.kintervals.front().first;
+    for (auto& iv : D.kintervals) D.stats.last_end_ns = std::max<int64_t>(D.stats.last_end_ns, iv.second);
     int64_t cs = D.kintervals[0].first, ce = D.kintervals[0].second;
     for (auto& iv : D.kintervals) {
       if (iv.first > ce) {

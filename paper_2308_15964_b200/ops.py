@@ -59,17 +59,25 @@ def dsyrk(alpha: float = -1.0, beta: float = 1.0) -> Op:
     return Op("dsyrk", N.OP_DSYRK, (alpha, beta))
 
 
-def dtrsm(inverse_blocks: bool = False) -> Op:
-    """B = B L^-T.  ``inverse_blocks``: L's tile comes from ``dpotrf(store_inverses=True)``
+def dtrsm(inverse_blocks=False) -> Op:
+    """B = B L^-T.  ``inverse_blocks=True``: L's tile comes from ``dpotrf(store_inverses=True)``
     and carries the inverses of its 64x64 diagonal blocks in its upper triangle, so the
-    solve runs as DMMA GEMM sweeps (x inverse block, then trailing update)."""
+    solve runs as DMMA GEMM sweeps (x inverse block, then trailing update).
+    ``inverse_blocks="full"``: L's tile comes from ``dpotrf(store_inverses="full")`` and
+    carries inv(L)^T in its strict upper triangle: the solve is ONE parallel DMMA GEMM."""
+    if inverse_blocks == "full":
+        return Op("dtrsm_fullinv", N.OP_DTRSM, iparam=(2,))
     return Op("dtrsm_inv" if inverse_blocks else "dtrsm", N.OP_DTRSM, iparam=(1 if inverse_blocks else 0,))
 
 
-def dpotrf(store_inverses: bool = False) -> Op:
+def dpotrf(store_inverses=False) -> Op:
     """Lower Cholesky in place.  Default: LAPACK 'L' semantics (upper triangle untouched).
-    ``store_inverses``: the strict upper triangle of each 64x64 diagonal block receives
-    inv(L_jj)^T (for ``dtrsm(inverse_blocks=True)``); the factor L is identical."""
+    ``store_inverses=True``: the strict upper triangle of each 64x64 diagonal block receives
+    inv(L_jj)^T (for ``dtrsm(inverse_blocks=True)``); ``"full"``: the whole strict upper
+    triangle receives inv(L)^T (n = 64 * 2^k, 128 <= n <= 4096; for
+    ``dtrsm(inverse_blocks="full")``).  The factor L is identical in every mode."""
+    if store_inverses == "full":
+        return Op("dpotrf_fullinv", N.OP_DPOTRF, iparam=(2,))
     return Op("dpotrf_inv" if store_inverses else "dpotrf", N.OP_DPOTRF, iparam=(1 if store_inverses else 0,))
 
 
@@ -131,3 +139,5 @@ trsm = dtrsm()
 potrf = dpotrf()
 trsm_inv = dtrsm(inverse_blocks=True)
 potrf_inv = dpotrf(store_inverses=True)
+trsm_fullinv = dtrsm(inverse_blocks="full")
+potrf_fullinv = dpotrf(store_inverses="full")

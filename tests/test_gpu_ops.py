@@ -238,3 +238,35 @@ def test_shared_commutative_members_on_gpu(gpu_engine):
     g.flush_all(keep_device=False)
     assert g.wait_all(timeout=60)
     assert [c.value for c in cells] == want
+
+
+@pytest.mark.parametrize("b", [128, 512, 1024])
+def test_dpotrf_full_inverse_and_one_gemm_trsm(gpu_engine, b):
+    """potrf_fullinv leaves inv(L)^T in the tile's strict upper triangle; trsm_fullinv
+    (one TRI-masked DGEMM + copy back) solves X L^T = B with it."""
+    A0 = inputs.spd_tile(61, 0, 0, b, b, b)
+    A = A0.copy()
+    B0 = inputs.uniform_tile(62, 0, 0, 300, b, b)
+    X = B0.copy()
+
+    def run(g):
+        g.task(sf.write(A), device=sf.ops.potrf_fullinv)
+        g.task(sf.read(A), sf.write(X), device=sf.ops.trsm_fullinv)
+    _run(gpu_engine, run)
+    want = A0.copy()
+    bodies.potrf_fullinv(want)
+    L = np.tril(A)
+    assert np.linalg.norm(A0 - L @ L.T) / np.linalg.norm(A0) <= 1e-12
+    iu = np.triu_indices(b, 1)
+    assert np.abs(A[iu] - want[iu]).max() <= 1e-12 * np.abs(want[iu]).max()
+    Xw = B0.copy()
+    bodies.trsm(np.tril(want), Xw)
+    assert np.linalg.norm(X - Xw) / np.linalg.norm(Xw) <= 1e-12
+    assert np.linalg.norm(X @ L.T - B0) / (np.linalg.norm(L) * np.linalg.norm(X)) <= 1e-13
+
+
+def test_full_inverse_rejects_unsupported_sizes(gpu_engine):
+    A = inputs.spd_tile(61, 0, 0, 320, 320, 320)
+    g = sf.TaskGraph().compute_on(gpu_engine)
+    with pytest.raises(sf.ConfigurationError):
+        g.task(sf.write(A), device=sf.ops.potrf_fullinv)

@@ -61,6 +61,13 @@ def main():
                 g.task(sf.write(A), device=sf.ops.potrf_inv)
             return run
         print(f"potrf_inv n={n}: {timed(eng, build):.1f} us")
+        if n >= 128:
+            def buildf(g, A=A, A0=A0):
+                A[...] = A0
+                g.task(sf.write(A), device=sf.ops.potrf_fullinv)
+                g.wait_all()
+                return lambda: g.task(sf.write(A), device=sf.ops.potrf_fullinv)
+            print(f"potrf_fullinv n={n}: {timed(eng, buildf):.1f} us")
     L0 = inputs.spd_tile(51, 0, 0, b, b, b)
     L = sf.pinned_empty((b, b))
     X = sf.pinned_empty((b, b))
@@ -69,10 +76,11 @@ def main():
     X[...] = inputs.uniform_tile(52, 0, 0, b, b, b)
     C[...] = inputs.uniform_tile(53, 0, 0, b, b, b)
     g0 = sf.TaskGraph().compute_on(eng)
-    g0.task(sf.write(L), device=sf.ops.potrf_inv)
+    g0.task(sf.write(L), device=sf.ops.potrf_fullinv)
     g0.wait_all()
     cases = {
         "trsm_inv": lambda g: g.task(sf.read(L), sf.write(X), device=sf.ops.trsm_inv),
+        "trsm_fullinv": lambda g: g.task(sf.read(L), sf.write(X), device=sf.ops.trsm_fullinv),
         "syrk_sub": lambda g: g.task(sf.read(X), sf.write(C), device=sf.ops.syrk_sub),
         "gemm_nt_sub": lambda g: g.task(sf.read(X), sf.read(L), sf.write(C), device=sf.ops.gemm_nt_sub),
     }
