@@ -154,7 +154,7 @@ def _emit(graph, fast):
 
 
 def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: bool = True,
-                priorities=False):
+                priorities=False, tile_block: int = 0):
     """C += A B over tiles, loop order i, j, k.
 
     ``priorities`` (False, True or a row-block height h): block row i gets priority
@@ -162,12 +162,26 @@ def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: boo
     scheduler the rows of C finish one after another (a few rows in flight)
     instead of every chain advancing in lock-step -- staging of A/C rows and the
     flush of finished C tiles then overlap the remaining compute.
+
+    ``tile_block`` = h > 0 (overrides ``priorities``): the C tiles are ranked in
+    h x h blocks (block-row-major), each block's tasks one priority level above the
+    next block's: a block needs only h rows of A and h columns of B, so when the
+    operands start on the host, staging spreads over the whole step.
     """
     nt = A.nt
+    if tile_block:
+        h = int(tile_block)
+        nbc = (nt + h - 1) // h
+        nblocks = nbc * nbc
+        rank = lambda i, j: nblocks - ((i // h) * nbc + j // h)  # noqa: E731
+    elif priorities:
+        rank = lambda i, j: (nt - i) // int(priorities)  # noqa: E731
+    else:
+        rank = lambda i, j: 0  # noqa: E731
     if not fast:
         for i in range(nt):
             for j in range(nt):
-                prio = (nt - i) // int(priorities) if priorities else 0
+                prio = rank(i, j)
                 for k in range(nt):
                     graph.task(read(A[i, k]), read(B[k, j]), write(C[i, j]), device=ops.gemm_nn,
                                priority=prio, name="gemm")
@@ -181,7 +195,8 @@ def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: boo
     jj, kk = jj.reshape(-1), kk.reshape(-1)
     for i in range(nt):
         hids = np.stack([HA[i, kk], HB[kk, jj], HC[i, jj]], axis=1)
-        batch.add_many(ops.gemm_nn, hids, modes, (nt - i) // int(priorities) if priorities else 0, "gemm")
+        prio = np.repeat(np.array([rank(i, j) for j in range(nt)], np.int32), nt)  # jj-major like hids
+        batch.add_many(ops.gemm_nn, hids, modes, prio, "gemm")
         batch.flush()
     return batch.submit()
 

@@ -18,13 +18,15 @@
 // full double) + 4 DMUL + 2 DADD + 6 DFMA = 23 FP64 ops per unordered pair,
 // 11.5 per ordered interaction (the one-directional formulation needs 21).
 //
-// Layout (warp-shuffle rotation).  A CTA owns a 512-target block of side a
-// and a 512-source block of side b; each of its 4 warps holds 128 targets in
-// registers (TPT = 4 per lane, with their accumulators).  The b block is
+// Layout (warp-shuffle rotation).  A CTA owns a BLK = 1024-target block of side
+// a and a 1024-source block of side b; each of its 4 warps holds 256 targets in
+// registers (TPT = 8 per lane, with their accumulators).  The b block is
 // walked in chunks of 64: every lane loads SPT = 2 sources (coalesced) and
 // zeroes their accumulators, then the warp does 32 rotation steps: evaluate
-// the lane's 4 x 2 pairs, pass the 2 sources and their accumulators to the
-// next lane (__shfl_sync).  After 32 steps every source has met all 128
+// the lane's 8 x 2 pairs, pass the 2 sources and their accumulators to the
+// next lane (__shfl_sync: 32 32-bit shuffles per step, so TPT = 8 keeps the
+// FP64 pipe -- 16 pairs x 23 instructions -- the bound, not the shuffle unit;
+// with TPT = 4 the shuffles were).  After 32 steps every source has met all 256
 // targets of the warp and is back on its home lane with its accumulated
 // contributions; the 4 warps' partials are summed in shared memory and added
 // to F_b with one FP64 atomic per component.  Targets flush their
@@ -45,9 +47,9 @@ namespace sfx {
 namespace {
 
 constexpr int THREADS = 128;           // 4 warps
-constexpr int TPT = 4;                 // targets per lane
+constexpr int TPT = 8;                 // targets per lane
 constexpr int SPT = 2;                 // sources per lane per chunk
-constexpr int BLK = 32 * TPT * (THREADS / 32);  // 512: targets per CTA = sources per CTA
+constexpr int BLK = 32 * TPT * (THREADS / 32);  // 1024: targets per CTA = sources per CTA
 constexpr int CHUNK = 32 * SPT;        // 64 sources per rotation round
 constexpr double FAR = 1e100;          // padding position (r2 ~ 1e200: finite, u ~ 1e-100)
 
