@@ -265,13 +265,21 @@ def insert_cholesky(graph, A: TiledMatrix, fast: bool = True, priorities="auto",
     """
     nt = A.nt
     if priorities == "auto":
-        # measured on one B200 (tools/chol_sweep.py): FIFO readiness order beats the
-        # column priorities (C3 30.8 vs 28.8 TFLOP/s, C5 33.4 vs 31.1): long runs of
-        # same-shape ready tasks make big grouped launches and the streams stay full.
-        # Across GPUs the column priorities keep the panel chain ahead of the
-        # owner-computes updates (untested on hardware: single-GPU boxes only).
+        # measured on one B200 (tools/chol_sweep.py): when the matrix fits in the tile
+        # cache, FIFO readiness order beats the column priorities (C3 30.8 vs 28.8,
+        # C5 33.4 vs 31.1 TFLOP/s): long runs of same-shape ready tasks make big
+        # grouped launches and the streams stay full.  When it does not fit, the
+        # column order keeps the LRU working set small (C3 with a 3 GiB arena for its
+        # 4.1 GiB of tiles: 25.9 vs 17.1 TFLOP/s, 4x fewer dirty write-backs).  Across
+        # GPUs the column priorities keep the panel chain ahead of the owner-computes
+        # updates (untested on hardware: single-GPU boxes only).
         eng = getattr(graph, "engine", None)
-        priorities = bool(eng is not None and getattr(eng, "ndev", 1) > 1)
+        ndev = getattr(eng, "ndev", 1) if eng is not None else 1
+        priorities = ndev > 1
+        if not priorities and eng is not None and getattr(eng, "backend", "cuda") == "cuda":
+            need = sum(t.nbytes for t in A.tiles.values())
+            cap = sum(eng.stats(d)["capacity"] for d in range(ndev))
+            priorities = need > 0.8 * cap
     if inverse_blocks == "auto":
         inverse_blocks = "full" if fullinv_tile(A.b) else True
     if inverse_blocks == "full":

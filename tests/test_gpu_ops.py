@@ -270,3 +270,29 @@ def test_full_inverse_rejects_unsupported_sizes(gpu_engine):
     g = sf.TaskGraph().compute_on(gpu_engine)
     with pytest.raises(sf.ConfigurationError):
         g.task(sf.write(A), device=sf.ops.potrf_fullinv)
+
+
+def test_cholesky_under_a_small_arena_evicts_and_matches_oracle():
+    """The LRU tile cache on real HBM: a working set 2.7x the arena forces
+    evictions with dirty write-backs and re-staging mid-factorization; the factor
+    still matches the oracle."""
+    n, b = 2048, 256
+    objs = programs.cholesky_operands(n, b)
+    want = {k: v.copy() for k, v in objs.items()}
+    programs.run_on_oracle(programs.cholesky_program(n // b), want, workers=4).stop()
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, 4), device_memory=(36 * b * b * 8) * 10 // 27)
+    try:
+        M = alg.TiledMatrix(n, b, lower=True)
+        for ij, t in M.tiles.items():
+            t[...] = objs[("A",) + ij]
+        g = sf.TaskGraph().compute_on(eng)
+        alg.insert_cholesky(g, M)
+        g.flush_all(keep_device=False)
+        assert g.wait_all(timeout=120)
+        st = eng.stats(0)
+        assert st["evictions"] > 0 and st["writebacks"] > 0
+        L = M.to_dense(lower_only=True)
+        Lw = programs.assemble_lower(want, n, b)
+        assert np.abs(L - Lw).max() / np.abs(Lw).max() <= 1e-12
+    finally:
+        eng.stop()

@@ -21,8 +21,10 @@ import paper_2308_15964_b200 as sf  # noqa: E402
 from paper_2308_15964_b200 import algorithms as alg  # noqa: E402
 
 
-def run(n, b, reps, streams, group, gps, prio, urgent):
-    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, streams), scheduler="prio", trace=False, group_max=group)
+def run(n, b, reps, streams, group, gps, prio, urgent, arena_gib=0.0):
+    mem = int(arena_gib * 2 ** 30) if arena_gib else None
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, streams), scheduler="prio", trace=False, group_max=group,
+                           device_memory=mem)
     eng.set_option("groups_per_stream", gps)
     if urgent is not None:
         eng.set_option("urgent_priority", urgent)
@@ -35,12 +37,17 @@ def run(n, b, reps, streams, group, gps, prio, urgent):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        alg.insert_cholesky(g, M, priorities={0: False, 1: True, 2: "critical"}[prio])
+        alg.insert_cholesky(g, M, priorities={0: False, 1: True, 2: "critical", 3: "auto"}[prio])
         g.wait_all()
         e1.record()
         torch.cuda.synchronize()
         if rep:
             ts.append(e0.elapsed_time(e1) / 1e3)
+    st = eng.stats(0)
+    if arena_gib:
+        print(f"  arena {arena_gib} GiB: evictions {st['evictions']}, write-backs {st['writebacks']}, "
+              f"H2D {st['bytes_to_device'] / 2 ** 30:.1f} GiB, D2H {st['bytes_from_device'] / 2 ** 30:.1f} GiB "
+              f"over {reps + 1} factorizations (+ fills)")
     eng.stop()
     t = statistics.mean(ts)
     return t, alg.flops_cholesky(n) / t / 1e12
@@ -54,14 +61,16 @@ def main():
     ap.add_argument("--streams", default="16")
     ap.add_argument("--group", default="32")
     ap.add_argument("--gps", default="2")
-    ap.add_argument("--prio", default="1", help="0 none, 1 column priorities, 2 critical-path only")
+    ap.add_argument("--prio", default="1", help="0 none, 1 column priorities, 2 critical-path only, 3 auto")
     ap.add_argument("--urgent", default="default")
+    ap.add_argument("--arena-gib", type=float, default=0.0, help="cap the device arena (LRU tile cache) size")
     a = ap.parse_args()
     ints = lambda s: [int(x) for x in s.split(",")]  # noqa: E731
     urg = [None if u == "default" else int(u) for u in a.urgent.split(",")]
     for st, gr, gps, pr, ur in itertools.product(ints(a.streams), ints(a.group), ints(a.gps), ints(a.prio), urg):
-        t, tf = run(a.n, a.b, a.reps, st, gr, gps, pr, ur)
-        print(f"streams={st} group={gr} groups_per_stream={gps} prio={pr} urgent={ur} tiles_per_cta="
+        t, tf = run(a.n, a.b, a.reps, st, gr, gps, pr, ur, a.arena_gib)
+        print(f"streams={st} group={gr} groups_per_stream={gps} prio={pr} urgent={ur} arena={a.arena_gib or 'all'} "
+              f"tiles_per_cta="
               f"{os.environ.get('SFX_GEMM_TILES_PER_CTA', 'auto')}: {t * 1e3:.1f} ms {tf:.2f} TFLOP/s", flush=True)
 
 
