@@ -9,7 +9,7 @@ import pytest
 
 import paper_2308_15964_b200 as sf
 from paper_2308_15964_b200 import algorithms as alg
-from oracle import programs
+from oracle import inputs, programs
 
 pytestmark = pytest.mark.gpu
 
@@ -95,5 +95,75 @@ def test_particles_with_per_device_partials(ndev):
             w = want[("F", g)]
             assert (np.abs(F[g][3] - w[3]) / np.abs(w[3])).max() <= 1e-10
             assert np.abs(F[g][:3] - w[:3]).max() <= 1e-11 * np.abs(w[:3]).max()
+    finally:
+        eng.stop()
+
+
+def test_real_cholesky_trace_is_bit_exact_with_the_reference():
+    """The dependency trace of the REAL GPU Cholesky (tile kernels on the B200, 32x32
+    tiles of 64) equals the reference's: the 16,368 dot edges and, in the
+    deterministic mode (1 GPU, 1 stream, FIFO, no grouping, gated insertion), the
+    one-worker pop order frozen from the reference engine (tests/golden)."""
+    import os
+
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "tile_graphs.npz"))
+    nt, b = 32, 64
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, 1), scheduler=None, device_memory=1 << 30, group_max=1)
+    try:
+        M = alg.TiledMatrix(nt * b, b, lower=True)
+        g = sf.TaskGraph().compute_on(eng)
+        alg.insert_fill_spd(g, M, 3)  # same graph: the filled tiles stay resident (device-dirty)
+        assert g.wait_all(timeout=60)
+        with g.gated():
+            tids = alg.insert_cholesky(g, M, priorities=False).tolist()
+        g.flush_all(keep_device=False)
+        assert g.wait_all(timeout=120)
+        index = {t: i for i, t in enumerate(tids)}
+        edges = sorted({(index[s], index[d]) for s, d, _ in g.edges() if s in index and d in index})
+        assert len(edges) == 16368
+        assert edges == sorted(map(tuple, gold["cholesky_nt32_edges"].tolist()))
+        pops = [index[e[3]] for e in g.trace.export_events() if e[0] == "Pop" and e[3] in index]
+        assert pops == gold["cholesky_nt32_pop"].tolist()
+        # and the factor is right
+        A0 = np.zeros((nt * b, nt * b))
+        for (i, j), _ in M.tiles.items():
+            A0[i * b:(i + 1) * b, j * b:(j + 1) * b] = inputs.spd_tile(3, i * b, j * b, b, b, nt * b)
+        A0 = np.tril(A0) + np.tril(A0, -1).T
+        L = M.to_dense(lower_only=True)
+        assert np.linalg.norm(A0 - L @ L.T) / np.linalg.norm(A0) <= 1e-12
+    finally:
+        eng.stop()
+
+
+def test_real_gemm_trace_is_bit_exact_with_the_reference():
+    """Same for the tiled DGEMM (C1 shape: 8x8 tiles, here of 64): 448 edges and the
+    reference's one-worker FIFO pop order, with the real DMMA tile kernels."""
+    import os
+
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "tile_graphs.npz"))
+    nt, b = 8, 64
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, 1), scheduler=None, device_memory=1 << 30, group_max=1)
+    try:
+        A, B, C = (alg.TiledMatrix(nt * b, b) for _ in range(3))
+        g = sf.TaskGraph().compute_on(eng)
+        alg.insert_fill_uniform(g, A, 1)
+        alg.insert_fill_uniform(g, B, 2)
+        alg.insert_zero(g, C)
+        assert g.wait_all(timeout=60)
+        with g.gated():
+            tids = alg.insert_gemm(g, A, B, C).tolist()
+        g.flush_all(keep_device=False)
+        assert g.wait_all(timeout=60)
+        index = {t: i for i, t in enumerate(tids)}
+        edges = sorted({(index[s], index[d]) for s, d, _ in g.edges() if s in index and d in index})
+        assert edges == sorted(map(tuple, gold["gemm_nt8_edges"].tolist()))
+        pops = [index[e[3]] for e in g.trace.export_events() if e[0] == "Pop" and e[3] in index]
+        assert pops == gold["gemm_nt8_pop"].tolist()
+        Ad = np.vstack([np.hstack([inputs.uniform_tile(1, i * b, j * b, b, b, nt * b) for j in range(nt)])
+                        for i in range(nt)])
+        Bd = np.vstack([np.hstack([inputs.uniform_tile(2, i * b, j * b, b, b, nt * b) for j in range(nt)])
+                        for i in range(nt)])
+        want = Ad @ Bd
+        assert (np.abs(C.to_dense() - want) / np.abs(want)).max() <= 1e-10
     finally:
         eng.stop()
