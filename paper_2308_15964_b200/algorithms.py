@@ -240,9 +240,9 @@ def cholesky_priorities(nt: int, kind: str, k: int, i: int = 0, j: int = 0) -> i
 
 
 def fullinv_tile(b: int) -> bool:
-    """Tile sizes the full-inverse POTRF/TRSM pair supports (64 * 2^k, 128..4096)."""
+    """Tile sizes the full-inverse POTRF/TRSM pair supports (64 * 2^k, 128..2048)."""
     nb = b // 64
-    return b % 64 == 0 and 128 <= b <= 4096 and nb & (nb - 1) == 0
+    return b % 64 == 0 and 128 <= b <= 2048 and nb & (nb - 1) == 0
 
 
 def insert_cholesky(graph, A: TiledMatrix, fast: bool = True, priorities="auto",

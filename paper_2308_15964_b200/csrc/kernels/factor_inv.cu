@@ -61,13 +61,16 @@ __global__ void store_upper_transposed_kernel(double* A, long long lda, const do
 }  // namespace
 
 bool fullinv_supported(int n) {
-  if (n < 128 || n % 64) return false;
+  if (n < 128 || n > 2048 || n % 64) return false;
   const int nb = n / 64;
   return (nb & (nb - 1)) == 0;  // power-of-two number of 64-blocks: exact doubling
 }
 
+// [coop POTRF workspace (barrier + block inverses)] [W: n x n] [T: n x n / 4]
+static size_t w_offset(int n) { return (coop_workspace_bytes(n) + (1ull << 20) - 1) >> 20 << 20; }
+
 size_t fullinv_workspace_bytes(int n) {
-  return (1ull << 20) + static_cast<size_t>(n) * n * 8 + static_cast<size_t>(n) * n / 4 * 8;
+  return w_offset(n) + static_cast<size_t>(n) * n * 8 + static_cast<size_t>(n) * n / 4 * 8;
 }
 
 cudaError_t launch_dpotrf_fullinv(double* A, long long lda, int n, int* info, void* workspace, size_t ws_bytes,
@@ -75,7 +78,7 @@ cudaError_t launch_dpotrf_fullinv(double* A, long long lda, int n, int* info, vo
   if (!fullinv_supported(n) || ws_bytes < fullinv_workspace_bytes(n)) return cudaErrorInvalidValue;
   cudaError_t e = launch_dpotrf_coop(A, lda, n, info, workspace, s, true);
   if (e != cudaSuccess) return e;
-  double* W = reinterpret_cast<double*>(static_cast<char*>(workspace) + (1ull << 20));
+  double* W = reinterpret_cast<double*>(static_cast<char*>(workspace) + w_offset(n));
   double* T = W + static_cast<size_t>(n) * n;
   e = cudaMemsetAsync(W, 0, static_cast<size_t>(n) * n * 8, s);
   if (e != cudaSuccess) return e;
@@ -83,7 +86,7 @@ cudaError_t launch_dpotrf_fullinv(double* A, long long lda, int n, int* info, vo
   count_launch();
   expand_diag_inv_kernel<<<(nelem + 255) / 256, 256, 0, s>>>(A, lda, W, n);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  GemmDesc d1[64], d2[64];
+  GemmDesc d1[32], d2[32];
   for (int sz = 64; 2 * sz <= n; sz *= 2) {
     const int pairs = n / (2 * sz);
     e = cudaMemsetAsync(T, 0, static_cast<size_t>(pairs) * sz * sz * 8, s);
@@ -96,7 +99,9 @@ cudaError_t launch_dpotrf_fullinv(double* A, long long lda, int n, int* info, vo
       // W21 = -W22 T  (W22 at (o+sz, o+sz); W21 at (o+sz, o), zero before)
       d2[p] = GemmDesc{W + (o + sz) * n + (o + sz), n, Tp, sz, W + (o + sz) * n + o, n};
     }
-    // ldc differs between T (sz) and W (n): separate launches per level
+    // ldc differs between T (sz) and W (n): separate launches per level.  A single
+    // cooperative launch of the levels with 64^3 DFMA block products was slower
+    // (1182 vs 1097 us for b = 1024): the DMMA kernel with split-K wins.
     if ((e = launch_dgemm_group(d1, pairs, sz, sz, sz, 1.0, 1.0, false, false, s)) != cudaSuccess) return e;
     if ((e = launch_dgemm_group(d2, pairs, sz, sz, sz, -1.0, 1.0, false, false, s)) != cudaSuccess) return e;
   }

@@ -62,7 +62,7 @@ class CudaBackend : public Backend {
     }
     return D.tscratch[stream];
   }
-  static constexpr size_t kScratchBytes = 64ull << 20;
+  static constexpr size_t kScratchBytes = 64ull << 20;  // >= fullinv_workspace_bytes(2048) = 42 MiB
 
  public:
   CudaBackend(int ndev, const int* ordinals) : devs_(ndev) {

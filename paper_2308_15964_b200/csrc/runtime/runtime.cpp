@@ -249,7 +249,7 @@ int Runtime::unreg(uint64_t hid) {
 // DPOTRF / DTRSM with the full triangular inverse (factor_inv.cu): exact doubling
 // over 64-blocks, and small enough for the cooperative factorization
 static bool fullinv_size(int64_t n) {
-  if (n < 128 || n > 4096 || n % 64) return false;
+  if (n < 128 || n > 2048 || n % 64) return false;
   const int64_t nb = n / 64;
   return (nb & (nb - 1)) == 0;
 }
@@ -378,7 +378,7 @@ int Runtime::validate(const sfx_task_desc& d, const sfx_access* acc, std::string
         return SFX_ERR_CONFIG;
       }
       if (d.iparam[0] == 2 && !fullinv_size(hs[0]->rows)) {
-        err = "dtrsm (full inverse): L must be 64 * 2^k with 128 <= n <= 4096";
+        err = "dtrsm (full inverse): L must be 64 * 2^k with 128 <= n <= 2048";
         return SFX_ERR_CONFIG;
       }
       return 0;
@@ -390,7 +390,7 @@ int Runtime::validate(const sfx_task_desc& d, const sfx_access* acc, std::string
         return SFX_ERR_CONFIG;
       }
       if (d.iparam[0] == 2 && !fullinv_size(hs[0]->rows)) {
-        err = "dpotrf (full inverse): A must be 64 * 2^k with 128 <= n <= 4096";
+        err = "dpotrf (full inverse): A must be 64 * 2^k with 128 <= n <= 2048";
         return SFX_ERR_CONFIG;
       }
       return 0;

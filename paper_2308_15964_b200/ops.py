@@ -74,7 +74,7 @@ def dpotrf(store_inverses=False) -> Op:
     """Lower Cholesky in place.  Default: LAPACK 'L' semantics (upper triangle untouched).
     ``store_inverses=True``: the strict upper triangle of each 64x64 diagonal block receives
     inv(L_jj)^T (for ``dtrsm(inverse_blocks=True)``); ``"full"``: the whole strict upper
-    triangle receives inv(L)^T (n = 64 * 2^k, 128 <= n <= 4096; for
+    triangle receives inv(L)^T (n = 64 * 2^k, 128 <= n <= 2048; for
     ``dtrsm(inverse_blocks="full")``).  The factor L is identical in every mode."""
     if store_inverses == "full":
         return Op("dpotrf_fullinv", N.OP_DPOTRF, iparam=(2,))
