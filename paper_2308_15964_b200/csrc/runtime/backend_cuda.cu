@@ -195,6 +195,14 @@ class CudaBackend : public Backend {
   int event_sync(int, void* ev, std::string& err) override {
     return cuda_err(cudaEventSynchronize(ev_of(ev)), "kernel execution", err);
   }
+  bool event_done(int, void* ev) override {
+    const cudaError_t e = cudaEventQuery(ev_of(ev));
+    if (e == cudaErrorNotReady) {
+      cudaGetLastError();
+      return false;
+    }
+    return true;
+  }
   int64_t event_time_ns(int d, void* ev) override {
     float ms = 0;
     if (cudaEventElapsedTime(&ms, devs_[d]->base, ev_of(ev)) != cudaSuccess) {

@@ -52,6 +52,7 @@ class SimBackend : public Backend {
   }
   int stream_wait(int, int, void*, std::string&) override { return SFX_OK; }
   int event_sync(int, void*, std::string&) override { return SFX_OK; }
+  bool event_done(int, void*) override { return true; }
   int64_t event_time_ns(int, void* ev) override { return static_cast<SimEvent*>(ev)->t; }
   int copy_h2d(int d, int, uint64_t dst, const void* src, uint64_t n, std::string&) override {
     memcpy(arenas_[d] + dst, src, n);

@@ -145,6 +145,7 @@ Runtime::~Runtime() {
     }
     h->blocks.clear();
   }
+  for (auto& d : devs_) d->pending_wb.clear();
   be_->shutdown();
   delete be_;
 }
@@ -584,8 +585,9 @@ void Runtime::record(Graph* g, int kind, int64_t t, int wid, uint64_t tid, int64
 }
 
 void Runtime::push_ready(Task* t, int wid) {
-  // engine.py:212-223: record Push before the task becomes poppable
-  const int d = place(t);
+  // engine.py:212-223: record Push before the task becomes poppable.  A member
+  // handed its commutative guards by a release keeps the device it holds them on.
+  const int d = (t->guards_held && t->dev >= 0) ? t->dev : place(t);
   t->dev = d;
   t->seq = push_seq_++;
   t->t_push = now_ns();
@@ -678,6 +680,11 @@ SyncP Runtime::new_sync(int d, int s, bool timing) {
   return p;
 }
 
+static bool debug_staging() {
+  static const bool on = getenv("SFX_DEBUG_STAGING") != nullptr;
+  return on;
+}
+
 void Runtime::drop_block(Block* b, bool write_back, std::vector<Action>* acts, int s) {
   // device.py:226-232 (+ the write-back leg of evict_victims)
   Handle* h = b->h;
@@ -693,6 +700,12 @@ void Runtime::drop_block(Block* b, bool write_back, std::vector<Action>* acts, i
     acts->push_back(Action{Action::RECORD, hs});
     h->host_ready = hs;
     h->host_valid = true;
+    // the space is reusable below, but the copy above has not read it yet: whoever
+    // gets these bytes next waits for the write-back (stream-ordered only on s)
+    D.pending_wb.push_back(Device::PendingWriteBack{b->off, b->size, hs});
+    if (debug_staging())
+      fprintf(stderr, "[sfx] writeback hid=%llu off=%llu stream=%d wait_ready=%d\n", (unsigned long long)h->hid,
+              (unsigned long long)b->off, s, (b->ready && !b->ready->complete) ? 1 : 0);
     D.stats.bytes_from_device += h->bytes;
     D.stats.copies_from_device += 1;
     D.stats.writebacks += 1;
@@ -716,6 +729,22 @@ void Runtime::drop_block(Block* b, bool write_back, std::vector<Action>* acts, i
   }
 }
 
+void Runtime::wait_pending_wb(int d, int s, uint64_t off, uint64_t size, std::vector<Action>& acts) {
+  Device& D = *devs_[d];
+  size_t keep = 0;
+  for (size_t k = 0; k < D.pending_wb.size(); ++k) {
+    auto& p = D.pending_wb[k];
+    const bool recorded = p.done->recorded.load(std::memory_order_acquire);
+    if (recorded && be_->event_done(d, p.done->event)) continue;  // drop finished write-backs
+    // a write-back planned on this same stream (possibly in this very plan, not yet
+    // recorded) is ordered before our copies by the stream itself
+    const bool same_stream = p.done->dev == d && p.done->stream == s;
+    if (!same_stream && p.off < off + size && off < p.off + p.size) acts.push_back(Action{Action::WAIT, p.done});
+    D.pending_wb[keep++] = p;
+  }
+  D.pending_wb.resize(keep);
+}
+
 int Runtime::evict_one(int d, int s, std::vector<Action>& acts, std::string& err) {
   // device.py:208-224: victim = least (stamp, hid) among unpinned blocks
   Device& D = *devs_[d];
@@ -727,6 +756,9 @@ int Runtime::evict_one(int d, int s, std::vector<Action>& acts, std::string& err
   }
   if (!victim) return 1;
   D.stats.evictions += 1;
+  if (debug_staging())
+    fprintf(stderr, "[sfx] evict hid=%llu off=%llu dirty=%d stream=%d\n", (unsigned long long)victim->h->hid,
+            (unsigned long long)victim->off, victim->dirty ? 1 : 0, s);
   drop_block(victim, true, &acts, s);
   return 0;
 }
@@ -767,6 +799,7 @@ int Runtime::ensure_block(int d, int s, Handle* h, std::vector<Action>& acts, st
         return SFX_ERR_STAGING;
       }
     }
+    wait_pending_wb(d, s, off, size, acts);
     b = new Block();
     b->h = h;
     b->dev = d;
@@ -932,6 +965,10 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
           return SFX_ERR_INTERNAL;
         }
         wait_on(h->host_ready);
+        if (debug_staging())
+          fprintf(stderr, "[sfx] stage hid=%llu off=%llu stream=%d task=%llu host_ready=%s\n",
+                  (unsigned long long)h->hid, (unsigned long long)b->off, s, (unsigned long long)t->tid,
+                  !h->host_ready ? "none" : (h->host_ready->complete ? "complete" : (h->host_ready->stream == s ? "same-stream" : "waited")));
         Action cp{Action::H2D, nullptr};
         cp.host = h->host;
         cp.dst_off = b->off;
@@ -965,6 +1002,13 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
     if (m == SFX_WRITE || m == SFX_MAYBE_WRITE) b->ready = t->end;
   }
 
+  if (debug_staging()) {
+    fprintf(stderr, "[sfx] plan task=%llu op=%u stream=%d", (unsigned long long)t->tid, t->op, s);
+    for (size_t k = 0; k < t->acc.size(); ++k)
+      fprintf(stderr, " [hid=%llu off=%llu m=%u]", (unsigned long long)t->acc[k].h->hid,
+              (unsigned long long)blocks[k]->off, t->acc[k].mode);
+    fprintf(stderr, " waits=%zu\n", t->waits.size());
+  }
   op.op = t->op;
   op.n = static_cast<int>(std::min<size_t>(t->acc.size(), 8));
   for (int k = 0; k < op.n; ++k) {
@@ -989,8 +1033,8 @@ int Runtime::issue(int d, int s, const std::vector<Task*>& group, std::vector<Ac
   for (Action& a : acts) {
     switch (a.kind) {
       case Action::WAIT: {
+        if (a.sync->dev == d && a.sync->stream == s) break;  // stream order suffices
         while (!a.sync->recorded.load(std::memory_order_acquire)) std::this_thread::yield();
-        if (a.sync->dev == d && a.sync->stream == s) break;
         rc = be_->stream_wait(d, s, a.sync->event, err);
         devs_[d]->stats.stream_waits += 1;
         break;
@@ -1077,6 +1121,7 @@ bool Runtime::acquire_commute(Task* t) {
   // atomics, so any interleaving is one of the orders commutativity allows):
   // members of a group run concurrently as long as they are on the same device
   // and no exclusive member holds the handle.
+  if (t->guards_held) return true;  // acquired when a release handed the handle over
   for (Handle* h : t->commute) {
     const bool busy = t->commute_shared
                           ? (h->commute_owner != nullptr || (h->shared_users > 0 && h->shared_dev != t->dev))
@@ -1094,10 +1139,13 @@ bool Runtime::acquire_commute(Task* t) {
       h->commute_owner = t;
     }
   }
+  t->guards_held = true;
   return true;
 }
 
 void Runtime::release_commute(Task* t) {
+  if (!t->guards_held) return;
+  t->guards_held = false;
   for (Handle* h : t->commute) {
     if (t->commute_shared) {
       if (--h->shared_users > 0) continue;
@@ -1106,11 +1154,23 @@ void Runtime::release_commute(Task* t) {
       if (h->commute_owner != t) continue;
       h->commute_owner = nullptr;
     }
-    // wake the parked members in FIFO order; each re-enters its device queue
-    while (!h->commute_waiters.empty()) {
+    // hand the freed handle to the parked members in FIFO order: each is tried
+    // right here (all-or-nothing over all its handles) and only a winner re-enters
+    // its device queue; a member that still finds another handle busy re-parks on
+    // that one.  Every waiter is touched O(1) times per handle it waits on -- not
+    // re-offered on every release (the reference's quadratic re-offer,
+    // handles.py:317-328).  Exclusive: the first winner owns h, the rest stay
+    // parked.  Shared: winners on h's new device keep coming until one parks on h.
+    size_t budget = h->commute_waiters.size();
+    while (budget-- > 0 && !h->commute_waiters.empty()) {
       Task* w = h->commute_waiters.front();
       h->commute_waiters.pop_front();
-      push_ready(w, -1);
+      if (acquire_commute(w)) {
+        push_ready(w, -1);
+        if (!w->commute_shared) break;
+        continue;
+      }
+      if (!h->commute_waiters.empty() && h->commute_waiters.back() == w) break;  // h itself is taken again
     }
   }
 }
@@ -1262,6 +1322,7 @@ int Runtime::plan_prefetch(int d, std::vector<Action>& acts) {
       if (D.free_bytes < size + D.capacity / 8) return;
       uint64_t off;
       if (!alloc_space(d, size, &off)) return;
+      wait_pending_wb(d, s, off, size, acts);
       Block* b = new Block();
       b->h = h;
       b->dev = d;
@@ -1280,6 +1341,9 @@ int Runtime::plan_prefetch(int d, std::vector<Action>& acts) {
       cp.dst_off = off;
       cp.n = h->bytes;
       acts.push_back(cp);
+      if (debug_staging())
+        fprintf(stderr, "[sfx] prefetch hid=%llu off=%llu stream=%d\n", (unsigned long long)h->hid,
+                (unsigned long long)off, s);
       SyncP cs = new_sync(d, s, false);
       acts.push_back(Action{Action::RECORD, cs});
       b->ready = cs;
@@ -1362,7 +1426,20 @@ void Runtime::exec_loop(int d) {
     Task* first = D.queue.pop();
     if (!first->commute.empty() && !acquire_commute(first)) continue;  // parked until the guard frees
     group.push_back(first);
-    if (groupable(first)) {
+    // A group only grows while the operands its members still have to stage fit in
+    // the free arena space: grouped launches that ran out of space mid-group (and
+    // evicted between members) were seen to produce wrong panel tiles (2048/256
+    // Cholesky in a 7 MB arena, >= 2 streams, groups >= 3; never with groups <= 2
+    // in 110 runs) -- root cause not found yet, see DESIGN.md "Known issues".
+    // With the working set resident (the benchmark configurations) nothing changes.
+    auto staging_bytes = [&](const Task* t) {
+      uint64_t n = 0;
+      for (const Access& a : t->acc)
+        if (!a.h->blocks[d]) n += std::max<uint64_t>((a.h->bytes + align_ - 1) / align_ * align_, align_);
+      return n;
+    };
+    uint64_t group_stage = staging_bytes(first);
+    if (groupable(first) && group_stage <= D.free_bytes) {
       const bool urgent = first->prio >= urgent_priority_;
       while (group.size() < group_max_ && D.queue.size() > 0 &&
              D.ninflight + static_cast<int>(group.size()) < static_cast<int>(window_)) {
@@ -1370,6 +1447,9 @@ void Runtime::exec_loop(int d) {
         if (!same_signature(first, nx) || commute_conflict(group, nx) || (nx->prio >= urgent_priority_) != urgent)
           break;
         if (first->op == SFX_OP_DTRSM && nx->prio != first->prio) break;  // a critical TRSM launches alone
+        const uint64_t more = staging_bytes(nx);
+        if (group_stage + more > D.free_bytes) break;  // would evict mid-group
+        group_stage += more;
         D.queue.pop();
         if (!nx->commute.empty() && !acquire_commute(nx)) continue;
         group.push_back(nx);
@@ -1403,17 +1483,23 @@ void Runtime::exec_loop(int d) {
       if (planned > 0) {
         // resources exhausted mid-group: launch what is planned, requeue the rest
         (void)mark;
+        if (debug_staging())
+          fprintf(stderr, "[sfx] midgroup requeue planned=%zu of %zu first=%llu\n", planned, group.size(),
+                  (unsigned long long)group[0]->tid);
         for (size_t k = group.size(); k-- > planned;) {
           Task* t = group[k];
           t->end.reset();
           t->start.reset();
           t->state = SFX_STATE_READY;
-          if (t->commute_shared) {
-            for (Handle* h : t->commute)
-              if (--h->shared_users == 0) h->shared_dev = -1;
-          } else {
-            for (Handle* h : t->commute)
-              if (h->commute_owner == t) h->commute_owner = nullptr;
+          if (t->guards_held) {
+            if (t->commute_shared) {
+              for (Handle* h : t->commute)
+                if (--h->shared_users == 0) h->shared_dev = -1;
+            } else {
+              for (Handle* h : t->commute)
+                if (h->commute_owner == t) h->commute_owner = nullptr;
+            }
+            t->guards_held = false;
           }
           D.queue.push_front(t);
         }
@@ -1424,6 +1510,9 @@ void Runtime::exec_loop(int d) {
       }
       // nothing planned yet: issue the write-backs planned so far, then wait for
       // any completion and re-plan
+      if (debug_staging())
+        fprintf(stderr, "[sfx] nothing-planned wait group=%zu first=%llu acts=%zu\n", group.size(),
+                (unsigned long long)group[0]->tid, acts.size());
       if (!acts.empty()) {
         lk.unlock();
         std::string e2;

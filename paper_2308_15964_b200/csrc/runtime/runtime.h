@@ -145,6 +145,7 @@ struct Task {
   int64_t t_push = 0, t_pop = 0, t_start = 0, t_end = 0;
   std::vector<Handle*> commute;  // commutative handles sorted by hid (graph.py:150-157)
   bool commute_shared = false;   // op accumulates with device atomics: guard in shared mode
+  bool guards_held = false;      // its commutative guards are acquired (idempotent acquire)
   bool detached = false;         // SFX_OP_EXTERN handed to the host agent: stream slots freed
 };
 
@@ -189,6 +190,8 @@ class Backend {
   virtual int event_record(int d, int stream, void* ev, std::string& err) = 0;
   virtual int stream_wait(int d, int stream, void* ev, std::string& err) = 0;
   virtual int event_sync(int d, void* ev, std::string& err) = 0;
+  // true once the recorded work before ev has executed (sim: always)
+  virtual bool event_done(int d, void* ev) = 0;
   // CLOCK_MONOTONIC ns of a completed timing event
   virtual int64_t event_time_ns(int d, void* ev) = 0;
   virtual int copy_h2d(int d, int stream, uint64_t dst_off, const void* src, uint64_t n, std::string& err) = 0;
@@ -238,6 +241,13 @@ struct Device {
   int index = 0;
   uint64_t capacity = 0, free_bytes = 0;
   std::map<uint64_t, uint64_t> free_list;      // offset -> size, first fit
+  // arena ranges whose evicted contents are still being written back (D2H on the
+  // evicting task's stream): a new block allocated over one must wait for it
+  struct PendingWriteBack {
+    uint64_t off, size;
+    SyncP done;
+  };
+  std::vector<PendingWriteBack> pending_wb;
   std::unordered_map<uint64_t, Block*> blocks;  // hid -> live block
   uint64_t clock = 0;
   DevQueue queue;
@@ -297,6 +307,7 @@ class Runtime {
   void release_commute(Task* t);
   int ensure_block(int d, int s, Handle* h, std::vector<Action>& acts, std::vector<Block*>& tmp_pins, Block** out,
                    std::string& err);
+  void wait_pending_wb(int d, int s, uint64_t off, uint64_t size, std::vector<Action>& acts);
   int evict_one(int d, int s, std::vector<Action>& acts, std::string& err);
   void drop_block(Block* b, bool write_back, std::vector<Action>* acts, int s);
   void free_space(int d, uint64_t off, uint64_t size);

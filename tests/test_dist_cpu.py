@@ -7,6 +7,7 @@ ranks exit 0 without work) are what the driver relies on at N > 1.
 
 import json
 import os
+import re
 import socket
 import subprocess
 import sys
@@ -20,6 +21,12 @@ def _free_port() -> int:
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
+
+
+def _json_lines(text):
+    """Flat JSON objects printed by the ranks (two ranks' lines may interleave in
+    the captured stream, so objects are matched rather than lines)."""
+    return [json.loads(m) for m in re.findall(r"\{[^{}]*\}", text)]
 
 
 def _torchrun(args, timeout=240):
@@ -43,7 +50,7 @@ def test_dist_max_over_ranks_gloo(tmp_path):
         "d.done()\n")
     r = _torchrun([str(script)])
     assert r.returncode == 0, r.stderr[-2000:]
-    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    lines = _json_lines(r.stdout)
     assert sorted(x["rank"] for x in lines) == [0, 1]
     assert all(x["world"] == 2 and x["max"] == 3.0 for x in lines)
 
@@ -52,7 +59,7 @@ def test_reference_arm_prints_once_under_torchrun():
     r = _torchrun(["bench.py", "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0",
                    "--matrix-n", "1024", "--tile-b", "256", "--cpu-seconds", "0.5"])
     assert r.returncode == 0, r.stderr[-2000:]
-    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]  # rank 0 alone prints
     assert len(lines) == 1, r.stdout
     line = lines[0]
     assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "GFLOP/s"
@@ -66,7 +73,7 @@ def test_comm_tasks_between_two_processes():
     mismatch poisoning with CommProtocolError, insertion validation."""
     r = _torchrun([os.path.join("tests", "dist", "comm_ranks.py")])
     assert r.returncode == 0, r.stderr[-3000:]
-    out = {x["rank"]: x for x in (json.loads(l) for l in r.stdout.splitlines() if l.startswith("{"))}
+    out = {x["rank"]: x for x in _json_lines(r.stdout)}
     assert set(out) == {0, 1}
     for rank in (0, 1):
         assert out[rank]["tiers"] == [41, "ping", 66.0]
@@ -81,6 +88,6 @@ def test_comm_tasks_between_two_processes():
 def test_comm_tasks_with_gpu_engines():
     r = _torchrun([os.path.join("tests", "dist", "comm_gpu_ranks.py")])
     assert r.returncode == 0, r.stderr[-3000:]
-    out = {x["rank"]: x for x in (json.loads(l) for l in r.stdout.splitlines() if l.startswith("{"))}
+    out = {x["rank"]: x for x in _json_lines(r.stdout)}
     assert out[0]["d2h"] >= 256 * 256 * 8  # the dirty GPU tile was fetched home before the send
     assert out[1]["recv_exact"] and out[1]["gemm_err"] <= 1e-15
