@@ -714,6 +714,9 @@ void Runtime::drop_block(Block* b, bool write_back, std::vector<Action>* acts, i
   if (b->prefetched) {
     b->prefetched = false;
     b->pins -= 1;
+    // its H2D copy may still be in flight on the prefetch stream: the space is only
+    // reusable after it (same mechanism as a pending write-back)
+    if (b->ready && !b->ready->complete) D.pending_wb.push_back(Device::PendingWriteBack{b->off, b->size, b->ready});
   }
   b->valid = false;
   b->dirty = false;
@@ -754,6 +757,16 @@ int Runtime::evict_one(int d, int s, std::vector<Action>& acts, std::string& err
     if (b->pins) continue;
     if (!victim || b->stamp < victim->stamp || (b->stamp == victim->stamp && b->h->hid < victim->h->hid)) victim = b;
   }
+  if (!victim) {
+    // only blocks held by the prefetcher remain: give one back (clean data, the host
+    // copy is valid) rather than waiting for a task that may need that very space
+    for (auto& kv : D.blocks) {
+      Block* b = kv.second;
+      if (!(b->prefetched && b->pins == 1)) continue;
+      if (!victim || b->stamp < victim->stamp || (b->stamp == victim->stamp && b->h->hid < victim->h->hid))
+        victim = b;
+    }
+  }
   if (!victim) return 1;
   D.stats.evictions += 1;
   if (debug_staging())
@@ -777,7 +790,8 @@ int Runtime::ensure_block(int d, int s, Handle* h, std::vector<Action>& acts, st
   if (!b) {
     auto pinned_by_others = [&]() {
       size_t mine = 0, all = 0;
-      for (auto& kv : D.blocks) all += kv.second->pins;
+      for (auto& kv : D.blocks)
+        if (!(kv.second->prefetched && kv.second->pins == 1)) all += kv.second->pins;  // prefetch pins yield
       for (Block* p : tmp_pins)
         if (p->dev == d) mine += 1;
       return all > mine || D.ninflight > 0;
@@ -1510,9 +1524,18 @@ void Runtime::exec_loop(int d) {
       }
       // nothing planned yet: issue the write-backs planned so far, then wait for
       // any completion and re-plan
-      if (debug_staging())
-        fprintf(stderr, "[sfx] nothing-planned wait group=%zu first=%llu acts=%zu\n", group.size(),
-                (unsigned long long)group[0]->tid, acts.size());
+      if (debug_staging()) {
+        fprintf(stderr, "[sfx] nothing-planned wait group=%zu first=%llu acts=%zu ninflight=%d free=%llu blocks:",
+                group.size(), (unsigned long long)group[0]->tid, acts.size(), D.ninflight,
+                (unsigned long long)D.free_bytes);
+        for (auto& kv : D.blocks)
+          fprintf(stderr, " [hid=%llu off=%llu pins=%d valid=%d dirty=%d pf=%d zombie=%d]", (unsigned long long)kv.first,
+                  (unsigned long long)kv.second->off, kv.second->pins, kv.second->valid ? 1 : 0,
+                  kv.second->dirty ? 1 : 0, kv.second->prefetched ? 1 : 0, kv.second->zombie ? 1 : 0);
+        fprintf(stderr, " task accesses:");
+        for (auto& a : group[0]->acc) fprintf(stderr, " %llu", (unsigned long long)a.h->hid);
+        fprintf(stderr, "\n");
+      }
       if (!acts.empty()) {
         lk.unlock();
         std::string e2;
