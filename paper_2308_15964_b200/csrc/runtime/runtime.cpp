@@ -1047,6 +1047,9 @@ int Runtime::issue(int d, int s, const std::vector<Task*>& group, std::vector<Ac
   for (Action& a : acts) {
     switch (a.kind) {
       case Action::WAIT: {
+        if (debug_staging())
+          fprintf(stderr, "[sfx]   issue s=%d WAIT on stream %d%s\n", s, a.sync->stream,
+                  (a.sync->dev == d && a.sync->stream == s) ? " (same, skipped)" : "");
         if (a.sync->dev == d && a.sync->stream == s) break;  // stream order suffices
         while (!a.sync->recorded.load(std::memory_order_acquire)) std::this_thread::yield();
         rc = be_->stream_wait(d, s, a.sync->event, err);
@@ -1054,9 +1057,11 @@ int Runtime::issue(int d, int s, const std::vector<Task*>& group, std::vector<Ac
         break;
       }
       case Action::H2D:
+        if (debug_staging()) fprintf(stderr, "[sfx]   issue s=%d H2D off=%llu\n", s, (unsigned long long)a.dst_off);
         rc = be_->copy_h2d(d, s, a.dst_off, a.host, a.n, err);
         break;
       case Action::D2H:
+        if (debug_staging()) fprintf(stderr, "[sfx]   issue s=%d D2H off=%llu\n", s, (unsigned long long)a.src_off);
         rc = be_->copy_d2h(d, s, a.host, a.src_off, a.n, err);
         break;
       case Action::P2P:
@@ -1075,6 +1080,7 @@ int Runtime::issue(int d, int s, const std::vector<Task*>& group, std::vector<Ac
   for (auto& op : ops)
     if (op.op != SFX_OP_FLUSH && op.op != SFX_OP_NOOP && op.op != SFX_OP_EXTERN) kern.push_back(op);
   if (!kern.empty()) {
+    if (debug_staging()) fprintf(stderr, "[sfx]   issue s=%d launch task=%llu\n", s, (unsigned long long)group[0]->tid);
     rc = be_->launch_group(d, s, kern, err);
     if (rc) return rc;
     devs_[d]->stats.kernel_launches += kern.size();  // sim: ops executed
@@ -1627,6 +1633,9 @@ void Runtime::comp_loop(int d) {
     Task* t = D.inflight.front();
     void* ev = t->end->event;
     SyncP keep = t->end;
+    if (debug_staging())
+      fprintf(stderr, "[sfx] comp wait task=%llu recorded=%d inflight=%zu\n", (unsigned long long)t->tid,
+              t->end->recorded.load() ? 1 : 0, D.inflight.size());
     lk.unlock();
     std::string err;
     int rc = be_->event_sync(d, ev, err);
