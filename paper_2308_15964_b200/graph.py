@@ -385,24 +385,23 @@ class TaskGraph:
         batch = self._batch
         self._batch = None
         n = len(batch)
-        descs = np.zeros(n, dtype=TASK_DTYPE)
         total = sum(len(b[3]) for b in batch)
-        acc = np.zeros(max(total, 1), dtype=ACCESS_DTYPE)
+        descs = bytearray(_DESC.size * n)
+        acc = bytearray(_ACC.size * max(total, 1))
+        gid = self._gid
+        pack_d, pack_a = _DESC.pack_into, _ACC.pack_into
+        dsz, asz = _DESC.size, _ACC.size
         k = 0
         for i, (tid, op, prio, hids, modes, dev) in enumerate(batch):
-            descs[i]["tid"] = tid
-            descs[i]["graph"] = self._gid
-            descs[i]["op"] = op.code
-            descs[i]["priority"] = prio
-            descs[i]["device"] = dev
-            descs[i]["n_access"] = len(hids)
-            descs[i]["fparam"] = op.fparam
-            descs[i]["iparam"] = op.iparam
+            fp, ip = op.fparam, op.iparam
+            pack_d(descs, i * dsz, tid, gid, op.code, int(prio), dev, len(hids), 0,
+                   fp[0], fp[1], fp[2], fp[3], ip[0], ip[1], ip[2], ip[3])
             for h, m in zip(hids, modes):
-                acc[k]["hid"] = h
-                acc[k]["mode"] = m
+                pack_a(acc, k * asz, h, m, 0)
                 k += 1
-        N.check(N.lib.sfx_submit(self._h, n, descs.ctypes.data, acc.ctypes.data), self._h)
+        dbuf = (ctypes.c_char * len(descs)).from_buffer(descs)
+        abuf = (ctypes.c_char * len(acc)).from_buffer(acc)
+        N.check(N.lib.sfx_submit(self._h, n, dbuf, abuf), self._h)
 
     # -- waiting (graph.py:199-217) --------------------------------------------
     def _failure(self) -> EngineFailedError:
