@@ -1458,8 +1458,9 @@ void Runtime::exec_loop(int d) {
         if (!a.h->blocks[d]) n += std::max<uint64_t>((a.h->bytes + align_ - 1) / align_ * align_, align_);
       return n;
     };
+    static const bool no_stage_limit = getenv("SFX_GROUP_NO_STAGE_LIMIT") != nullptr;  // experiment switch
     uint64_t group_stage = staging_bytes(first);
-    if (groupable(first) && group_stage <= D.free_bytes) {
+    if (groupable(first) && (no_stage_limit || group_stage <= D.free_bytes)) {
       const bool urgent = first->prio >= urgent_priority_;
       while (group.size() < group_max_ && D.queue.size() > 0 &&
              D.ninflight + static_cast<int>(group.size()) < static_cast<int>(window_)) {
@@ -1468,7 +1469,7 @@ void Runtime::exec_loop(int d) {
           break;
         if (first->op == SFX_OP_DTRSM && nx->prio != first->prio) break;  // a critical TRSM launches alone
         const uint64_t more = staging_bytes(nx);
-        if (group_stage + more > D.free_bytes) break;  // would evict mid-group
+        if (!no_stage_limit && group_stage + more > D.free_bytes) break;  // would evict mid-group
         group_stage += more;
         D.queue.pop();
         if (!nx->commute.empty() && !acquire_commute(nx)) continue;
@@ -1529,7 +1530,12 @@ void Runtime::exec_loop(int d) {
         break;
       }
       // nothing planned yet: issue the write-backs planned so far, then wait for
-      // any completion and re-plan
+      // any completion and re-plan.  The completion count is sampled NOW, before
+      // the lock is released for the issue: a completion that lands while the
+      // write-backs are issued must still wake this wait (it used to be sampled
+      // after re-locking, which could miss the last in-flight task and hang).
+      uint64_t total_before = 0;
+      for (auto& dv : devs_) total_before += dv->stats.tasks_executed;
       if (debug_staging()) {
         fprintf(stderr, "[sfx] nothing-planned wait group=%zu first=%llu acts=%zu ninflight=%d free=%llu blocks:",
                 group.size(), (unsigned long long)group[0]->tid, acts.size(), D.ninflight,
@@ -1556,13 +1562,13 @@ void Runtime::exec_loop(int d) {
           break;
         }
       }
-      uint64_t total_before = 0;
-      for (auto& dv : devs_) total_before += dv->stats.tasks_executed;
+
       done_cv_.wait(lk, [&] {
         uint64_t tot = 0;
         for (auto& dv : devs_) tot += dv->stats.tasks_executed;
         return stopping_ || fail_code_ || tot != total_before;
       });
+      if (debug_staging()) fprintf(stderr, "[sfx] executor woke (first=%llu)\n", (unsigned long long)group[0]->tid);
       if (stopping_ || fail_code_) {
         rc = -100;
         break;
@@ -1639,7 +1645,9 @@ void Runtime::comp_loop(int d) {
     lk.unlock();
     std::string err;
     int rc = be_->event_sync(d, ev, err);
+    if (debug_staging()) fprintf(stderr, "[sfx] comp synced task=%llu rc=%d\n", (unsigned long long)t->tid, rc);
     lk.lock();
+    if (debug_staging()) fprintf(stderr, "[sfx] comp locked task=%llu\n", (unsigned long long)t->tid);
     const int64_t tc0 = now_ns();
     D.inflight.pop_front();
     if (rc) poison(SFX_ERR_CUDA, err);

@@ -167,3 +167,37 @@ def test_real_gemm_trace_is_bit_exact_with_the_reference():
         assert (np.abs(C.to_dense() - want) / np.abs(want)).max() <= 1e-10
     finally:
         eng.stop()
+
+
+@pytest.mark.parametrize("streams", [1, 2, 4])
+def test_random_programs_through_a_tiny_arena_on_the_gpu(streams):
+    """The reference's random programs (every access mode) on real CUDA streams
+    through an arena of four 64-byte slots: most accesses evict, dirty cells are
+    written back and re-staged while other streams run, and the executor often
+    has to wait for a completion before it can plan (this found a missed
+    wake-up that hung the engine).  Values equal the sequential execution
+    frozen from the reference."""
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "random_programs.json")) as fh:
+        progs = json.load(fh)
+    mode = {"read": sf.read, "write": sf.write, "atomic": sf.atomic_write, "commute": sf.commutative_write,
+            "maybe": sf.maybe_write}
+    widest = max(1 + len(t[2]) for q in progs[:60] for t in q["tasks"])
+    assert widest <= 4  # the CUDA arena is at least 256 bytes: 4 slots of 64
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, streams), device_memory=256, arena_align=64)
+    try:
+        for p in progs[:60]:
+            g = sf.TaskGraph().compute_on(eng)
+            cells = [sf.Cell(i + 1) for i in range(p["n_cells"])]
+            for m, target, reads, a, b in p["tasks"]:
+                acc = [mode[m](cells[target])] + [sf.read(cells[r]) for r in reads]
+                g.task(*acc, device=sf.ops.cell(m, a, b))
+            for c in cells:
+                g.flush_to_host(c)
+            assert g.wait_all(timeout=60)
+            assert [c.value for c in cells] == p["sequential"]
+        assert eng.stats(0)["evictions"] > 0
+    finally:
+        eng.stop()
