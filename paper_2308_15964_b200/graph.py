@@ -266,19 +266,21 @@ class TaskGraph:
     def task(self, *accesses, host=None, device=None, priority: int = 0, name=None):
         if __debug__:
             ident = threading.get_ident()
-            assert self._inserter_ident in (None, ident), "tasks must be inserted by a single thread"
-            self._inserter_ident = ident
+            if self._inserter_ident != ident:
+                assert self._inserter_ident is None, "tasks must be inserted by a single thread"
+                self._inserter_ident = ident
         if self.engine is None:
             raise ConfigurationError("attach the graph to an engine before inserting")
-        if device is None:
-            if host is not None:
+        if device.__class__ is not ops_mod.Op:
+            if device is None:
+                if host is not None:
+                    raise ConfigurationError(
+                        "host callables run on the CPU oracle only: the GPU engine has no CPU fallback; "
+                        "pass device=<paper_2308_15964_b200.ops op>")
+                raise ConfigurationError("a task needs a host or device callable")
+            if not isinstance(device, ops_mod.Op):
                 raise ConfigurationError(
-                    "host callables run on the CPU oracle only: the GPU engine has no CPU fallback; "
-                    "pass device=<paper_2308_15964_b200.ops op>")
-            raise ConfigurationError("a task needs a host or device callable")
-        if not isinstance(device, ops_mod.Op):
-            raise ConfigurationError(
-                f"device= must be a registered op (paper_2308_15964_b200.ops), got {device!r}")
+                    f"device= must be a registered op (paper_2308_15964_b200.ops), got {device!r}")
         hids = []
         modes = []
         entries = self._entries
@@ -294,7 +296,8 @@ class TaskGraph:
                 raise DuplicateAccessError(f"task declares {type(spec.obj).__name__} twice")
             hids.append(hid)
             modes.append(_MODE_CODE[spec.mode])
-        tid = _next_tid()
+        with _id_lock:  # _reserve_tids swaps the counter under this lock
+            tid = next(_tid_counter)
         if name is not None:
             self._names[tid] = name
         self._tids.append(tid)
