@@ -60,6 +60,7 @@ def parse():
                     help="launch-group size for the Cholesky legs (tools/chol_sweep.py: 8 best for b=1024)")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--e2e-row-priorities", type=int, default=0)
+    ap.add_argument("--e2e-skew", type=int, default=-1, help="insert_gemm skew on the e2e leg (-1: 2*nt, 0: FIFO)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -272,9 +273,12 @@ def main_ours(args, dist):
 
     # ---- e2e: host-resident inputs through the public API ----
     def e2e_step():
-        # block-row priorities: rows of C finish one after another, so their flush
-        # (D2H) and the next rows' staging (H2D) overlap the remaining compute
-        alg.insert_gemm(g, A, B, C, priorities=args.e2e_row_priorities)
+        # wavefront priorities (insert_gemm skew): the k-chains of the C tiles start
+        # staggered over 2*nt waves, so C's staging (2 GiB H2D) and its flush
+        # (2 GiB D2H) spread over the step instead of piling up in the first and
+        # last waves (tools/e2e_probe.py: 25.7 -> 28.3 TFLOP/s)
+        alg.insert_gemm(g, A, B, C, priorities=args.e2e_row_priorities,
+                        skew=args.e2e_skew if args.e2e_skew >= 0 else 2 * nt)
         for t in C.tiles.values():
             g.flush_to_host(t)                      # C back to the host (write-mode flush)
         for M in (A, B):

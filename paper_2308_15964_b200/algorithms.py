@@ -154,7 +154,7 @@ def _emit(graph, fast):
 
 
 def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: bool = True,
-                priorities=False, tile_block: int = 0):
+                priorities=False, tile_block: int = 0, skew: int = 0):
     """C += A B over tiles, loop order i, j, k.
 
     ``priorities`` (False, True or a row-block height h): block row i gets priority
@@ -163,12 +163,20 @@ def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: boo
     instead of every chain advancing in lock-step -- staging of A/C rows and the
     flush of finished C tiles then overlap the remaining compute.
 
+    ``skew`` = S > 0 (overrides the others): a wavefront -- task (i, j, k) gets
+    priority -(k + S * (i * nt + j) // nt^2), so the k-chains of the C tiles start
+    staggered over S waves: when the operands start on the host, C's staging and
+    its final flush spread over the run instead of piling up in the first and
+    last waves.
+
     ``tile_block`` = h > 0 (overrides ``priorities``): the C tiles are ranked in
     h x h blocks (block-row-major), each block's tasks one priority level above the
     next block's: a block needs only h rows of A and h columns of B, so when the
     operands start on the host, staging spreads over the whole step.
     """
     nt = A.nt
+    if skew:
+        off = lambda i, j: int(skew) * (i * nt + j) // (nt * nt)  # noqa: E731
     if tile_block:
         h = int(tile_block)
         nbc = (nt + h - 1) // h
@@ -181,8 +189,8 @@ def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: boo
     if not fast:
         for i in range(nt):
             for j in range(nt):
-                prio = rank(i, j)
                 for k in range(nt):
+                    prio = -(k + off(i, j)) if skew else rank(i, j)
                     graph.task(read(A[i, k]), read(B[k, j]), write(C[i, j]), device=ops.gemm_nn,
                                priority=prio, name="gemm")
         return None
@@ -195,7 +203,10 @@ def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: boo
     jj, kk = jj.reshape(-1), kk.reshape(-1)
     for i in range(nt):
         hids = np.stack([HA[i, kk], HB[kk, jj], HC[i, jj]], axis=1)
-        prio = np.repeat(np.array([rank(i, j) for j in range(nt)], np.int32), nt)  # jj-major like hids
+        if skew:  # per task: -(k + offset of its chain)
+            prio = -(kk + np.array([off(i, j) for j in range(nt)], np.int64)[jj]).astype(np.int32)
+        else:
+            prio = np.repeat(np.array([rank(i, j) for j in range(nt)], np.int32), nt)  # jj-major like hids
         batch.add_many(ops.gemm_nn, hids, modes, prio, "gemm")
         batch.flush()
     return batch.submit()

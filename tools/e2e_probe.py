@@ -57,6 +57,7 @@ def main():
     ap.add_argument("--no-bw", action="store_true")
     ap.add_argument("--row-block", type=int, default=0, help="insert_gemm priorities (row-block height, 0 = off)")
     ap.add_argument("--tile-block", type=int, default=0, help="insert_gemm tile_block (h x h C blocks, 0 = off)")
+    ap.add_argument("--skew", type=int, default=0, help="insert_gemm skew (wavefront over S waves, 0 = off)")
     a = ap.parse_args()
     if not a.no_bw:
         bw()
@@ -73,7 +74,7 @@ def main():
     g.wait_all()
 
     def e2e_step(gr):
-        alg.insert_gemm(gr, A, B, C, priorities=a.row_block, tile_block=a.tile_block)
+        alg.insert_gemm(gr, A, B, C, priorities=a.row_block, tile_block=a.tile_block, skew=a.skew)
         for M in (C, A, B):
             for t in M.tiles.values():
                 gr.flush_to_host(t)
