@@ -794,7 +794,13 @@ int Runtime::ensure_block(int d, int s, Handle* h, std::vector<Action>& acts, st
         if (!(kv.second->prefetched && kv.second->pins == 1)) all += kv.second->pins;  // prefetch pins yield
       for (Block* p : tmp_pins)
         if (p->dev == d) mine += 1;
-      return all > mine || D.ninflight > 0;
+      if (all > mine) return true;
+      // blocks pinned by tasks of OTHER devices (peer-pull sources) -- and zombies
+      // (invalidated while pinned, already out of D.blocks) -- are released by
+      // completions anywhere: wait while any device has work in flight
+      for (auto& dv : devs_)
+        if (dv->ninflight > 0) return true;
+      return false;
     };
     while (D.free_bytes < size) {
       if (evict_one(d, s, acts, err)) {
