@@ -956,6 +956,11 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
       wait_on(b->ready);
     } else {
       D.stats.misses += 1;
+      // the block may have been allocated by an earlier, failed plan over a range
+      // whose previous contents are still being written back on another stream:
+      // the copy into it must wait for that write-back (allocation-time waits
+      // only cover blocks allocated by this plan)
+      wait_pending_wb(d, s, b->off, b->size, acts);
       int src = -1;
       if (h->dirty_dev >= 0 && h->dirty_dev != d) {
         src = h->dirty_dev;
@@ -1453,18 +1458,18 @@ void Runtime::exec_loop(int d) {
     if (!first->commute.empty() && !acquire_commute(first)) continue;  // parked until the guard frees
     group.push_back(first);
     // A group only grows while the operands its members still have to stage fit in
-    // the free arena space: grouped launches that ran out of space mid-group (and
-    // evicted between members) were seen to produce wrong panel tiles (2048/256
-    // Cholesky in a 7 MB arena, >= 2 streams, groups >= 3; never with groups <= 2
-    // in 110 runs) -- root cause not found yet, see DESIGN.md "Known issues".
-    // With the working set resident (the benchmark configurations) nothing changes.
+    // the free arena space, so no member evicts between the members of one
+    // launch: under a tile cache much smaller than the working set this cuts the
+    // eviction traffic (C3 with a 3 GiB arena: 25.9 -> 27.3 TFLOP/s).  (It first
+    // served as the mitigation of the write-back race fixed in plan() pass 2; with
+    // SFX_GROUP_NO_STAGE_LIMIT=1 the limit is off, tools/arena_stress.py stays correct.)
     auto staging_bytes = [&](const Task* t) {
       uint64_t n = 0;
       for (const Access& a : t->acc)
         if (!a.h->blocks[d]) n += std::max<uint64_t>((a.h->bytes + align_ - 1) / align_ * align_, align_);
       return n;
     };
-    static const bool no_stage_limit = getenv("SFX_GROUP_NO_STAGE_LIMIT") != nullptr;  // experiment switch
+    static const bool no_stage_limit = getenv("SFX_GROUP_NO_STAGE_LIMIT") != nullptr;  // for stress tests
     uint64_t group_stage = staging_bytes(first);
     if (groupable(first) && (no_stage_limit || group_stage <= D.free_bytes)) {
       const bool urgent = first->prio >= urgent_priority_;

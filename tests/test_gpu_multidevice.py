@@ -4,6 +4,8 @@ completion threads; cudaMemcpyPeerAsync between them degenerates to a device
 copy).  This exercises placement, peer pulls, cross-device event waits and
 invalidation with the real backend even on a single-GPU box."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -234,3 +236,19 @@ def test_random_programs_across_devices_through_tiny_arenas(ndev, streams):
         assert sum(eng.stats(d)["bytes_p2p_in"] for d in range(ndev)) > 0
     finally:
         eng.stop()
+
+
+def test_tile_cache_stress_with_requeued_groups():
+    """Regression test for the write-back race: a Cholesky through a 13-slot tile
+    cache with launch groups that run out of space mid-group (the staging-aware
+    group limit switched off, so requeued members re-plan on other streams over
+    ranges still being written back).  Every factor must be exact."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SFX_GROUP_NO_STAGE_LIMIT="1", GM="8")
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "arena_stress.py"), "12", "full", "4", "1"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "wrong factors: 0 of 12" in r.stdout, r.stdout[-2000:]
