@@ -5,8 +5,9 @@
 
 2048^2 / 256 tiles (36 lower tiles of 512 KiB) through a ~7 MB arena (13 slots):
 nearly every task evicts.  Environment: MEM=<arena bytes>, PF=0/1 (prefetch),
-GM=<group_max>, GPS=<groups per stream>, SFX_GROUP_NO_STAGE_LIMIT=1 (disable the
-staging-aware launch-group limit: reproduces DESIGN.md §6c).
+GM=<group_max>, GPS=<groups per stream>, NDEV=<logical devices on GPU 0, 2-D
+block-cyclic tiles, peer pulls>, SFX_GROUP_NO_STAGE_LIMIT=1 (disable the
+staging-aware launch-group limit: the regime of the write-back race in DESIGN.md §6c).
 """
 import os
 import sys
@@ -33,7 +34,8 @@ def main():
     mem = int(os.environ.get("MEM", (36 * b * b * 8) * 10 // 27))
     bad = 0
     for rep in range(reps):
-        eng = sf.create_engine(sf.WorkerTeam.of_devices(1, streams), device_memory=mem)
+        ndev = int(os.environ.get("NDEV", "1"))
+        eng = sf.create_engine(sf.WorkerTeam.of_devices(ndev, streams), device_memory=mem, ordinals=[0] * ndev)
         for opt, env in (("prefetch", "PF"), ("group_max", "GM"), ("groups_per_stream", "GPS")):
             if os.environ.get(env) is not None:
                 eng.set_option(opt, int(os.environ[env]))
@@ -41,6 +43,8 @@ def main():
         for ij, t in M.tiles.items():
             t[...] = objs[("A",) + ij]
         g = sf.TaskGraph().compute_on(eng)
+        if ndev > 1:
+            alg.block_cyclic(g, M, *alg.grid_shape(ndev))
         alg.insert_cholesky(g, M, priorities=prio, inverse_blocks=inv)
         g.flush_all(keep_device=False)
         g.wait_all(timeout=120)
