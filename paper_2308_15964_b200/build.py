@@ -90,7 +90,35 @@ def build(verbose: bool = False, force: bool = False) -> str:
         os.replace(tmp, OUT)
         if verbose:
             print("linked", os.path.relpath(OUT, ROOT))
+    _build_pyext(verbose, force)
     return OUT
+
+
+def _build_pyext(verbose: bool, force: bool) -> None:
+    """The optional CPython fast path for single-task submits (csrc/pyext/sfxfast.c),
+    linked against libsfx.so (rpath $ORIGIN).  Failure is not fatal: the ctypes
+    path stays in use."""
+    import sysconfig
+
+    src = os.path.join(CSRC, "pyext", "sfxfast.c")
+    out = os.path.join(PKG, "_sfxfast" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
+    if not os.path.exists(src):
+        return
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(src), os.path.getmtime(OUT)):
+        return
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        return
+    cmd = [cc, "-O2", "-shared", "-fPIC", "-I", sysconfig.get_paths()["include"], "-I", os.path.join(ROOT, "include"),
+           src, "-o", out + ".tmp", "-L", PKG, "-l:libsfx.so", "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        if verbose:
+            print("python fast path not built:", r.stderr.strip()[:300])
+        return
+    os.replace(out + ".tmp", out)
+    if verbose:
+        print("linked", os.path.relpath(out, ROOT))
 
 
 if __name__ == "__main__":

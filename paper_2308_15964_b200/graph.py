@@ -22,6 +22,11 @@ import time
 import numpy as np
 
 from . import _native as N
+
+try:  # CPython fast path for single-task submits (csrc/pyext/sfxfast.c); ctypes otherwise
+    from ._sfxfast import submit1 as _fast_submit1
+except ImportError:  # pragma: no cover - the build makes it next to libsfx.so
+    _fast_submit1 = None
 from . import memory
 from . import ops as ops_mod
 from .access import _CODES as _MODE_CODE
@@ -218,6 +223,7 @@ class TaskGraph:
         N.check(N.lib.sfx_graph_create(engine._h, ctypes.byref(gid)), engine._h)
         self.engine = engine
         self._h = engine._h
+        self._hval = engine._h.value  # raw runtime pointer for the fast submit path
         self._gid = gid.value
         engine.adopt(self)
         self._t0 = time.perf_counter_ns()
@@ -307,6 +313,12 @@ class TaskGraph:
     def _submit_one(self, tid, op, priority, hids, modes, dev_hint=-1):
         if self._batch is not None:
             self._batch.append((tid, op, priority, hids, modes, dev_hint))
+            return
+        if _fast_submit1 is not None:
+            rc = _fast_submit1(self._hval, self._gid, tid, op.code, int(priority), dev_hint, op.fparam, op.iparam,
+                               hids, modes)
+            if rc < 0:
+                N.check(rc, self._h)
             return
         # one struct.pack_into per descriptor into reused buffers (ctypes field
         # assignment costs ~10x more per task)
