@@ -1523,17 +1523,10 @@ void Runtime::exec_loop(int d) {
           t->end.reset();
           t->start.reset();
           t->state = SFX_STATE_READY;
-          if (t->guards_held) {
-            if (t->commute_shared) {
-              for (Handle* h : t->commute)
-                if (--h->shared_users == 0) h->shared_dev = -1;
-            } else {
-              for (Handle* h : t->commute)
-                if (h->commute_owner == t) h->commute_owner = nullptr;
-            }
-            t->guards_held = false;
-          }
           D.queue.push_front(t);
+          // give its commutative guards back -- handing them to parked members,
+          // who would otherwise wait on a free handle; it re-acquires when popped
+          if (t->guards_held) release_commute(t);
         }
         group.resize(planned);
         ops.resize(planned);
