@@ -12,7 +12,8 @@
 //
 // Design (B200, sm_100a):
 //  * CTA tile 128 x 128, K-step 16 doubles (128 B rows -> 128B TMA swizzle),
-//    4-stage TMA ring with full/empty mbarriers, 1 producer warp + 8 DMMA warps
+//    3-stage TMA ring with full/empty mbarriers (+ a TMA-prefetched C tile),
+//    1 producer warp + 8 DMMA warps
 //    (warp tile 64 x 32 = 8 x 4 DMMA fragments).
 //  * k-permutation: within a 16-wide K step, thread (g, t) of a DMMA uses the
 //    true k = 4t + kk for mma sub-step kk.  A summation index may be permuted
@@ -119,7 +120,7 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], CONSUMER_WARPS * 32);
+      ptx::mbar_init(&empty[s], CONSUMER_WARPS);
     }
     ptx::mbar_init(cfull, 1);
     ptx::mbar_init(cempty, CONSUMER_WARPS * 32);
@@ -224,7 +225,10 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
             }
           }
         }
-        if (h == 1) ptx::mbar_arrive(&empty[s]);  // operands are in registers: the slot may be refilled
+        if (h == 1) {  // operands are in registers: the slot may be refilled (one arrive per warp)
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&empty[s]);
+        }
 #pragma unroll
         for (int e = 0; e < 2; ++e)
 #pragma unroll
