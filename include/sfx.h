@@ -231,7 +231,8 @@ int sfx_violations(sfx_runtime* rt, uint64_t* n);
  * "urgent_priority" (priority from which tasks use the high-priority streams,
  * default 1000000), "prefetch" (0/1: stage queued tasks' host operands while
  * all streams are busy, default 1 on CUDA), "prefetch_depth" (queued tasks
- * looked at, default 64) */
+ * looked at, default 64), "kernel_timing" (0/1: launch-group timing events,
+ * as SFX_FLAG_KTIME; always on while tracing) */
 int sfx_set_option(sfx_runtime* rt, const char* key, int64_t value);
 
 /* external tasks (SFX_OP_EXTERN): block up to timeout_s (< 0: forever) until at

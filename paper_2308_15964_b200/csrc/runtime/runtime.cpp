@@ -1860,6 +1860,9 @@ int Runtime::set_option(const std::string& key, int64_t value) {
     prefetch_ = value != 0 && !be_->is_sim();
   } else if (key == "prefetch_depth") {
     prefetch_depth_ = static_cast<int>(std::max<int64_t>(0, value));
+  } else if (key == "kernel_timing") {
+    // launch-group timing events (SFX_FLAG_KTIME); tracing keeps them on
+    ktime_ = trace_ || value != 0;
   } else if (key == "window") {
     window_ = static_cast<uint32_t>(std::max<int64_t>(1, value));
     for (auto& d : devs_) d->exec_cv.notify_all();
