@@ -309,6 +309,28 @@ def test_wait_all_timeout_and_resume():
         eng.stop()
 
 
+def test_runtime_options_and_kernel_timing_toggle():
+    eng = sim_engine(kernel_timing=True)
+    try:
+        for key, val in (("group_max", 8), ("groups_per_stream", 4), ("prefetch", 0), ("prefetch_depth", 16),
+                         ("window", 256), ("urgent_priority", 10), ("kernel_timing", 0), ("kernel_timing", 1)):
+            eng.set_option(key, val)
+        with pytest.raises(sf.ConfigurationError):
+            eng.set_option("no_such_knob", 1)
+        g = sf.TaskGraph().compute_on(eng)
+        c = sf.Cell(1)
+        for _ in range(4):
+            g.task(sf.commutative_write(c), device=sf.ops.cell("commute", 1, 1))
+        eng.set_option("kernel_timing", 0)
+        for _ in range(4):
+            g.task(sf.commutative_write(c), device=sf.ops.cell("commute", 1, 1))
+        g.wait_all()
+        g.flush_all()
+        assert c.value == 9
+    finally:
+        eng.stop()
+
+
 def test_insertion_errors_match_reference():
     eng = sim_engine()
     try:
