@@ -313,10 +313,13 @@ __device__ bool factor64(Smem& s) {
       if (e < rows * 16) s.c[o + 16 + (e >> 4)][o + (e & 15)] = v[u];
     }
     __syncthreads();
-    // trailing lower update: c[i][k] -= sum_q c[i][o+q] c[k][o+q], o+16 <= k <= i < 64
-    for (int e = tid; e < rows * rows; e += THREADS) {
-      const int i = o + 16 + e / rows, k = o + 16 + e % rows;
-      if (k > i) continue;
+    // trailing lower update: c[i][k] -= sum_q c[i][o+q] c[k][o+q], o+16 <= k <= i < 64;
+    // threads walk the lower triangle only (row ii of it starts at ii(ii+1)/2)
+    for (int e = tid; e < rows * (rows + 1) / 2; e += THREADS) {
+      int ii = static_cast<int>((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+      while ((ii + 1) * (ii + 2) / 2 <= e) ++ii;
+      while (ii * (ii + 1) / 2 > e) --ii;
+      const int i = o + 16 + ii, k = o + 16 + (e - ii * (ii + 1) / 2);
       double acc = s.c[i][k];
 #pragma unroll
       for (int q = 0; q < 16; ++q) acc = fma(-s.c[i][o + q], s.c[k][o + q], acc);
