@@ -324,8 +324,8 @@ def test_runtime_options_and_kernel_timing_toggle():
         eng.set_option("kernel_timing", 0)
         for _ in range(4):
             g.task(sf.commutative_write(c), device=sf.ops.cell("commute", 1, 1))
+        g.flush_all()  # flush tasks are asynchronous like every task
         g.wait_all()
-        g.flush_all()
         assert c.value == 9
     finally:
         eng.stop()
