@@ -4,25 +4,37 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...     (one process per GPU)
 
-Workload at N=1 (BASELINE.json configs[1]): tiled DGEMM 16384 x 16384 FP64
-with 512 x 512 tiles ("1024 tiles") -> 32,768 GEMM tasks per step, inserted
-through the drop-in TaskGraph API and executed by the native runtime.  A step
-is one full tiled C += A B pass; inputs (3 x 2 GiB) are far larger than the
-126 MB L2, so no flush is needed between steps.  With N ranks every rank runs
-its own C2 instance on its GPU (weak scaling, no data-path collective: the
-DGEMM configs are 1 GPU per config).
+Workload by GPU count (``--workload auto``, the default):
 
-Legs of the JSON line:
-  value      device-resident inputs, FP64 GFLOP/s summed over ranks (CUDA
-             events on the device, max step time over ranks)
-  e2e        same metric through the public API from pinned HOST buffers: every
-             step stages A, B, C host->device on demand and flushes C back
-  roofline   FP64 DMMA pipe: achieved TFLOP/s of the DGEMM kernel over the timed
-             region vs the DMMA peak measured in-run on this GPU
+  N = 1   BASELINE.json configs[1] (C2): tiled DGEMM 16384 x 16384 FP64 with
+          512 x 512 tiles ("1024 tiles") -> 32,768 GEMM tasks per step, inserted
+          through the drop-in TaskGraph API and executed by the native runtime.
+          Inputs (3 x 2 GiB) are far larger than the 126 MB L2: no flush needed.
+  N > 1   BASELINE.json configs[2] (C3): tiled Cholesky 32768 x 32768 / 1024
+          tiles over all N GPUs from ONE runtime (rank 0): 2-D block-cyclic
+          owner-computes placement, panels pulled peer-to-peer over NVLink
+          (strong scaling).  The same run also factors C3 on GPU 0 alone so
+          the line carries its own 1-GPU reference.  Fewer visible GPUs than
+          N is an error (no silent fallback to one GPU).
+
+Legs of the N = 1 JSON line:
+  value         device-resident inputs, FP64 GFLOP/s (CUDA events, max over ranks)
+  check         every leg verifies its output after its timed region (verify.py):
+                sampled C tiles vs numpy, the C3 randomized residual, sampled
+                C4 particles; the tolerances and the errors are in the line
+  e2e           same metric through the public API from pinned HOST buffers: every
+                step stages A, B, C host->device on demand and flushes C back;
+                achieved H2D / D2H GB/s next to the measured PCIe rates
+  roofline      FP64 DMMA pipe: achieved TFLOP/s of the DGEMM kernel over the
+                timed region vs the DMMA peak measured in-run on this GPU
   cpu_baseline  the reference algorithm on the host cores (oracle restatement of
-             the reference STF engine + numpy bodies; rank 0, N=1), bounded sample
-  secondary  Cholesky 32768/1024 (C3) and particles 2^20/256 groups (C4) on one
-             GPU, and the runtime overhead in us/task (reference protocol)
+                the reference STF engine + numpy bodies; rank 0, N=1), bounded
+                samples of C2 (headline), C1, C3 and C4, and the reference's
+                overhead protocol on the same cores
+  secondary     C1, C3 (with residual) and C4 (with sampled check) on one GPU,
+                and the runtime overhead in us/task: the reference protocol
+                (src/bench.py:67-117) with T = host cores, N = 1000,
+                D in {0, 1e-4, 1e-3} s, write and commute, deps in {1, 5, 20}
 """
 
 from __future__ import annotations
@@ -39,6 +51,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+import verify  # noqa: E402  (numpy output checkers; no oracle)
+
 METRIC = "FP64 GFLOP/s tiled Cholesky/GEMM at 1/2/4/8 B200 (% FP64 peak); µs/task"
 
 
@@ -48,10 +62,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--workload", choices=("gemm", "cholesky", "particles"), default="gemm",
-                    help="gemm: C2 tiled DGEMM (default, BASELINE configs[1]); cholesky: tiled Cholesky over "
-                         "all --gpus GPUs from one runtime (C3 at n=32768/1024, C5 at n=65536/1024); "
-                         "particles: C4 (2^20 particles, 256 groups) over all --gpus GPUs from one runtime")
+    ap.add_argument("--workload", choices=("auto", "gemm", "cholesky", "particles"), default="auto",
+                    help="auto: gemm (C2) at N=1, cholesky (C3) over N GPUs at N>1; cholesky/particles run "
+                         "over all --gpus GPUs from one runtime")
+    ap.add_argument("--ordinals", default=None,
+                    help="comma-separated CUDA ordinals for the multi-GPU legs (e.g. 0,0 = two logical "
+                         "devices on one GPU, for functional runs on a 1-GPU box)")
     ap.add_argument("--n", "--matrix-n", dest="n", type=int, default=None)
     ap.add_argument("--b", "--tile-b", dest="b", type=int, default=None)
     ap.add_argument("--streams", type=int, default=32)
@@ -59,10 +75,11 @@ def parse():
     ap.add_argument("--chol-group", type=int, default=8,
                     help="launch-group size for the Cholesky legs (tools/chol_sweep.py: 8 best for b=1024)")
     ap.add_argument("--no-secondary", action="store_true")
-    ap.add_argument("--e2e-row-priorities", type=int, default=0)
+    ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--e2e-skew", type=int, default=-1, help="insert_gemm skew on the e2e leg (-1: 2*nt, 0: FIFO)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--overhead-n", type=int, default=1000)
     return ap.parse_args()
 
 
@@ -114,27 +131,30 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
-        self.index = index
+    def __init__(self, index):
+        self.index = index if isinstance(index, (list, tuple)) else [index]
         self.samples = []
         self._stop = threading.Event()
         self._th = None
 
     def start(self):
+        ids = ",".join(str(i) for i in sorted(set(self.index)))
+
         def run():
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                    out = subprocess.run(["nvidia-smi", "-i", ids, "--query-gpu=" + self.FIELDS,
                                           "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                          timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([x.strip() for x in out.split(",")])
+                    for line in out.splitlines():
+                        self.samples.append([x.strip() for x in line.split(",")])
                 except Exception:
                     pass
                 self._stop.wait(0.2)
 
         self._th = threading.Thread(target=run, daemon=True)
         self._th.start()
+        return self
 
     def stop(self):
         self._stop.set()
@@ -152,14 +172,132 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.samples)}
 
 
-# ----------------------------------------------------------------- CPU leg
+# ------------------------------------------------- overhead protocol (both arms)
 
-def cpu_baseline(n: int, b: int, seconds: float, steps: int = 1, warmup: int = 0):
+def derive_report(t0: int, insertion_ns: int, ends, duration: float) -> dict:
+    """Per-rep numbers from raw end timestamps, restated from the reference's
+    src/bench.py:96-117 (O_avg = makespan / N - D; O_max = worst gap between
+    consecutive ends of a chain minus D; insertion cost per task)."""
+    T = len(ends)
+    N = len(ends[0])
+    makespan_s = (max(max(row) for row in ends) - t0) / 1e9
+    o_max = None
+    for row in ends:
+        prev = t0
+        for end in sorted(row):
+            gap = (end - prev) / 1e9 - duration
+            o_max = gap if o_max is None or gap > o_max else o_max
+            prev = end
+    return {"insertion_per_task_us": insertion_ns / 1e3 / (T * N), "makespan_s": makespan_s,
+            "o_avg_us": (makespan_s / N - duration) * 1e6, "o_max_us": o_max * 1e6}
+
+
+def _mean_reports(reps):
+    return {k: statistics.mean(r[k] for r in reps) for k in reps[0]}
+
+
+def overhead_gpu(sf, dev, T, N, D, mode, deps, reps=3):
+    """The reference overhead protocol on the GPU engine: T chains (CUDA streams)
+    x N tasks, each writing (or commutatively writing) its chain cell and reading
+    deps-1 extra cells; the body is a D-second device spin (no kernel at D = 0).
+    End timestamps are the tasks' CUDA end events on the host clock."""
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, T), trace=True, ordinals=[dev], device_memory=1 << 26)
+    acc = sf.write if mode == "write" else sf.commutative_write
+    op = sf.ops.noop if D == 0 else sf.ops.spin(int(D * 1e9))
+    out = []
+    try:
+        for _ in range(reps + 1):  # the first rep warms the streams / event pools
+            g = sf.TaskGraph().compute_on(eng)
+            chains = [sf.Cell(0) for _ in range(T)]
+            extras = [[sf.Cell(0) for _ in range(deps - 1)] for _ in range(T)]
+            for c in range(T):  # stage the cells before the clock starts (the reference's are host objects)
+                g.task(sf.write(chains[c]), *[sf.write(x) for x in extras[c]], device=sf.ops.noop)
+            g.wait_all()
+            owner = {}
+            t0 = time.perf_counter_ns()
+            for i in range(N):
+                for c in range(T):
+                    v = g.task(acc(chains[c]), *[sf.read(x) for x in extras[c]], device=op)
+                    owner[v.task_id] = (c, i)
+            ins = time.perf_counter_ns() - t0
+            g.wait_all()
+            ends = [[0] * N for _ in range(T)]
+            for kind, t, _, tid, _ in g.trace.export_events():
+                if kind == "TaskEnd" and tid in owner:
+                    c, i = owner[tid]
+                    ends[c][i] = t + g._t0  # export_events is relative to the graph's t0
+            out.append(derive_report(t0, ins, ends, D))
+    finally:
+        eng.stop()
+    return _mean_reports(out[1:])
+
+
+def overhead_cpu(T, N, D, mode, deps, reps=2):
+    """The same protocol on the oracle restatement of the reference engine (host
+    worker threads, precise-sleep bodies as in the reference)."""
+    from oracle import stf
+
+    m = stf.WRITE if mode == "write" else stf.COMMUTE
+    out = []
+
+    def precise_sleep(d):  # reference src/bench.py:29-37
+        if d <= 0:
+            return
+        deadline = time.perf_counter() + d
+        if d > 200e-6:
+            time.sleep(d - 150e-6)
+        while time.perf_counter() < deadline:
+            time.sleep(0)
+
+    for _ in range(reps):
+        orc = stf.Oracle(workers=T, trace=False)
+        chains = [[0] for _ in range(T)]
+        extras = [[[0] for _ in range(deps - 1)] for _ in range(T)]
+        ends = [[0] * N for _ in range(T)]
+
+        def body(c, i):
+            row = ends[c]
+
+            def run(*_):
+                precise_sleep(D)
+                row[i] = time.perf_counter_ns()
+            return run
+
+        t0 = time.perf_counter_ns()
+        for i in range(N):
+            for c in range(T):
+                orc.task([(m, chains[c])] + [(stf.READ, x) for x in extras[c]], body=body(c, i))
+        ins = time.perf_counter_ns() - t0
+        orc.wait_all()
+        orc.stop()
+        out.append(derive_report(t0, ins, ends, D))
+    return _mean_reports(out)
+
+
+OVERHEAD_GRID = [(D, mode, 1) for D in (0.0, 1e-4, 1e-3) for mode in ("write", "commute")] + \
+                [(1e-4, mode, deps) for deps in (5, 20) for mode in ("write", "commute")]
+
+
+def overhead_rows(fn, T, N):
+    rows = []
+    for D, mode, deps in OVERHEAD_GRID:
+        r = fn(T, N, D, mode, deps)
+        r.update({"D_s": D, "mode": mode, "deps": deps, "T": T, "N": N})
+        rows.append(r)
+    return rows
+
+
+# ----------------------------------------------------------------- CPU legs
+
+def cpu_baseline(n: int, b: int, seconds: float, steps: int = 1, warmup: int = 0, extra: bool = True,
+                 overhead_n: int = 1000):
     """Reference algorithm on the host: the oracle's restatement of the reference
     STF engine (one worker thread per core) running numpy tile bodies, on the
     first block-rows of the same tiled DGEMM (bounded sample).  One calibration
     pass sizes the sample to about `seconds`; then `warmup` untimed and `steps`
-    timed samples run, and the mean rate of the timed ones is returned."""
+    timed samples run, and the mean rate of the timed ones is returned.  With
+    ``extra``: C1 in full and bounded samples of C3 / C4, plus the reference
+    overhead protocol on the same cores."""
     import numpy as np
     from threadpoolctl import threadpool_limits
 
@@ -201,41 +339,148 @@ def cpu_baseline(n: int, b: int, seconds: float, steps: int = 1, warmup: int = 0
     t0 = time.perf_counter()
     X @ Y
     lib = 2.0 * m ** 3 / (time.perf_counter() - t0) / 1e9
-    return {"value": flops / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "port",
-            "library_ceiling_gflops": lib, "library_ceiling": f"numpy/OpenBLAS {m}^2 FP64 A@B, all host threads",
-            "sample": f"tiled DGEMM {n}/{b}: block-rows 0..{rows - 1} of C ({rows * nt * nt} tasks, "
-                      f"{flops / 1e12:.2f} TFLOP per sample) on the oracle STF engine (restated reference, "
-                      f"{cores} host worker threads, numpy bodies, 1 BLAS thread each); "
-                      f"{len(dts)} timed sample(s), mean",
-            "seconds": dt}
+    out = {"value": flops / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "port",
+           "library_ceiling_gflops": lib, "library_ceiling": f"numpy/OpenBLAS {m}^2 FP64 A@B, all host threads",
+           "sample": f"tiled DGEMM {n}/{b}: block-rows 0..{rows - 1} of C ({rows * nt * nt} tasks, "
+                     f"{flops / 1e12:.2f} TFLOP per sample) on the oracle STF engine (restated reference, "
+                     f"{cores} host worker threads, numpy bodies, 1 BLAS thread each); "
+                     f"{len(dts)} timed sample(s), mean",
+           "seconds": dt}
+    if extra:
+        with threadpool_limits(1):
+            out["configs"] = cpu_configs(cores)
+        out["overhead"] = {"protocol": "reference src/bench.py:67-117 on the oracle engine, host worker threads, "
+                                       "precise-sleep bodies", "runs": overhead_rows(overhead_cpu, cores, overhead_n)}
+    return out
+
+
+def cpu_configs(cores):
+    """C1 in full, and the first panel steps of C3 / the first pair tasks of C4,
+    on the oracle engine with numpy bodies (1 BLAS thread per worker)."""
+    import numpy as np
+
+    from oracle import inputs, programs, stf
+
+    res = {}
+    # C1: DGEMM 2048 / 256, all 512 tasks
+    n, b = 2048, 256
+    objs = programs.gemm_operands(n, b)
+    t0 = time.perf_counter()
+    programs.run_on_oracle(programs.gemm_program(n // b), objs, workers=cores, trace=False).stop()
+    dt = time.perf_counter() - t0
+    res["C1"] = {"gflops": 2.0 * n ** 3 / dt / 1e9, "seconds": dt, "sample": "full (512 tasks)"}
+    # C3: Cholesky 32768 / 1024, panel steps 0..2 (the first 1,488 tasks)
+    n, b, steps = 32768, 1024, 3
+    nt = n // b
+    prog = [t for t in programs.cholesky_program(nt)]
+    cut = []
+    for kind, acc, prio in prog:
+        if kind == "potrf" and acc[0][1][1] >= steps:
+            break
+        cut.append((kind, acc, prio))
+    keys = {key for _, acc, _ in cut for _, key in acc}
+    objs = {key: inputs.spd_tile(3, key[1] * b, key[2] * b, b, b, n) for key in keys}
+    t0 = time.perf_counter()
+    programs.run_on_oracle(cut, objs, workers=cores, trace=False).stop()
+    dt = time.perf_counter() - t0
+    fl = programs.flops(cut, b)
+    res["C3"] = {"gflops": fl / dt / 1e9, "seconds": dt,
+                 "sample": f"panel steps 0..{steps - 1} of C3 ({len(cut)} of 5984 tasks, {fl / 1e12:.2f} TFLOP)"}
+    # C4: particles 2^20 / 256 groups: the first 3 * cores pair tasks
+    per = 4096
+    npairs = 3 * cores
+    P = [inputs.particles(4, g * per, per) for g in range(npairs + 1)]
+    F = [np.zeros((4, per)) for _ in range(npairs + 1)]
+    orc = stf.Oracle(workers=cores, trace=False)
+    from oracle import bodies
+    t0 = time.perf_counter()
+    for j in range(1, npairs + 1):
+        orc.task([(stf.READ, P[0]), (stf.READ, P[j]), (stf.COMMUTE, F[0]), (stf.COMMUTE, F[j])],
+                 body=bodies.p2p_pair)
+    orc.wait_all()
+    dt = time.perf_counter() - t0
+    orc.stop()
+    inter = 2.0 * per * per * npairs
+    res["C4"] = {"interactions_per_s": inter / dt, "seconds": dt,
+                 "sample": f"{npairs} pair tasks of 4096 x 4096 particles (mutual)"}
+    return res
 
 
 def run_reference(args, dist):
+    """The reference arm: the reference algorithm on the host cores (the oracle
+    port of the reference STF engine + numpy bodies), same metric and config as
+    our arm at this N.  Under torchrun only rank 0 runs."""
     if dist.rank != 0:
-        return  # under torchrun only rank 0 runs the CPU reference
-    args.n, args.b = args.n or 16384, args.b or 512
-    # each step is a bounded sample; the whole --steps/--warmup run stays within a few minutes
+        return
+    workload = resolve_workload(args, max(args.gpus, dist.world))
     per_step = max(1.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
-    res = cpu_baseline(args.n, args.b, per_step, steps=args.steps, warmup=args.warmup)
-    nt = args.n // args.b
+    if workload == "gemm":
+        args.n, args.b = args.n or 16384, args.b or 512
+        res = cpu_baseline(args.n, args.b, per_step, steps=args.steps, warmup=args.warmup, extra=False)
+        nt = args.n // args.b
+        cfg = {"workload": f"tiled DGEMM {args.n}x{args.n} fp64, {args.b}x{args.b} tiles (BASELINE configs[1], "
+                           f"C2), {nt ** 3} GEMM tasks per step per GPU", "n": args.n, "b": args.b,
+               "cpu_sample": res["sample"]}
+        value, seconds, sample = res["value"], res["seconds"], res["sample"]
+    else:
+        from threadpoolctl import threadpool_limits
+
+        with threadpool_limits(1):
+            c3 = cpu_configs(os.cpu_count() or 1)["C3"]
+        value, seconds, sample = c3["gflops"], c3["seconds"], c3["sample"]
+        cfg = {"workload": "tiled Cholesky 32768x32768 fp64, 1024x1024 tiles (BASELINE configs[2], C3)",
+               "n": 32768, "b": 1024, "cpu_sample": sample}
+    cores = os.cpu_count() or 1
     line = {
-        "impl": "reference", "metric": METRIC, "value": res["value"], "unit": "GFLOP/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["seconds"] * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"tiled DGEMM {args.n}x{args.n} fp64, {args.b}x{args.b} tiles (BASELINE configs[1], "
-                               f"C2), {nt ** 3} GEMM tasks per step per GPU",
-                   "n": args.n, "b": args.b, "cpu_sample": res["sample"]},
-        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample",
-                                             "library_ceiling_gflops", "library_ceiling")},
-        "e2e": {"value": res["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": seconds * 1e3,
+        "higher_is_better": True, "scaling": "weak" if workload == "gemm" else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------- GPU legs
 
-def main_ours(args, dist):
-    import numpy as np
+def pcie_rates(dev: int):
+    """Pinned host <-> device copy rates (GB/s) with CUDA events, 1 GiB each way."""
+    import torch
+
+    nbytes = 1 << 30
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{dev}")
+    out = {}
+    for name, (dst, src) in (("h2d", (d, h)), ("d2h", (h, d))):
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            dst.copy_(src, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        out[name] = 3 * nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9
+    del h, d
+    return out
+
+
+def gemm_check(g, A, B, C, mult, seed):
+    """Flush A, B, C (read mode: device copies stay) and check sampled C tiles."""
+    for M in (A, B, C):
+        for t in M.tiles.values():
+            g.flush_to_host(t, keep_device=True)
+    g.wait_all()
+    samples = verify.sample_tiles(A.nt, 4, seed=seed)
+    rel, comp = verify.gemm_tile_errors(C.tiles, A.tiles, B.tiles, samples, mult=mult)
+    return {"tiles_checked": len(samples), "max_rel_err": rel, "max_componentwise_err": comp,
+            "tol_rel": verify.GEMM_REL_TOL, "tol_componentwise": verify.GEMM_COMPONENTWISE_TOL,
+            "expected": f"C = {mult:g} * A B", "pass": rel <= verify.GEMM_REL_TOL and
+            comp <= verify.GEMM_COMPONENTWISE_TOL}
+
+
+def main_gemm(args, dist):
     import torch
 
     import paper_2308_15964_b200 as sf
@@ -260,14 +505,11 @@ def main_ours(args, dist):
         alg.insert_gemm(g, A, B, C)
         g.wait_all()
 
-    if os.environ.get("SFX_BENCH_KTIME", "1") == "0":  # diagnostics: the device leg without timing events
-        eng.set_option("kernel_timing", 0)
-
     for _ in range(args.warmup):
         step()
     st0 = eng.stats(0)
-    clocks = ClockSampler(dev)
-    clocks.start()
+    p0 = sf.gemm_paths()
+    clocks = ClockSampler(dev).start()
     times = []
     for _ in range(args.steps):
         dist.barrier()
@@ -280,9 +522,11 @@ def main_ours(args, dist):
         times.append(e0.elapsed_time(e1) / 1e3)
     clk = clocks.stop()
     st1 = eng.stats(0)
+    p1 = sf.gemm_paths()
     step_s = dist.max(statistics.mean(times))
     value = flops * dist.world / step_s / 1e9
     launches = st1["kernel_launches"] - st0["kernel_launches"]
+    check = None if args.no_check else gemm_check(g, A, B, C, float(args.warmup + args.steps), seed=1)
 
     # ---- e2e: host-resident inputs through the public API ----
     def e2e_step():
@@ -290,8 +534,7 @@ def main_ours(args, dist):
         # staggered over 2*nt waves, so C's staging (2 GiB H2D) and its flush
         # (2 GiB D2H) spread over the step instead of piling up in the first and
         # last waves (tools/e2e_probe.py: 25.7 -> 28.3 TFLOP/s)
-        alg.insert_gemm(g, A, B, C, priorities=args.e2e_row_priorities,
-                        skew=args.e2e_skew if args.e2e_skew >= 0 else 2 * nt)
+        alg.insert_gemm(g, A, B, C, skew=args.e2e_skew if args.e2e_skew >= 0 else 2 * nt)
         for t in C.tiles.values():
             g.flush_to_host(t)                      # C back to the host (write-mode flush)
         for M in (A, B):
@@ -308,7 +551,8 @@ def main_ours(args, dist):
     e2e_step()  # first pass moves everything to the host side
     s0 = eng.stats(0)
     et = []
-    for _ in range(max(2, args.steps // 2)):
+    ke = max(2, args.steps // 2)
+    for _ in range(ke):
         dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -318,14 +562,28 @@ def main_ours(args, dist):
         torch.cuda.synchronize()
         et.append(e0.elapsed_time(e1) / 1e3)
     s1 = eng.stats(0)
-    ksteps = len(et)
     e2e_s = dist.max(statistics.mean(et))
-    e2e = {"value": flops * dist.world / e2e_s / 1e9, "unit": "GFLOP/s",
-           "h2d_bytes_per_step": (s1["bytes_to_device"] - s0["bytes_to_device"]) // ksteps,
-           "d2h_bytes_per_step": (s1["bytes_from_device"] - s0["bytes_from_device"]) // ksteps,
-           "ms_per_step": e2e_s * 1e3}
+    h2d = (s1["bytes_to_device"] - s0["bytes_to_device"]) // ke
+    d2h = (s1["bytes_from_device"] - s0["bytes_from_device"]) // ke
+    e2e = {"value": flops * dist.world / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+           "h2d_gbs": h2d / e2e_s / 1e9, "d2h_gbs": d2h / e2e_s / 1e9}
+    if not args.no_check:
+        # the host now holds C = (warmup + steps + 1 + ke) A B (every e2e pass accumulates)
+        samples = verify.sample_tiles(nt, 3, seed=2)
+        rel, comp = verify.gemm_tile_errors(C.tiles, A.tiles, B.tiles, samples,
+                                            mult=float(args.warmup + args.steps + 1 + ke))
+        e2e["check"] = {"tiles_checked": len(samples), "max_rel_err": rel, "max_componentwise_err": comp,
+                        "pass": rel <= verify.GEMM_REL_TOL and comp <= verify.GEMM_COMPONENTWISE_TOL}
     eng.stop()
     del A, B, C
+    try:
+        pc = pcie_rates(dev)
+        e2e["pcie_h2d_gbs"], e2e["pcie_d2h_gbs"] = pc["h2d"], pc["d2h"]
+        e2e["transfer_note"] = ("h2d_gbs / d2h_gbs: bytes moved per e2e step / step time (copies overlap the "
+                                "kernels); pcie_*_gbs: 1 GiB pinned copies alone, CUDA events")
+    except Exception as exc:  # the probe must not hide the line
+        e2e["pcie_error"] = repr(exc)
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "dgemm_traffic.json")
@@ -347,6 +605,7 @@ def main_ours(args, dist):
     busy_ns = st1["busy_ns"] - st0["busy_ns"]
     flop_task = 2.0 * b ** 3
     achieved = tasks * flop_task / (busy_ns * 1e-9) / 1e12 if busy_ns else value / dist.world / 1e3
+    paths = {k: p1[k] - p0[k] for k in p1}
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": achieved / peak_tf, "traffic": traffic,
                 "peak_source": "FP64 DMMA (mma.sync m8n8k4 -> DMMA.8x8x4) peak measured in-run on this GPU "
@@ -358,6 +617,7 @@ def main_ours(args, dist):
                 "launch_avg_us": sum_ns / max(groups, 1) / 1e3,
                 "launch_concurrency": sum_ns / busy_ns if busy_ns else None,
                 "kernel_share_of_step": busy_ns * 1e-9 / (sum(times)) if busy_ns else None,
+                "kernel_paths": paths,
                 "achieved_how": "algorithmic flops of the timed launches / union of their CUDA-event "
                                 "intervals on the launching streams (timed region only)"}
 
@@ -370,7 +630,7 @@ def main_ours(args, dist):
                    "n": n, "b": b, "tasks_per_step": nt ** 3, "streams_per_gpu": args.streams,
                    "group_max": args.group, "scheduler": "prio",
                    "l2": "inputs (6 GiB) larger than L2; no flush", "parallelism": f"replica x{dist.world}"},
-        "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+        "clocks": clk, "check": check, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
         "pct_fp64_peak": 100.0 * value / dist.world / 1e3 / peak_tf,
     }
 
@@ -378,117 +638,67 @@ def main_ours(args, dist):
         line["secondary"] = secondary(sf, alg, dev, args, peak_tf)
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
         try:
-            cb = cpu_baseline(n, b, args.cpu_seconds)
+            cb = cpu_baseline(n, b, args.cpu_seconds, overhead_n=args.overhead_n)
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample",
-                                                       "library_ceiling_gflops", "library_ceiling")}
+                                                       "library_ceiling_gflops", "library_ceiling", "configs",
+                                                       "overhead")}
         except Exception as exc:  # the CPU leg must not hide the GPU line
             line["cpu_baseline"] = {"error": repr(exc)}
     if dist.rank == 0:
         print(json.dumps(line), flush=True)
 
 
-def secondary(sf, alg, dev, args, peak_tf):
+def cholesky_run(sf, alg, ordinals, n, b, streams, group, reps, check, clocks=None):
+    """Factor C3-style SPD matrices ``reps`` times on the given devices from one
+    runtime (block-cyclic when several); returns per-rep seconds, stats and the
+    residual of the last rep."""
     import torch
 
-    out = {}
-    # C3: tiled Cholesky 32768 / 1024 on one GPU
-    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, args.streams), scheduler="prio", trace=False,
-                           ordinals=[dev], group_max=args.chol_group)
-    n, b = 32768, 1024
+    ndev = len(ordinals)
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(ndev, streams), scheduler="prio", trace=False,
+                           ordinals=list(ordinals), group_max=group)
     M = alg.TiledMatrix(n, b, lower=True)
-    g = sf.TaskGraph().compute_on(eng)
-    ts = []
-    for rep in range(3):
-        alg.insert_fill_spd(g, M, 3)
-        g.wait_all()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        alg.insert_cholesky(g, M)
-        g.wait_all()
-        e1.record()
-        torch.cuda.synchronize()
-        if rep:
-            ts.append(e0.elapsed_time(e1) / 1e3)
-    t = statistics.mean(ts)
-    out["cholesky_C3"] = {"n": n, "b": b, "tasks": 5984, "seconds": t, "gflops": alg.flops_cholesky(n) / t / 1e9,
-                          "pct_fp64_peak": 100 * alg.flops_cholesky(n) / t / 1e12 / peak_tf}
-    eng.stop()
-    del M
-    # C4: particles 2^20 in 256 groups, one evaluation
-    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, args.streams), trace=False, ordinals=[dev],
-                           kernel_timing=True)
-    ng, per = 256, 4096
-    P = [sf.pinned_empty((4, per)) for _ in range(ng)]
-    F = [sf.pinned_empty((4, per)) for _ in range(ng)]
-    g = sf.TaskGraph().compute_on(eng)
-    alg.insert_fill_particles(g, P, 4)
-    for f in F:
-        g.task(sf.write(f), device=sf.ops.zero())
-    g.wait_all()
-    ts = []
-    for rep in range(3):
-        torch.cuda.synchronize()
-        s0 = eng.stats(0)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        alg.insert_particles(g, P, F)
-        g.wait_all()
-        e1.record()
-        torch.cuda.synchronize()
-        s1 = eng.stats(0)
-        if rep:
-            ts.append(e0.elapsed_time(e1) / 1e3)
-    t = statistics.mean(ts)
-    inter = alg.interactions(ng * per)
-    dfma_tf = sf.fp64_dfma_peak(dev)
-    # mutual kernel: 23 FP64 instructions per unordered pair = 2 ordered interactions
-    # (csrc/kernels/particles.cu); FP64-pipe bound = (DFMA peak / 2 flop) instr/s / 11.5
-    bound = dfma_tf * 1e12 / 2 / 11.5
-    busy = (s1["busy_ns"] - s0["busy_ns"]) * 1e-9
-    out["particles_C4"] = {"particles": ng * per, "groups": ng, "tasks": 32896, "seconds": t,
-                           "interactions_per_s": inter / t,
-                           "gflops_20flop_convention": inter * alg.FLOP_PER_INTERACTION / t / 1e9,
-                           "roofline": {"bound": "fp64 pipe (DFMA/DMUL/DADD)", "unit": "interactions/s",
-                                        "achieved": inter / busy if busy else None,
-                                        "peak": bound, "frac": inter / busy / bound if busy else None,
-                                        "dfma_peak_tflops": dfma_tf,
-                                        "fp64_instr_per_interaction": 11.5,
-                                        "kernel_share_of_step": busy / t,
-                                        "launches": s1["timed_groups"] - s0["timed_groups"]}}
-    eng.stop()
-    # runtime overhead per task: reference protocol (src/bench.py:67-117): T chains x N
-    # tasks, each task writes (or commutatively writes) its chain cell and runs for D;
-    # O_avg = makespan / N - D per chain step, insertion cost per task
-    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, 4), trace=False, ordinals=[dev])
-    T, N = 4, 2000
-    rows = []
-    for mode in ("write", "commute"):
-        acc = sf.write if mode == "write" else sf.commutative_write
-        for D in (0.0, 10e-6):
-            op = sf.ops.noop if D == 0 else sf.ops.spin(int(D * 1e9))
+    P, Q = alg.grid_shape(ndev)
+    times = []
+    A = None
+    res = None
+    try:
+        s_before = None
+        for rep in range(reps):
             g = sf.TaskGraph().compute_on(eng)
-            cells = [sf.Cell(0) for _ in range(T)]
-            res = []
-            for rep in range(3):
-                t0 = time.perf_counter()
-                for i in range(N):
-                    for c in cells:
-                        g.task(acc(c), device=op)
-                t1 = time.perf_counter()
-                g.wait_all()
-                t2 = time.perf_counter()
-                if rep:
-                    res.append(((t1 - t0) / (T * N), (t2 - t0) / N - D))
-            rows.append({"mode": mode, "D_us": D * 1e6, "T": T, "N": N,
-                         "insert_us_per_task": 1e6 * statistics.mean(r[0] for r in res),
-                         "O_avg_us": 1e6 * statistics.mean(r[1] for r in res),
-                         "O_avg_us_per_task": 1e6 * statistics.mean(r[1] for r in res) / T})
-    out["runtime_overhead"] = {"protocol": "reference src/bench.py:67-117: T chains x N tasks, O_avg = "
-                                           "makespan/N - D (wall clock from first insertion to wait_all), "
-                                           "Python per-task insertion", "runs": rows}
-    eng.stop()
-    return out
+            if ndev > 1:
+                alg.block_cyclic(g, M, P, Q)
+            alg.insert_fill_spd(g, M, 3)
+            if check and rep == reps - 1:
+                g.flush_all(keep_device=True)
+            g.wait_all()
+            if check and rep == reps - 1:
+                A = {ij: t.copy() for ij, t in M.tiles.items()}
+            for o in set(ordinals):
+                torch.cuda.synchronize(o)
+            if rep == 1 and clocks is not None:
+                clocks.start()
+            if rep == reps - 1:
+                s_before = [eng.stats(d) for d in range(ndev)]
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            alg.insert_cholesky(g, M)
+            g.wait_all()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+        stats = [eng.stats(d) for d in range(ndev)]
+        delta = [{k: s1[k] - s0[k] for k in ("bytes_p2p_in", "copies_p2p_in", "tasks_executed", "t_plan_ns",
+                                             "t_issue_ns", "t_complete_ns", "groups")}
+                 for s0, s1 in zip(s_before, stats)]
+        if check:
+            g.flush_all(keep_device=False)
+            g.wait_all()
+            res = verify.cholesky_residual(A, M.tiles, n, b)
+    finally:
+        eng.stop()
+    return times, delta, res
 
 
 def main_cholesky(args, dist):
@@ -508,59 +718,157 @@ def main_cholesky(args, dist):
     if dist.rank != 0:
         dist.barrier()
         return
+    ordinals = [int(x) for x in args.ordinals.split(",")] if args.ordinals else list(range(ndev))
+    if len(ordinals) != ndev:
+        raise SystemExit(f"--ordinals names {len(ordinals)} devices but --gpus is {ndev}")
+    visible = torch.cuda.device_count()
+    if max(ordinals) >= visible:
+        raise SystemExit(f"bench: {ndev} GPUs requested but only {visible} visible (no fallback to fewer GPUs)")
     n, b = args.n or 32768, args.b or 1024
     nt = n // b
-    peak_tf, _ = sf.fp64_peak(0)
-    eng = sf.create_engine(sf.WorkerTeam.of_devices(ndev, args.streams), scheduler="prio", trace=False,
-                           ordinals=list(range(ndev)), group_max=args.chol_group)
-    M = alg.TiledMatrix(n, b, lower=True)
-    P, Q = alg.grid_shape(ndev)
-    times = []
-    clocks = ClockSampler(0)
-    for rep in range(args.warmup + args.steps):
-        g = sf.TaskGraph().compute_on(eng)
-        alg.block_cyclic(g, M, P, Q)
-        alg.insert_fill_spd(g, M, 3)
-        g.wait_all()
-        for d in range(ndev):
-            torch.cuda.synchronize(d)
-        if rep == args.warmup:
-            clocks.start()
-        t0 = time.perf_counter()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        alg.insert_cholesky(g, M)
-        g.wait_all()
-        e1.record()
-        torch.cuda.synchronize()
-        if rep >= args.warmup:
-            times.append(e0.elapsed_time(e1) / 1e3)
-    clk = clocks.stop()
-    stats = [eng.stats(d) for d in range(ndev)]
-    eng.stop()
-    t = statistics.mean(times)
+    peak_tf, _ = sf.fp64_peak(ordinals[0])
     flops = alg.flops_cholesky(n)
+    clocks = ClockSampler(ordinals)
+    times, delta, res = cholesky_run(sf, alg, ordinals, n, b, args.streams, args.chol_group,
+                                     args.warmup + args.steps, not args.no_check, clocks)
+    clk = clocks.stop()
+    t = statistics.mean(times[args.warmup:])
     value = flops / t / 1e9
+    one = None
+    if ndev > 1:
+        # the 1-GPU reference of the scaling curve, measured in the same run
+        t1, _, _ = cholesky_run(sf, alg, [ordinals[0]], n, b, args.streams, args.chol_group, 3, False)
+        one = {"n_gpus": 1, "value": flops / statistics.mean(t1[1:]) / 1e9, "unit": "GFLOP/s",
+               "ms_per_step": 1e3 * statistics.mean(t1[1:])}
     ntasks = nt + nt * (nt - 1) + nt * (nt - 1) * (nt - 2) // 6  # potrf + trsm + syrk + gemm
+    p2p = sum(d["bytes_p2p_in"] for d in delta)
+    tasks = sum(d["tasks_executed"] for d in delta)
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ndev, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic SPD (R+R^T)/2 + n*I, generated on device",
-        "config": {"workload": f"tiled Cholesky {n}x{n} fp64, {b}x{b} tiles, {ndev} GPU(s) from one runtime",
-                   "n": n, "b": b, "tasks": ntasks, "grid": [P, Q], "streams_per_gpu": args.streams,
-                   "parallelism": f"owner-computes 2-D block-cyclic {P}x{Q}, NVLink peer pulls",
-                   "l2": "working set (%.1f GiB) larger than L2" % (len(M.tiles) * b * b * 8 / 2 ** 30)},
+        "config": {"workload": f"tiled Cholesky {n}x{n} fp64, {b}x{b} tiles (BASELINE configs[2], C3), "
+                               f"{ntasks} tasks, {ndev} GPU(s) from one runtime",
+                   "n": n, "b": b, "tasks": ntasks, "grid": list(alg.grid_shape(ndev)),
+                   "ordinals": ordinals, "streams_per_gpu": args.streams,
+                   "parallelism": "owner-computes 2-D block-cyclic, NVLink peer pulls",
+                   "l2": "working set (%.1f GiB) larger than L2" % (nt * (nt + 1) / 2 * b * b * 8 / 2 ** 30)},
         "clocks": clk,
+        "check": None if res is None else {"cholesky_residual": res, "tol": verify.CHOL_RESIDUAL_TOL,
+                                           "pass": res <= verify.CHOL_RESIDUAL_TOL,
+                                           "how": "||A x - L L^T x|| / (||A||_F ||x||), 4 seeded x"},
         "pct_fp64_peak": 100.0 * value / 1e3 / (peak_tf * ndev),
         "roofline": {"bound": "tensor", "achieved": value / 1e3 / ndev, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": value / 1e3 / ndev / peak_tf, "traffic": None,
                      "peak_source": "FP64 DMMA peak measured in-run (sfx_fp64_peak), per GPU"},
-        "p2p_bytes": sum(s["bytes_p2p_in"] for s in stats),
-        "gpu_launches": stats[0]["kernel_launches"],
+        "scaling_reference": one,
+        "p2p": {"bytes_per_step": p2p, "gbs": p2p / t / 1e9,
+                "per_gpu_bytes": [d["bytes_p2p_in"] for d in delta]},
+        "runtime_host_us_per_task": {k: sum(d[k] for d in delta) / 1e3 / max(tasks, 1)
+                                     for k in ("t_plan_ns", "t_issue_ns", "t_complete_ns")},
+        "gpu_launches": None,
     }
     print(json.dumps(line), flush=True)
     dist.barrier()
+
+
+def secondary(sf, alg, dev, args, peak_tf):
+    import torch
+
+    out = {}
+    # C1: DGEMM 2048 / 256 (the oracle-run config) on the GPU, checked
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, 16), scheduler="prio", trace=False, ordinals=[dev])
+    n, b = 2048, 256
+    A, B, C = (alg.TiledMatrix(n, b) for _ in range(3))
+    g = sf.TaskGraph().compute_on(eng)
+    alg.insert_fill_uniform(g, A, 1)
+    alg.insert_fill_uniform(g, B, 2)
+    alg.insert_zero(g, C)
+    g.wait_all()
+    ts = []
+    for rep in range(4):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        alg.insert_gemm(g, A, B, C)
+        g.wait_all()
+        e1.record()
+        torch.cuda.synchronize()
+        if rep:
+            ts.append(e0.elapsed_time(e1) / 1e3)
+    t = statistics.mean(ts)
+    out["dgemm_C1"] = {"n": n, "b": b, "tasks": 512, "seconds": t, "gflops": alg.flops_gemm(n) / t / 1e9,
+                       "check": gemm_check(g, A, B, C, 4.0, seed=4)}
+    eng.stop()
+    del A, B, C
+    # C3: tiled Cholesky 32768 / 1024 on one GPU, residual of the last rep
+    n, b = 32768, 1024
+    times, _, res = cholesky_run(sf, alg, [dev], n, b, args.streams, args.chol_group, 3, True)
+    t = statistics.mean(times[1:])
+    out["cholesky_C3"] = {"n": n, "b": b, "tasks": 5984, "seconds": t, "gflops": alg.flops_cholesky(n) / t / 1e9,
+                          "pct_fp64_peak": 100 * alg.flops_cholesky(n) / t / 1e12 / peak_tf,
+                          "check": {"cholesky_residual": res, "tol": verify.CHOL_RESIDUAL_TOL,
+                                    "pass": res <= verify.CHOL_RESIDUAL_TOL}}
+    # C4: particles 2^20 in 256 groups, one evaluation
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, args.streams), trace=False, ordinals=[dev],
+                           kernel_timing=True)
+    ng, per = 256, 4096
+    P = [sf.pinned_empty((4, per)) for _ in range(ng)]
+    F = [sf.pinned_empty((4, per)) for _ in range(ng)]
+    g = sf.TaskGraph().compute_on(eng)
+    alg.insert_fill_particles(g, P, 4)
+    g.wait_all()
+    ts = []
+    for rep in range(3):
+        for f in F:
+            g.task(sf.write(f), device=sf.ops.zero())
+        g.wait_all()
+        torch.cuda.synchronize()
+        s0 = eng.stats(0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        alg.insert_particles(g, P, F)
+        g.wait_all()
+        e1.record()
+        torch.cuda.synchronize()
+        s1 = eng.stats(0)
+        if rep:
+            ts.append(e0.elapsed_time(e1) / 1e3)
+    t = statistics.mean(ts)
+    for x in P + F:
+        g.flush_to_host(x, keep_device=True)
+    g.wait_all()
+    pot, force = verify.particle_errors(P, F, verify.sample_particles(ng, per, 48))
+    inter = alg.interactions(ng * per)
+    dfma_tf = sf.fp64_dfma_peak(dev)
+    # mutual kernel: 23 FP64 instructions per unordered pair = 2 ordered interactions
+    # (csrc/kernels/particles.cu); FP64-pipe bound = (DFMA peak / 2 flop) instr/s / 11.5
+    bound = dfma_tf * 1e12 / 2 / 11.5
+    busy = (s1["busy_ns"] - s0["busy_ns"]) * 1e-9
+    out["particles_C4"] = {"particles": ng * per, "groups": ng, "tasks": 32896, "seconds": t,
+                           "interactions_per_s": inter / t,
+                           "gflops_20flop_convention": inter * alg.FLOP_PER_INTERACTION / t / 1e9,
+                           "check": {"targets_checked": 48, "pot_rel_err": pot, "force_norm_err": force,
+                                     "pass": pot <= verify.POT_REL_TOL and force <= verify.FORCE_NORM_TOL},
+                           "roofline": {"bound": "fp64 pipe (DFMA/DMUL/DADD)", "unit": "interactions/s",
+                                        "achieved": inter / busy if busy else None,
+                                        "peak": bound, "frac": inter / busy / bound if busy else None,
+                                        "frac_20flop_convention": (inter * alg.FLOP_PER_INTERACTION / busy / 1e12
+                                                                   / dfma_tf) if busy else None,
+                                        "dfma_peak_tflops": dfma_tf,
+                                        "fp64_instr_per_interaction": 11.5,
+                                        "kernel_share_of_step": busy / t,
+                                        "launches": s1["timed_groups"] - s0["timed_groups"]}}
+    eng.stop()
+    # runtime overhead per task: the reference protocol (src/bench.py:67-117)
+    T = os.cpu_count() or 4
+    out["runtime_overhead"] = {
+        "protocol": "reference src/bench.py:67-117: T chains x N tasks, body = D s device spin (no kernel at "
+                    "D = 0), deps-1 extra read cells; O_avg = makespan/N - D, O_max = worst end-to-end gap "
+                    "in a chain - D (end times = CUDA end events on the host clock), Python insertion cost",
+        "runs": overhead_rows(lambda T_, N_, D, mode, deps: overhead_gpu(sf, dev, T_, N_, D, mode, deps),
+                              T, args.overhead_n)}
+    return out
 
 
 def main_particles(args, dist):
@@ -575,9 +883,12 @@ def main_particles(args, dist):
     if dist.rank != 0:
         dist.barrier()
         return
+    ordinals = [int(x) for x in args.ordinals.split(",")] if args.ordinals else list(range(ndev))
+    if max(ordinals) >= torch.cuda.device_count():
+        raise SystemExit(f"bench: {ndev} GPUs requested but only {torch.cuda.device_count()} visible")
     ng, per = 256, 4096
-    dfma_tf = sf.fp64_dfma_peak(0)
-    eng = sf.create_engine(sf.WorkerTeam.of_devices(ndev, args.streams), trace=False, ordinals=list(range(ndev)),
+    dfma_tf = sf.fp64_dfma_peak(ordinals[0])
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(ndev, args.streams), trace=False, ordinals=ordinals,
                            group_max=args.group)
     P = [sf.pinned_empty((4, per)) for _ in range(ng)]
     F = [sf.pinned_empty((4, per)) for _ in range(ng)]
@@ -586,12 +897,12 @@ def main_particles(args, dist):
     g.wait_all()
     parts = None
     times = []
-    clocks = ClockSampler(0)
+    clocks = ClockSampler(ordinals)
     for rep in range(args.warmup + args.steps):
         for f in F:
             g.task(sf.write(f), device=sf.ops.zero())
         g.wait_all()
-        for d in range(ndev):
+        for d in set(ordinals):
             torch.cuda.synchronize(d)
         if rep == args.warmup:
             clocks.start()
@@ -604,6 +915,10 @@ def main_particles(args, dist):
         if rep >= args.warmup:
             times.append(e0.elapsed_time(e1) / 1e3)
     clk = clocks.stop()
+    for x in P + F:
+        g.flush_to_host(x, keep_device=True)
+    g.wait_all()
+    pot, force = verify.particle_errors(P, F, verify.sample_particles(ng, per, 48))
     stats = [eng.stats(d) for d in range(ndev)]
     eng.stop()
     t = statistics.mean(times)
@@ -615,9 +930,12 @@ def main_particles(args, dist):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (positions uniform in the unit cube, charges in [0.5, 1], generated on device)",
         "config": {"workload": f"particles {ng * per} in {ng} groups, 32896 tasks, {ndev} GPU(s) from one runtime",
+                   "ordinals": ordinals,
                    "parallelism": "pair tasks in balanced blocks per GPU, per-GPU partial accumulators, "
                                   "dacc reduction (peer pulls)", "l2": "one evaluation per step"},
         "clocks": clk,
+        "check": {"targets_checked": 48, "pot_rel_err": pot, "force_norm_err": force,
+                  "pass": pot <= verify.POT_REL_TOL and force <= verify.FORCE_NORM_TOL},
         "roofline": {"bound": "fp64 pipe", "achieved": inter / t, "peak": bound, "unit": "interactions/s",
                      "frac": inter / t / bound, "dfma_peak_tflops_per_gpu": dfma_tf},
         "p2p_bytes": sum(s["bytes_p2p_in"] for s in stats),
@@ -627,6 +945,12 @@ def main_particles(args, dist):
     dist.barrier()
 
 
+def resolve_workload(args, ngpus):
+    if args.workload != "auto":
+        return args.workload
+    return "gemm" if ngpus == 1 else "cholesky"
+
+
 def main():
     args = parse()
     dist = Dist()
@@ -634,13 +958,17 @@ def main():
         run_reference(args, dist)
         return
     dist.init("nccl")
-    if args.workload == "cholesky":
+    workload = resolve_workload(args, max(args.gpus, dist.world))
+    if workload == "cholesky":
         main_cholesky(args, dist)
-    elif args.workload == "particles":
+    elif workload == "particles":
         main_particles(args, dist)
     else:
+        if args.gpus > 1 and dist.world == 1:
+            raise SystemExit("bench: --workload gemm runs one C2 replica per rank; launch it with torchrun "
+                             "for several GPUs (no silent fallback to one GPU)")
         args.n, args.b = args.n or 16384, args.b or 512
-        main_ours(args, dist)
+        main_gemm(args, dist)
     dist.done()
 
 

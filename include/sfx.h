@@ -55,6 +55,10 @@ extern "C" {
 #define SFX_ERR_DUPLICATE (-7)     /* DuplicateAccessError (errors.py:16-17)        */
 #define SFX_ERR_REGISTRATION (-8)  /* RegistrationError (errors.py:8-9)             */
 #define SFX_ERR_UNSUPPORTED (-9)   /* op needs a CUDA device (sim backend)          */
+#define SFX_ERR_NUMERIC (-10)      /* a tile body reported a numerical failure (DPOTRF:
+                                      non-positive pivot, LAPACK info > 0); the cause
+                                      of an engine failure, like the LinAlgError the
+                                      oracle's np.linalg.cholesky raises              */
 
 /* ---- access modes (access.py:16-21) ---- */
 #define SFX_READ 0
@@ -94,6 +98,10 @@ extern "C" {
                                   device copies dropped), then the task is handed out by
                                   sfx_extern_poll and finished by sfx_extern_done, which
                                   releases its successors                              */
+#define SFX_OP_FAULT 7         /* failure injection for the engine-failure tests: iparam[0] = 0
+                                  an invalid launch configuration (the launch itself fails,
+                                  non-sticky), 1 a device-side trap (sticky: the CUDA context
+                                  is lost; run it in a throw-away process)             */
 #define SFX_OP_ADD_I64 5       /* every operand (int64 cells): += iparam[0] with device
                                   atomics.  Like P2P_PAIR/P2P_SELF it accumulates
                                   atomically, so its commutative members of one group run
@@ -251,6 +259,24 @@ int sfx_fp64_peak(int ordinal, double* tflops, double* sm_mhz);
 /* FP64 pipe (DFMA, 2 flop per FMA) throughput microbenchmark: the roofline
  * denominator of the particle kernel, whose work is DFMA/DMUL/DADD */
 int sfx_fp64_dfma_peak(int ordinal, double* tflops);
+
+/* DGEMM launch-path counters (process-wide, since load): which configuration of
+ * the grouped DMMA kernel ran.  out[k] for k < n, n <= SFX_GEMM_PATHS.  Parity
+ * tests use them to prove they exercised the benchmarked path (C-prefetch,
+ * several output tiles per persistent CTA, no split-K). */
+#define SFX_GEMM_LAUNCHES 0          /* grouped launches                                    */
+#define SFX_GEMM_TASKS 1             /* tile tasks carried by them                          */
+#define SFX_GEMM_WORK_ITEMS 2        /* (task, output tile, k-slice) work items             */
+#define SFX_GEMM_CPREF 3             /* launches with the TMA C-prefetch epilogue           */
+#define SFX_GEMM_MULTI_TILE 4        /* launches with >= 2 output tiles per persistent CTA  */
+#define SFX_GEMM_CPREF_MULTI_TILE 5  /* both: the C2 headline configuration                 */
+#define SFX_GEMM_SPLITK 6            /* split-K launches (FP64 atomic epilogue)             */
+#define SFX_GEMM_TRI 7               /* TRI-masked launches (full-inverse TRSM)             */
+#define SFX_GEMM_LOWER 8             /* lower-triangle launches (DSYRK)                     */
+#define SFX_GEMM_NN 9                /* B stored K x N                                      */
+#define SFX_GEMM_NT 10               /* B stored N x K (Cholesky update, DSYRK)             */
+#define SFX_GEMM_PATHS 11
+int sfx_gemm_paths(uint64_t* out, uint32_t n);
 
 #ifdef __cplusplus
 }

@@ -9,6 +9,8 @@ from __future__ import annotations
 import ctypes
 import os
 
+import numpy as np
+
 from .errors import (
     ConfigurationError,
     DuplicateAccessError,
@@ -32,6 +34,7 @@ ERR_INTERNAL = -6
 ERR_DUPLICATE = -7
 ERR_REGISTRATION = -8
 ERR_UNSUPPORTED = -9
+ERR_NUMERIC = -10
 
 READ, WRITE, ATOMIC_WRITE, COMMUTATIVE_WRITE, MAYBE_WRITE = 0, 1, 2, 3, 4
 
@@ -50,6 +53,7 @@ OP_CELL = 2
 OP_BYTES_ADD = 3
 OP_FLUSH = 4
 OP_EXTERN = 6
+OP_FAULT = 7
 OP_ADD_I64 = 5
 OP_DGEMM = 10
 OP_DSYRK = 11
@@ -144,6 +148,7 @@ def _load():
         "sfx_extern_poll": ([P, ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), ctypes.c_double],
                             ctypes.c_int),
         "sfx_extern_done": ([P, ctypes.c_uint64, ctypes.c_int, ctypes.c_char_p], ctypes.c_int),
+        "sfx_gemm_paths": ([P, u32], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -160,7 +165,17 @@ EXPORTED = ("sfx_abi_version", "sfx_device_count", "sfx_create", "sfx_destroy", 
             "sfx_submit", "sfx_pause", "sfx_resume", "sfx_wait_all", "sfx_wait_task",
             "sfx_task_state", "sfx_flush", "sfx_stats", "sfx_resident", "sfx_block_state",
             "sfx_trace", "sfx_edges", "sfx_violations", "sfx_set_option", "sfx_host_alloc", "sfx_host_free",
-            "sfx_fp64_peak", "sfx_fp64_dfma_peak", "sfx_extern_poll", "sfx_extern_done")
+            "sfx_fp64_peak", "sfx_fp64_dfma_peak", "sfx_extern_poll", "sfx_extern_done", "sfx_gemm_paths")
+
+GEMM_PATH_NAMES = ("launches", "tasks", "work_items", "cpref", "multi_tile", "cpref_multi_tile", "splitk", "tri",
+                   "lower", "nn", "nt")
+
+
+def gemm_paths() -> dict:
+    """Process-wide DGEMM launch-path counters (sfx_gemm_paths)."""
+    buf = (ctypes.c_uint64 * len(GEMM_PATH_NAMES))()
+    lib.sfx_gemm_paths(buf, len(GEMM_PATH_NAMES))
+    return dict(zip(GEMM_PATH_NAMES, list(buf)))
 
 _ERRORS = {
     ERR_CONFIG: ConfigurationError,
@@ -178,6 +193,17 @@ class CudaError(SeqflowError):
 
 
 _ERRORS[ERR_CUDA] = CudaError
+
+
+class NotPositiveDefiniteError(SeqflowError, np.linalg.LinAlgError):
+    """A DPOTRF tile had a non-positive leading minor (LAPACK info > 0).
+
+    Also a ``numpy.linalg.LinAlgError``: the oracle's body (np.linalg.cholesky)
+    raises that class, so the ``__cause__`` of the EngineFailedError has the same
+    type on both paths (reference engine.py:154-157, 227-243)."""
+
+
+_ERRORS[ERR_NUMERIC] = NotPositiveDefiniteError
 
 
 def error_for(code: int, msg: str) -> Exception:

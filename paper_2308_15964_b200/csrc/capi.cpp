@@ -250,4 +250,10 @@ int sfx_fp64_dfma_peak(int ordinal, double* tflops) {
   return SFX_OK;
 }
 
+int sfx_gemm_paths(uint64_t* out, uint32_t n) {
+  if (!out) return SFX_ERR_CONFIG;
+  for (uint32_t k = 0; k < n && k < SFX_GEMM_PATHS; ++k) out[k] = sfx::g_gemm_paths[k].load();
+  return SFX_OK;
+}
+
 }  // extern "C"

@@ -225,16 +225,28 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
             }
           }
         }
-        if (h == 1) {  // operands are in registers: the slot may be refilled (one arrive per warp)
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&empty[s]);
-        }
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
+        for (int e = 0; e < 2; ++e) {
 #pragma unroll
           for (int i = 0; i < 8; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i][e], b[j][e]);
+          if (h == 1 && e == 0) {
+            // Release the stage (one arrive per warp) only once every shared load
+            // this warp issued from it has COMPLETED.  An mbarrier arrive does not
+            // wait for in-flight ld.shared results: arriving right after the last
+            // load let the producer's next TMA overwrite rows the warp had not read
+            // yet (round 1: rows 56-63 of C tiles = the last A fragment, wrong by
+            // ~1e-4 relative, only with 2 output tiles per CTA where the producer
+            // runs ahead into the next tile; tools/c2_check.py).  The fence makes
+            // each lane wait for its outstanding loads (MEMBAR.ALL.CTA), __syncwarp
+            // orders the lanes before lane 0 arrives.  Placed after the first half
+            // of this k-step's DMMAs, which need those registers anyway.
+            ptx::fence_cta();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&empty[s]);
+          }
+        }
       }
     }
 
@@ -409,6 +421,28 @@ bool make_tmap_f64_2d(CUtensorMap* tm, const double* base, uint64_t inner, uint6
 
 namespace {
 
+}  // namespace
+
+// launch-configuration counters (sfx_gemm_paths): which kernel path ran, so the
+// parity tests can prove that they exercised the benchmarked configuration
+std::atomic<unsigned long long> g_gemm_paths[SFX_GEMM_PATHS];
+
+namespace {
+
+void count_gemm_path(bool cpref, int per, int ksplit, bool tri, bool lower, bool trans_b, int ntasks, int total) {
+  auto add = [](int k, unsigned long long v) { g_gemm_paths[k].fetch_add(v, std::memory_order_relaxed); };
+  add(SFX_GEMM_LAUNCHES, 1);
+  add(SFX_GEMM_TASKS, static_cast<unsigned long long>(ntasks));
+  add(SFX_GEMM_WORK_ITEMS, static_cast<unsigned long long>(total));
+  if (cpref) add(SFX_GEMM_CPREF, 1);
+  if (per >= 2) add(SFX_GEMM_MULTI_TILE, 1);
+  if (cpref && per >= 2) add(SFX_GEMM_CPREF_MULTI_TILE, 1);
+  if (ksplit > 1) add(SFX_GEMM_SPLITK, 1);
+  if (tri) add(SFX_GEMM_TRI, 1);
+  if (lower) add(SFX_GEMM_LOWER, 1);
+  if (trans_b) add(SFX_GEMM_NT, 1); else add(SFX_GEMM_NN, 1);
+}
+
 int num_sms() {
   static int n[64] = {};
   int dev = 0;
@@ -488,6 +522,7 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
   const int per = tiles_per_cta(total, K);
   const int grid = (total + per - 1) / per;
   count_launch();
+  count_gemm_path(p.cpref != 0, per, p.ksplit, TRI, lower, TB, n, total);
   dgemm_dmma_kernel<TB, G, TRI><<<grid, THREADS, SMEM_BYTES, stream>>>(p);
   return cudaGetLastError();
 }

@@ -69,9 +69,11 @@ __global__ void __launch_bounds__(LEAF) trsm_leaf_kernel(double* B, long long ld
 // each owning a 4x4 block of the lower triangle in registers (outer-product
 // form, column scaling deferred).  Column j is broadcast through a
 // double-buffered shared vector: one barrier and <= 16 FMAs per thread per step.
-__global__ void __launch_bounds__(256) potrf_leaf_kernel(double* A, long long lda, int n, int* info) {
+__global__ void __launch_bounds__(256) potrf_leaf_kernel(double* A, long long lda, int n, int* info, int off) {
   __shared__ double colbuf[2][LEAF];
   __shared__ double pivs[LEAF];
+  __shared__ int first_bad;
+  if (threadIdx.x == 0) first_bad = LEAF + 1;
   const int tid = threadIdx.x;
   const int ti = tid >> 4, tk = tid & 15;
   const int R = ti * 4, C = tk * 4;
@@ -114,9 +116,12 @@ __global__ void __launch_bounds__(256) potrf_leaf_kernel(double* A, long long ld
     }
   }
   __syncthreads();
-  if (tid < LEAF && !(pivs[tid] > 0.0) && tid < n) {
-    if (info) atomicCAS(info, 0, tid + 1);
-  }
+  if (tid < LEAF && tid < n && !(pivs[tid] > 0.0)) atomicMin(&first_bad, tid + 1);
+  __syncthreads();
+  // info (mapped host word): leaves run in column order on one stream, so the first
+  // failing leaf stores first; LAPACK info = order of the first non-positive minor
+  if (tid == 0 && info && first_bad <= LEAF && *reinterpret_cast<volatile int*>(info) == 0)
+    *reinterpret_cast<volatile int*>(info) = off + first_bad;
   if (!active) return;
 #pragma unroll
   for (int r = 0; r < 4; ++r)
@@ -151,15 +156,15 @@ cudaError_t launch_dtrsm(const double* L, long long ldl, double* B, long long ld
   return launch_dtrsm(L + n1 * ldl + n1, ldl, B + n1, ldb, M, n2, s);
 }
 
-cudaError_t launch_dpotrf(double* A, long long lda, int n, int* info, cudaStream_t s) {
+cudaError_t launch_dpotrf(double* A, long long lda, int n, int* info, cudaStream_t s, int off) {
   if (n <= 0) return cudaSuccess;
   if (n <= LEAF) {
     count_launch();
-    potrf_leaf_kernel<<<1, 256, 0, s>>>(A, lda, n, info);
+    potrf_leaf_kernel<<<1, 256, 0, s>>>(A, lda, n, info, off);
     return cudaGetLastError();
   }
   const int n1 = split(n), n2 = n - n1;
-  cudaError_t e = launch_dpotrf(A, lda, n1, info, s);
+  cudaError_t e = launch_dpotrf(A, lda, n1, info, s, off);
   if (e) return e;
   // A21 <- A21 * L11^-T
   e = launch_dtrsm(A, lda, A + n1 * lda, lda, n2, n1, s);
@@ -167,7 +172,7 @@ cudaError_t launch_dpotrf(double* A, long long lda, int n, int* info, cudaStream
   // A22 -= A21 A21^T (lower)
   e = launch_dgemm(A + n1 * lda, lda, A + n1 * lda, lda, A + n1 * lda + n1, lda, n2, n2, n1, -1.0, 1.0, true, true, s);
   if (e) return e;
-  return launch_dpotrf(A + n1 * lda + n1, lda, n2, info, s);
+  return launch_dpotrf(A + n1 * lda + n1, lda, n2, info, s, off + n1);
 }
 
 }  // namespace sfx

@@ -163,11 +163,11 @@ __device__ __forceinline__ void warp_potrf_inv16(double (*c)[P], int o, double (
   double r[16], rinv[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) r[k] = (k <= i) ? c[o + i][o + k] : 0.0;
-  bool ok = true;
+  int first_bad = 0;  // 1-based pivot index of the first non-positive pivot (warp-uniform)
 #pragma unroll 16
   for (int j = 0; j < 16; ++j) {
     const double d = __shfl_sync(0xffffffffu, r[j], j);  // pivot (Schur complement) from lane j
-    ok &= d > 0.0;
+    if (!(d > 0.0) && first_bad == 0) first_bad = j + 1;
     const double rs = rsqrt_refined(d);
     rinv[j] = rs;
     // scale column j below the diagonal, then the rank-1 update of the trailing rows.
@@ -185,7 +185,7 @@ __device__ __forceinline__ void warp_potrf_inv16(double (*c)[P], int o, double (
       }
     }
   }
-  if (!ok && lane == 0) *bad = 1;
+  if (first_bad && lane == 0 && *bad == 0) *bad = o + first_bad;  // 1-based column in the 64-block
   if (lane < 16) {
 #pragma unroll
     for (int k = 0; k < 16; ++k)
@@ -367,7 +367,10 @@ __device__ void factor_block(Smem& s, double* A, long long lda, int kb, double* 
   load_N(s.c, Akk, lda);
   __syncthreads();
   const bool ok = factor64(s);
-  if (!ok && tid == 0 && info) atomicCAS(info, 0, kb * T + 1);
+  // info (mapped host word, see Backend::status_alloc): only CTA 0 factors diagonal
+  // blocks, in order, so the first failing block is the first to store
+  if (!ok && tid == 0 && info && *reinterpret_cast<volatile int*>(info) == 0)
+    *reinterpret_cast<volatile int*>(info) = kb * T + s.bad;
   for (int e = tid; e < T * T; e += THREADS) {  // L back, original upper triangle kept
     const int i = e >> 6, k = e & 63;
     if (k <= i) Akk[i * lda + k] = s.c[i][k];

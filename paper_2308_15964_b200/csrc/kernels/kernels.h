@@ -6,11 +6,15 @@
 
 #include <atomic>
 
+#include "sfx.h"
+
 namespace sfx {
 
 // every kernel launch issued by the runtime's ops (evidence for gpu_launches)
 extern std::atomic<unsigned long long> g_kernel_launches;
 inline void count_launch() { g_kernel_launches.fetch_add(1, std::memory_order_relaxed); }
+// DGEMM launch-path counters (SFX_GEMM_* in sfx.h)
+extern std::atomic<unsigned long long> g_gemm_paths[];
 
 bool make_tmap_f64_2d(CUtensorMap* tm, const double* base, uint64_t inner, uint64_t outer, uint64_t ld,
                       uint32_t box_inner, uint32_t box_outer, bool swizzle128);
@@ -67,7 +71,9 @@ cudaError_t launch_dtrsm_coop_group(const TrsmDesc* d, int ntasks, int M, int n,
                                     cudaStream_t s);
 
 cudaError_t launch_dtrsm(const double* L, long long ldl, double* B, long long ldb, int M, int n, cudaStream_t s);
-cudaError_t launch_dpotrf(double* A, long long lda, int n, int* info, cudaStream_t s);
+// info: if non-null, receives the 1-based order of the first non-positive leading
+// minor (LAPACK dpotrf info) unless it is already non-zero; `off` = column offset
+cudaError_t launch_dpotrf(double* A, long long lda, int n, int* info, cudaStream_t s, int off = 0);
 struct P2PDesc {
   const double* Pi;
   long long ldpi;
@@ -92,6 +98,8 @@ cudaError_t launch_fill_spd(double* a, long long rows, long long cols, long long
 cudaError_t launch_fill_particles(double* p, long long n, long long ld, long long seed, long long first,
                                   cudaStream_t s);
 cudaError_t launch_spin(long long ns, cudaStream_t s);
+// failure injection (SFX_OP_FAULT): 0 = invalid launch configuration, 1 = device trap
+cudaError_t launch_fault(int kind, cudaStream_t s);
 // A += sum of n addends (FP64 rows x cols, each with its own ld), n <= 7
 cudaError_t launch_dacc(double* a, long long lda, long long rows, long long cols, const double* const* add,
                         const long long* ld, int n, cudaStream_t s);

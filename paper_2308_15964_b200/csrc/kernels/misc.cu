@@ -230,6 +230,19 @@ cudaError_t launch_add_i64(long long* const* cells, int n, long long delta, cuda
   return cudaGetLastError();
 }
 
+__global__ void fault_kernel(int kind) {
+  if (kind == 1) __trap();
+}
+
+cudaError_t launch_fault(int kind, cudaStream_t s) {
+  count_launch();
+  if (kind == 0)
+    fault_kernel<<<1, 4096, 0, s>>>(0);  // > 1024 threads per block: cudaErrorInvalidConfiguration
+  else
+    fault_kernel<<<1, 32, 0, s>>>(1);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_spin(long long ns, cudaStream_t s) {
   count_launch();
   spin_kernel<<<1, 32, 0, s>>>(ns);

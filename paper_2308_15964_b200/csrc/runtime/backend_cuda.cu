@@ -34,7 +34,12 @@ class CudaBackend : public Backend {
     std::vector<Ev*> pool_timing, pool_plain;
     cudaEvent_t base = nullptr;
     int64_t base_ns = 0;
-    int* info = nullptr;
+    bool base_shared = false;  // base event owned by an earlier logical device on the same GPU
+    // status words (DPOTRF info) in mapped pinned host memory: kernels store into
+    // them directly, the completion thread reads them after the end event
+    int* status = nullptr;
+    int* status_dev = nullptr;
+    std::vector<int> status_free;
     bool ready = false;
     std::vector<void*> scratch;  // per stream (cooperative streams only)
     // per stream, allocated on first use (stream-ordered): TRSM with the full
@@ -63,6 +68,8 @@ class CudaBackend : public Backend {
     return D.tscratch[stream];
   }
   static constexpr size_t kScratchBytes = 64ull << 20;  // >= fullinv_workspace_bytes(2048) = 42 MiB
+  static constexpr int kStatusSlots = 4096;
+  int* status_ptr(int d, int slot) { return slot >= 0 ? devs_[d]->status_dev + slot : nullptr; }
 
  public:
   CudaBackend(int ndev, const int* ordinals) : devs_(ndev) {
@@ -97,9 +104,14 @@ class CudaBackend : public Backend {
     e = cudaMalloc(&D.arena, bytes);
     if (e) return cuda_err(e, "arena cudaMalloc", err);
     D.cap = bytes;
-    e = cudaMalloc(&D.info, sizeof(int));
-    if (e) return cuda_err(e, "cudaMalloc info", err);
-    cudaMemset(D.info, 0, sizeof(int));
+    e = cudaHostAlloc(reinterpret_cast<void**>(&D.status), kStatusSlots * sizeof(int),
+                      cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e) return cuda_err(e, "cudaHostAlloc status words", err);
+    memset(D.status, 0, kStatusSlots * sizeof(int));
+    e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&D.status_dev), D.status, 0);
+    if (e) return cuda_err(e, "cudaHostGetDevicePointer", err);
+    D.status_free.clear();
+    for (int k = kStatusSlots; k-- > 0;) D.status_free.push_back(k);
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
     const int total = nstreams + nurgent + ncoop + nprefetch;
@@ -127,7 +139,17 @@ class CudaBackend : public Backend {
       }
       cudaGetLastError();
     }
-    // timestamp calibration: host CLOCK_MONOTONIC of the base event
+    // timestamp calibration: host CLOCK_MONOTONIC of the base event.  Logical
+    // devices on the same GPU share the first one's base (one device clock), so
+    // their timestamps compare exactly (violations() uses no slack for them)
+    for (int o = 0; o < d; ++o)
+      if (devs_[o]->ordinal == D.ordinal && devs_[o]->base) {
+        D.base = devs_[o]->base;
+        D.base_ns = devs_[o]->base_ns;
+        D.base_shared = true;
+        D.ready = true;
+        return cuda_err(cudaGetLastError(), "device init", err);
+      }
     e = cudaEventCreate(&D.base);
     if (e) return cuda_err(e, "cudaEventCreate", err);
     cudaEventRecord(D.base, D.streams[0]);
@@ -151,6 +173,7 @@ class CudaBackend : public Backend {
   }
 
   void bind_thread(int d) override { cudaSetDevice(devs_[d]->ordinal); }
+  bool same_clock(int a, int b) const override { return devs_[a]->ordinal == devs_[b]->ordinal; }
   uint64_t arena_capacity(int d) override { return devs_[d]->cap; }
   void* arena_ptr(int d, uint64_t off) override { return devs_[d]->arena + off; }
 
@@ -225,10 +248,28 @@ class CudaBackend : public Backend {
                     "peer copy", err);
   }
   uint64_t kernel_launches() const override { return g_kernel_launches.load(); }
+  int status_alloc(int d) override {
+    Dev& D = *devs_[d];
+    std::lock_guard<std::mutex> g(D.pool_mu);
+    if (D.status_free.empty()) return -1;
+    const int k = D.status_free.back();
+    D.status_free.pop_back();
+    return k;
+  }
+  int status_take(int d, int slot) override {
+    Dev& D = *devs_[d];
+    std::lock_guard<std::mutex> g(D.pool_mu);
+    volatile int* w = D.status + slot;
+    const int v = *w;
+    *w = 0;
+    D.status_free.push_back(slot);
+    return v;
+  }
   bool supports(uint32_t op) const override {
     switch (op) {
       case SFX_OP_NOOP:
       case SFX_OP_SPIN:
+      case SFX_OP_FAULT:
       case SFX_OP_CELL:
       case SFX_OP_BYTES_ADD:
       case SFX_OP_ADD_I64:
@@ -259,6 +300,9 @@ class CudaBackend : public Backend {
     switch (op.op) {
       case SFX_OP_SPIN:
         e = launch_spin(op.ip[0], s);
+        break;
+      case SFX_OP_FAULT:
+        e = launch_fault(static_cast<int>(op.ip[0]), s);
         break;
       case SFX_OP_ZERO:
         e = cudaMemsetAsync(o[0].dptr, 0, o[0].bytes, s);
@@ -330,16 +374,18 @@ class CudaBackend : public Backend {
                            static_cast<int>(o[1].cols), s);
         }
         break;
-      case SFX_OP_DPOTRF:
+      case SFX_OP_DPOTRF: {
+        int* info = status_ptr(d, op.status_slot);
         if (op.ip[0] == 2 && devs_[d]->scratch[stream] && fullinv_supported(static_cast<int>(o[0].rows)))
-          e = launch_dpotrf_fullinv(f64(o[0]), o[0].ld, static_cast<int>(o[0].rows), devs_[d]->info,
-                                    devs_[d]->scratch[stream], kScratchBytes, s);
+          e = launch_dpotrf_fullinv(f64(o[0]), o[0].ld, static_cast<int>(o[0].rows), info, devs_[d]->scratch[stream],
+                                    kScratchBytes, s);
         else if (devs_[d]->scratch[stream] && coop_supported(static_cast<int>(o[0].rows), static_cast<int>(o[0].rows)))
-          e = launch_dpotrf_coop(f64(o[0]), o[0].ld, static_cast<int>(o[0].rows), devs_[d]->info,
-                                 devs_[d]->scratch[stream], s, op.ip[0] != 0);
+          e = launch_dpotrf_coop(f64(o[0]), o[0].ld, static_cast<int>(o[0].rows), info, devs_[d]->scratch[stream], s,
+                                 op.ip[0] != 0);
         else
-          e = launch_dpotrf(f64(o[0]), o[0].ld, static_cast<int>(o[0].rows), devs_[d]->info, s);
+          e = launch_dpotrf(f64(o[0]), o[0].ld, static_cast<int>(o[0].rows), info, s);
         break;
+      }
       case SFX_OP_P2P_PAIR:
         e = launch_p2p(f64(o[0]), o[0].ld, static_cast<int>(o[0].cols), f64(o[1]), o[1].ld, static_cast<int>(o[1].cols),
                        f64(o[2]), o[2].ld, f64(o[3]), o[3].ld, false, op.fp[0], s);
@@ -439,11 +485,12 @@ class CudaBackend : public Backend {
       }
       D.pool_timing.clear();
       D.pool_plain.clear();
-      if (D.base) cudaEventDestroy(D.base);
+      if (D.base && !D.base_shared) cudaEventDestroy(D.base);
       for (auto st : D.streams) cudaStreamDestroy(st);
       D.streams.clear();
       if (D.arena) cudaFree(D.arena);
-      if (D.info) cudaFree(D.info);
+      if (D.status) cudaFreeHost(D.status);
+      D.status = nullptr;
       for (void* p : D.scratch)
         if (p) cudaFree(p);
       D.scratch.clear();

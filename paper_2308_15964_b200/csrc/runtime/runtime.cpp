@@ -310,6 +310,7 @@ int Runtime::validate(const sfx_task_desc& d, const sfx_access* acc, std::string
   switch (d.op) {
     case SFX_OP_NOOP:
     case SFX_OP_SPIN:
+    case SFX_OP_FAULT:
       return 0;
     case SFX_OP_CELL:
       if (d.n_access < 1 || d.n_access > 8) {
@@ -492,10 +493,23 @@ int Runtime::submit(uint32_t n, const sfx_task_desc* descs, const sfx_access* ac
     t->acc.reserve(d.n_access);
     for (uint32_t k = 0; k < d.n_access; ++k) bind(t, handles_[acc[ai + k].hid], acc[ai + k].mode);
     ai += d.n_access;
-    for (auto& a : t->acc)
-      if (a.mode == SFX_COMMUTATIVE_WRITE) t->commute.push_back(a.h);
-    std::sort(t->commute.begin(), t->commute.end(), [](const Handle* x, const Handle* y) { return x->hid < y->hid; });
-    t->commute_shared = accumulates_atomically(t->op);
+    // guards: commutative handles (exclusive, or shared for ops that accumulate with
+    // device atomics); with several devices also atomic handles, in shared mode:
+    // atomic members of one slot run concurrently only on ONE device -- members
+    // placed elsewhere wait for them to complete and then pull the result (a
+    // serial order of atomic updates is one the atomic semantics allow)
+    std::vector<std::pair<Handle*, uint8_t>> guards;
+    for (auto& a : t->acc) {
+      if (a.mode == SFX_COMMUTATIVE_WRITE)
+        guards.emplace_back(a.h, accumulates_atomically(t->op) ? 1 : 0);
+      else if (a.mode == SFX_ATOMIC_WRITE && ndev_ > 1)
+        guards.emplace_back(a.h, 1);
+    }
+    std::sort(guards.begin(), guards.end(), [](const auto& x, const auto& y) { return x.first->hid < y.first->hid; });
+    for (auto& gp : guards) {
+      t->commute.push_back(gp.first);
+      t->commute_sh.push_back(gp.second);
+    }
     Graph* g = graphs_[d.graph].get();
     g->tasks.push_back(t);
     g->inserted += 1;
@@ -528,7 +542,6 @@ int Runtime::flush(uint32_t gid, uint64_t tid, uint64_t hid, int write_mode) {
 
 int Runtime::place(Task* t) {
   if (ndev_ == 1) return 0;
-  if (t->hint >= 0) return t->hint % ndev_;
   if (t->op == SFX_OP_FLUSH || t->op == SFX_OP_EXTERN) {
     Handle* h = t->acc[0].h;
     if (h->dirty_dev >= 0) return h->dirty_dev;
@@ -536,16 +549,25 @@ int Runtime::place(Task* t) {
       if (h->blocks[e] && h->blocks[e]->valid) return e;
     return 0;
   }
-  // concurrent atomic/commutative members share the device of their group
-  for (auto& a : t->acc)
-    if ((a.mode == SFX_ATOMIC_WRITE || a.mode == SFX_COMMUTATIVE_WRITE) && a.h->group_dev >= 0) return a.h->group_dev;
+  auto grouped = [](uint32_t m) { return m == SFX_ATOMIC_WRITE || m == SFX_COMMUTATIVE_WRITE; };
   int chosen = -1;
-  // owner computes: the device holding the freshest copy of a written tile
+  // members of an active atomic/commutative group follow the group's device (it
+  // overrides a hint): concurrent members must share one device copy.  Members
+  // that still end up elsewhere (a task joining two groups on different devices)
+  // are serialised by the shared guards of acquire_commute.
   for (auto& a : t->acc)
-    if (mode_writes(a.mode) && a.h->dirty_dev >= 0) {
-      chosen = a.h->dirty_dev;
+    if (grouped(a.mode) && a.h->group_dev >= 0) {
+      chosen = a.h->group_dev;
       break;
     }
+  if (chosen < 0 && t->hint >= 0) chosen = t->hint % ndev_;
+  // owner computes: the device holding the freshest copy of a written tile
+  if (chosen < 0)
+    for (auto& a : t->acc)
+      if (mode_writes(a.mode) && a.h->dirty_dev >= 0) {
+        chosen = a.h->dirty_dev;
+        break;
+      }
   if (chosen < 0)
     for (auto& a : t->acc)
       if (mode_writes(a.mode) && a.h->home >= 0) {
@@ -569,7 +591,7 @@ int Runtime::place(Task* t) {
     }
   }
   for (auto& a : t->acc)
-    if (a.mode == SFX_ATOMIC_WRITE || a.mode == SFX_COMMUTATIVE_WRITE) a.h->group_dev = chosen;
+    if (grouped(a.mode) && a.h->group_dev < 0) a.h->group_dev = chosen;
   return chosen;
 }
 
@@ -1023,7 +1045,7 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
     b->dirty = true;
     h->dirty_dev = d;
     h->host_valid = false;
-    if (m == SFX_COMMUTATIVE_WRITE && !t->commute_shared) h->commute_last = t->end;
+    if (m == SFX_COMMUTATIVE_WRITE && !accumulates_atomically(t->op)) h->commute_last = t->end;
     if (m == SFX_WRITE || m == SFX_MAYBE_WRITE) b->ready = t->end;
   }
 
@@ -1036,6 +1058,8 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
   }
   op.op = t->op;
   op.n = static_cast<int>(std::min<size_t>(t->acc.size(), 8));
+  if (t->op == SFX_OP_DPOTRF && t->status_slot < 0) t->status_slot = be_->status_alloc(d);
+  op.status_slot = t->status_slot;
   for (int k = 0; k < op.n; ++k) {
     Handle* h = t->acc[k].h;
     op.o[k].dptr = be_->arena_ptr(d, blocks[k]->off);
@@ -1148,13 +1172,14 @@ bool Runtime::same_signature(const Task* a, const Task* b) const {
 
 bool Runtime::acquire_commute(Task* t) {
   // all-or-nothing in hid order; on failure the task parks on the busy handle.
-  // Shared mode (the op accumulates into its commutative operands with device
-  // atomics, so any interleaving is one of the orders commutativity allows):
-  // members of a group run concurrently as long as they are on the same device
-  // and no exclusive member holds the handle.
+  // Shared mode (the op accumulates into the handle with device atomics, or an
+  // atomic_write access, so any interleaving is one of the orders the semantics
+  // allow): members run concurrently as long as they are on the same device and
+  // no exclusive member holds the handle.
   if (t->guards_held) return true;  // acquired when a release handed the handle over
-  for (Handle* h : t->commute) {
-    const bool busy = t->commute_shared
+  for (size_t k = 0; k < t->commute.size(); ++k) {
+    Handle* h = t->commute[k];
+    const bool busy = t->commute_sh[k]
                           ? (h->commute_owner != nullptr || (h->shared_users > 0 && h->shared_dev != t->dev))
                           : ((h->commute_owner && h->commute_owner != t) || h->shared_users > 0);
     if (busy) {
@@ -1162,8 +1187,9 @@ bool Runtime::acquire_commute(Task* t) {
       return false;
     }
   }
-  for (Handle* h : t->commute) {
-    if (t->commute_shared) {
+  for (size_t k = 0; k < t->commute.size(); ++k) {
+    Handle* h = t->commute[k];
+    if (t->commute_sh[k]) {
       h->shared_users += 1;
       h->shared_dev = t->dev;
     } else {
@@ -1174,11 +1200,18 @@ bool Runtime::acquire_commute(Task* t) {
   return true;
 }
 
+static bool shared_on(const Task* t, const Handle* h) {
+  for (size_t k = 0; k < t->commute.size(); ++k)
+    if (t->commute[k] == h) return t->commute_sh[k] != 0;
+  return false;
+}
+
 void Runtime::release_commute(Task* t) {
   if (!t->guards_held) return;
   t->guards_held = false;
-  for (Handle* h : t->commute) {
-    if (t->commute_shared) {
+  for (size_t k = 0; k < t->commute.size(); ++k) {
+    Handle* h = t->commute[k];
+    if (t->commute_sh[k]) {
       if (--h->shared_users > 0) continue;
       h->shared_dev = -1;
     } else {
@@ -1198,7 +1231,7 @@ void Runtime::release_commute(Task* t) {
       h->commute_waiters.pop_front();
       if (acquire_commute(w)) {
         push_ready(w, -1);
-        if (!w->commute_shared) break;
+        if (!shared_on(w, h)) break;
         continue;
       }
       if (!h->commute_waiters.empty() && h->commute_waiters.back() == w) break;  // h itself is taken again
@@ -1208,12 +1241,12 @@ void Runtime::release_commute(Task* t) {
 
 bool Runtime::commute_conflict(const std::vector<Task*>& group, const Task* t) const {
   // members of one commutative group must never run concurrently on the same
-  // handle -- unless all of them accumulate atomically (shared guard)
-  for (const Access& a : t->acc) {
-    if (a.mode != SFX_COMMUTATIVE_WRITE) continue;
+  // handle -- unless both take it in shared mode
+  for (size_t k = 0; k < t->commute.size(); ++k) {
+    const Handle* h = t->commute[k];
     for (const Task* g : group)
-      for (const Access& b : g->acc)
-        if (b.h == a.h && !(t->commute_shared && g->commute_shared)) return true;
+      for (size_t j = 0; j < g->commute.size(); ++j)
+        if (g->commute[j] == h && !(t->commute_sh[k] && g->commute_sh[j])) return true;
   }
   return false;
 }
@@ -1237,6 +1270,14 @@ void Runtime::complete(Task* t) {
   t->pinned.clear();
   t->copy_syncs.clear();
   t->waits.clear();
+  if (t->status_slot >= 0) {
+    // engine.py:227-243: a failing body poisons the engine; the cause names the task
+    const int info = be_->status_take(t->dev, t->status_slot);
+    t->status_slot = -1;
+    if (info != 0)
+      poison(SFX_ERR_NUMERIC, fmt("dpotrf (task %llu): the leading minor of order %d is not positive definite",
+                                  (unsigned long long)t->tid, info));
+  }
   Graph* g = graphs_[t->gid].get();
   if (ktime_ && t->start && t->end) {
     D.stats.timed_tasks += 1;
@@ -1839,7 +1880,9 @@ int Runtime::violations(uint64_t* n) {
         for (Task* b : h->slots[i + 1].tasks) {
           if (a->state != SFX_STATE_FINISHED || b->state != SFX_STATE_FINISHED) continue;
           if (!a->t_end || !b->t_start) continue;
-          const int64_t slack = (a->dev == b->dev) ? 0 : 20000;  // cross-device clock calibration
+          // devices on one GPU share one clock: no slack; across GPUs the host-side
+          // calibration of each device's base event is good to a few microseconds
+          const int64_t slack = be_->same_clock(a->dev, b->dev) ? 0 : 20000;
           if (b->t_start + slack < a->t_end) ++bad;
         }
   }

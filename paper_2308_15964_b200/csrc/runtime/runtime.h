@@ -143,10 +143,15 @@ struct Task {
   std::vector<Block*> pinned;     // unpinned at completion
   std::vector<SyncP> copy_syncs;  // copies issued on this task's stream
   int64_t t_push = 0, t_pop = 0, t_start = 0, t_end = 0;
-  std::vector<Handle*> commute;  // commutative handles sorted by hid (graph.py:150-157)
-  bool commute_shared = false;   // op accumulates with device atomics: guard in shared mode
+  // guarded handles sorted by hid (graph.py:150-157): its commutative handles, and on
+  // a multi-device runtime its atomic ones; commute_sh[k]: guard k in shared mode
+  // (members run concurrently on ONE device: an op that accumulates with device
+  // atomics, or any atomic_write member)
+  std::vector<Handle*> commute;
+  std::vector<uint8_t> commute_sh;
   bool guards_held = false;      // its commutative guards are acquired (idempotent acquire)
   bool detached = false;         // SFX_OP_EXTERN handed to the host agent: stream slots freed
+  int status_slot = -1;          // device-written status word (DPOTRF info), read at completion
 };
 
 struct Operand {
@@ -159,6 +164,7 @@ struct Operand {
 struct OpLaunch {
   uint32_t op = 0;
   int n = 0;
+  int status_slot = -1;  // Backend::status_alloc slot the kernel reports into (DPOTRF info)
   Operand o[8];
   double fp[4];
   int64_t ip[4];
@@ -183,6 +189,8 @@ class Backend {
   virtual int init_device(int d, int ordinal, int nstreams, int nurgent, int ncoop, int nprefetch,
                           uint64_t arena_bytes, std::string& err) = 0;
   virtual void bind_thread(int d) = 0;
+  // timestamps of devices a and b come from one clock (same physical GPU)
+  virtual bool same_clock(int a, int b) const { return a == b; }
   virtual uint64_t arena_capacity(int d) = 0;
   virtual void* arena_ptr(int d, uint64_t off) = 0;
   virtual void* event_create(int d, bool timing) = 0;
@@ -208,6 +216,12 @@ class Backend {
     return 0;
   }
   virtual bool supports(uint32_t op) const = 0;
+  // status words written by kernels (DPOTRF info: 0 = success, else the 1-based
+  // order of the first non-positive leading minor); host-visible once the
+  // launching task's end event completed.  -1: none available (sim)
+  virtual int status_alloc(int) { return -1; }
+  // read the word, reset it to 0 and return the slot to the pool
+  virtual int status_take(int, int) { return 0; }
   // kernels launched so far by this process's ops (0 for the simulator)
   virtual uint64_t kernel_launches() const { return 0; }
   virtual void shutdown() = 0;

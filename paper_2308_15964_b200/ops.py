@@ -131,6 +131,13 @@ def add_i64(delta: int) -> Op:
     return Op("add_i64", N.OP_ADD_I64, iparam=(int(delta),))
 
 
+def fault(kind: str = "launch") -> Op:
+    """Failure injection (engine-failure tests): ``"launch"`` = a kernel launch with an
+    invalid configuration (the launch fails; the CUDA context survives), ``"trap"`` = a
+    device-side trap (sticky: the process's CUDA context is lost)."""
+    return Op(f"fault_{kind}", N.OP_FAULT, iparam=({"launch": 0, "trap": 1}[kind],))
+
+
 noop = Op("noop", N.OP_NOOP)
 gemm_nn = dgemm(1.0, 1.0, False)
 gemm_nt_sub = dgemm(-1.0, 1.0, True)

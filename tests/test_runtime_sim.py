@@ -513,3 +513,59 @@ def test_shared_commutative_guard_mixed_with_exclusive_members(devices, streams)
     finally:
         eng.stop()
     assert [c.value for c in cells] == want
+
+
+def _submit_with_hints(g, op, cells_per_task, hints, mode=sf.AccessMode.ATOMIC_WRITE):
+    import numpy as np
+
+    n = len(cells_per_task)
+    k = len(cells_per_task[0])
+    hids = np.array([[g.hid_of(c) for c in row] for row in cells_per_task], np.uint64).reshape(-1)
+    return g.submit_arrays(np.full(n, op.code, np.uint32), np.tile(np.array(op.fparam), (n, 1)),
+                           np.tile(np.array(op.iparam, np.int64), (n, 1)), np.zeros(n, np.int32),
+                           np.full(n, k, np.uint32), hids, np.full(n * k, mode.code, np.uint32),
+                           devices=np.asarray(hints, np.int32))
+
+
+def test_atomic_group_members_share_one_device_despite_hints():
+    """members of one atomic slot run concurrently, so they must share
+    one device copy.  The group's device (set by its first member) overrides
+    later members' hints and the tiles' homes."""
+    eng = sim_engine(2, 2)
+    try:
+        g = sf.TaskGraph().compute_on(eng)
+        c = sf.Cell(0)
+        g.place(c, 1)
+        _submit_with_hints(g, sf.ops.add_i64(1), [[c]] * 40, [0, 1] * 20)
+        g.flush_to_host(c)
+        assert g.wait_all(timeout=30)
+        assert c.value == 40
+        assert eng.stats(0)["tasks_executed"] >= 40 and eng.stats(1)["tasks_executed"] == 0
+    finally:
+        eng.stop()
+
+
+def test_atomic_members_joining_two_device_groups_serialise():
+    """A member whose atomic handles belong to groups on different devices runs
+    under the shared guards (never concurrently with the other device's members);
+    the result equals the serial sum."""
+    rng = random.Random(3)
+    eng = sim_engine(2, 3)
+    try:
+        g = sf.TaskGraph().compute_on(eng)
+        cells = [sf.Cell(0) for _ in range(4)]
+        want = [0] * 4
+        rows, hints = [], []
+        for _ in range(400):
+            i, j = rng.sample(range(4), 2)
+            rows.append([cells[i], cells[j]])
+            hints.append(rng.randrange(2))
+            want[i] += 2
+            want[j] += 2
+        _submit_with_hints(g, sf.ops.add_i64(2), rows, hints)
+        for c in cells:
+            g.flush_to_host(c)
+        assert g.wait_all(timeout=30)
+        assert [c.value for c in cells] == want
+    finally:
+        eng.stop()
