@@ -664,10 +664,10 @@ def cholesky_run(sf, alg, ordinals, n, b, streams, group, reps, check, clocks=No
     res = None
     try:
         s_before = None
+        g = sf.TaskGraph().compute_on(eng)  # one graph: the tiles keep their handles across reps
+        if ndev > 1:
+            alg.block_cyclic(g, M, P, Q)
         for rep in range(reps):
-            g = sf.TaskGraph().compute_on(eng)
-            if ndev > 1:
-                alg.block_cyclic(g, M, P, Q)
             alg.insert_fill_spd(g, M, 3)
             if check and rep == reps - 1:
                 g.flush_all(keep_device=True)

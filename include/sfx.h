@@ -249,6 +249,10 @@ int sfx_set_option(sfx_runtime* rt, const char* key, int64_t value);
  * reports it with sfx_extern_done (status != 0 poisons the engine with msg). */
 int sfx_extern_poll(sfx_runtime* rt, uint64_t* tids, uint64_t cap, uint64_t* n, double timeout_s);
 int sfx_extern_done(sfx_runtime* rt, uint64_t tid, int status, const char* msg);
+/* an external agent's failure after its task already finished (a send whose
+ * payload was staged and released before the transfer): poisons the engine with
+ * msg (engine.py:227-243, first failure wins) */
+int sfx_fail(sfx_runtime* rt, const char* msg);
 
 /* pinned host memory (cudaHostAlloc; aligned malloc in sim) for tiles */
 int sfx_host_alloc(uint64_t bytes, int sim, void** out);

@@ -49,7 +49,14 @@ class TiledMatrix:
             t[...] = value
         return self
 
-    def to_dense(self, lower_only: bool = False) -> np.ndarray:
+    def to_dense(self, lower_only=None) -> np.ndarray:
+        """Dense copy of the host tiles.  ``lower_only`` (default: True for a lower
+        matrix) keeps only the lower triangle of the diagonal tiles: after
+        ``insert_cholesky`` with the default full-inverse POTRF their strict upper
+        triangle holds inv(L)^T (a by-product the TRSMs read), where the reference
+        program leaves the input there (LAPACK 'L' semantics for the lower part)."""
+        if lower_only is None:
+            lower_only = self.lower
         n, b = self.n, self.b
         out = np.zeros((n, n))
         for (i, j), t in self.tiles.items():
@@ -259,6 +266,12 @@ def fullinv_tile(b: int) -> bool:
 def insert_cholesky(graph, A: TiledMatrix, fast: bool = True, priorities="auto",
                     inverse_blocks="auto"):
     """In-place right-looking tiled Cholesky of the lower tiles of A (A = L L^T).
+
+    The diagonal tiles' strict upper triangle: with the default full-inverse POTRF
+    it receives inv(L)^T (a by-product the TRSMs read); ``inverse_blocks=False``
+    leaves it untouched like the reference's LAPACK-'L' program.  The factor L
+    (the lower tiles and the diagonal tiles' lower triangle) is the same in every
+    mode; ``TiledMatrix.to_dense()`` returns only L for lower matrices.
 
     ``inverse_blocks``: True = POTRF also leaves the inverses of its 64x64
     diagonal blocks in the diagonal tile's upper triangle and every TRSM runs as

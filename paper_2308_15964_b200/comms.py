@@ -138,11 +138,22 @@ class CommAgent:
 
     # -- transfers (two-part message, reference comms.py:415-427) --------------
     @staticmethod
-    def _transfer(op: _Op) -> None:
+    def _stage(op: _Op):
+        """A private copy of a send's payload (the task's buffer is free after it)."""
+        import torch
+
+        payload = torch.from_numpy(payload_view(op.obj)).clone()
+        if payload.numel() > op.comm.max_message_size:
+            raise CommProtocolError(f"message of {payload.numel()} bytes exceeds the limit "
+                                    f"{op.comm.max_message_size}")
+        return payload
+
+    @staticmethod
+    def _transfer(op: _Op, staged=None) -> None:
         import torch
 
         dist, comm = op.comm.dist, op.comm
-        payload = torch.from_numpy(payload_view(op.obj))
+        payload = staged if staged is not None else torch.from_numpy(payload_view(op.obj))
         nbytes = payload.numel()
         if op.kind in ("send", "bcast_root"):
             if nbytes > comm.max_message_size:
@@ -178,13 +189,29 @@ class CommAgent:
                     return
                 op = q[0]
             try:
-                self._transfer(op)
-                if not self._stop:  # the runtime is gone once its engine stopped
-                    N.lib.sfx_extern_done(h, op.tid, 0, None)
+                if op.kind in ("send", "bcast_root"):
+                    # a send completes as soon as it is posted (reference comms.py:
+                    # universe.put, then _complete): the payload is staged and the task
+                    # finishes -- releasing its READ access -- before the transfer,
+                    # which may wait for the peer's matching receive.  Otherwise a
+                    # send(X) followed by recv(X) on both ranks would deadlock: each
+                    # recv waits for its own send, each send for the peer's recv.
+                    staged = self._stage(op)
+                    if not self._stop:
+                        N.lib.sfx_extern_done(h, op.tid, 0, None)
+                    self._transfer(op, staged)
+                else:
+                    self._transfer(op)
+                    if not self._stop:  # the runtime is gone once its engine stopped
+                        N.lib.sfx_extern_done(h, op.tid, 0, None)
             except Exception as exc:  # noqa: BLE001 -- reported through the engine
                 self.error = exc
                 if not self._stop:
-                    N.lib.sfx_extern_done(h, op.tid, 1, f"{type(exc).__name__}: {exc}".encode())
+                    msg = f"{type(exc).__name__}: {exc}".encode()
+                    if op.kind in ("send", "bcast_root"):
+                        N.lib.sfx_fail(h, msg)  # the task already finished: poison directly
+                    else:
+                        N.lib.sfx_extern_done(h, op.tid, 1, msg)
             with self._lock:
                 q.popleft()
 

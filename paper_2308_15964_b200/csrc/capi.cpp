@@ -161,6 +161,10 @@ int sfx_extern_done(sfx_runtime* r, uint64_t tid, int status, const char* msg) {
   return guarded(r, [&](sfx::Runtime& rt) { return rt.extern_done(tid, status, msg); });
 }
 
+int sfx_fail(sfx_runtime* r, const char* msg) {
+  return guarded(r, [&](sfx::Runtime& rt) { return rt.fail(msg ? msg : "external agent failed"); });
+}
+
 int sfx_resident(sfx_runtime* r, int dev, uint64_t* hids, uint64_t cap, uint64_t* n) {
   return guarded(r, [&](sfx::Runtime& rt) { return rt.resident(dev, hids, cap, n); });
 }

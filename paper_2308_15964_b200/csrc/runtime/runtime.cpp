@@ -173,6 +173,44 @@ int Runtime::reg(uint32_t gid, uint64_t hid, void* host, uint64_t bytes, int64_t
     last_error = fmt("handle %llu is already registered", (unsigned long long)hid);
     return SFX_ERR_REGISTRATION;
   }
+  // One host buffer, one live handle across graphs.  The reference registry is
+  // per graph (graph.py:35) and its device arenas key blocks by hid, so the same
+  // object in two graphs has two device copies; with device caches that outlive
+  // a graph's work, an old graph's dirty copy written back later would clobber
+  // what the new graph staged.  The older handle is retired here: its dirty copy
+  // is written home and its blocks dropped, and the old graph can no longer use
+  // it.  If it still has pending accesses the registration fails instead (wait
+  // for the old graph first).  Handles of the SAME graph may overlap (array
+  // views and their whole object, reference access.py:103-129).
+  if (host && bytes) {
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(host), hi = lo + bytes;
+    std::vector<Handle*> olds;
+    for (auto it = host_ranges_.lower_bound(hi); it != host_ranges_.begin();) {
+      --it;
+      if (it->first + max_handle_bytes_ <= lo) break;
+      Handle* o = it->second;
+      if (it->first + o->bytes > lo && o->gid != gid) olds.push_back(o);
+    }
+    for (Handle* o : olds) {
+      bool busy = o->active < o->slots.size();
+      for (Block* b : o->blocks) busy = busy || (b && b->pins > 0);
+      if (busy) {
+        last_error = fmt("the object's memory is still in use by graph %u (pending accesses): wait for that graph "
+                         "before registering the object in another graph", o->gid);
+        return SFX_ERR_REGISTRATION;
+      }
+    }
+    for (Handle* o : olds) {
+      int rc = retire_blocks(o);
+      if (rc) return rc;
+      o->superseded = true;
+      for (auto it = host_ranges_.begin(); it != host_ranges_.end(); ++it)
+        if (it->second == o) {
+          host_ranges_.erase(it);
+          break;
+        }
+    }
+  }
   auto h = std::make_unique<Handle>();
   h->hid = hid;
   h->gid = gid;
@@ -184,6 +222,10 @@ int Runtime::reg(uint32_t gid, uint64_t hid, void* host, uint64_t bytes, int64_t
   h->dtype = dtype;
   h->blocks.assign(ndev_, nullptr);
   handles_[hid] = h.get();
+  if (host && bytes) {
+    host_ranges_.emplace(reinterpret_cast<uintptr_t>(host), h.get());
+    max_handle_bytes_ = std::max(max_handle_bytes_, bytes);
+  }
   git->second->handles.push_back(h.get());
   handle_store_.push_back(std::move(h));
   return SFX_OK;
@@ -200,26 +242,11 @@ int Runtime::set_home(uint64_t hid, int dev) {
   return SFX_OK;
 }
 
-int Runtime::unreg(uint64_t hid) {
-  std::unique_lock<std::mutex> lk(mu_);
-  auto it = handles_.find(hid);
-  if (it == handles_.end()) {
-    last_error = "object is not registered";
-    return SFX_ERR_REGISTRATION;
-  }
-  Handle* h = it->second;
-  if (h->active < h->slots.size()) {
-    // handles.py:179-182
-    last_error = "cannot unregister an object with pending accesses";
-    return SFX_ERR_REGISTRATION;
-  }
+int Runtime::retire_blocks(Handle* h) {
+  // caller holds mu_ and checked that no block is pinned
   for (int d = 0; d < ndev_; ++d) {
     Block* b = h->blocks[d];
     if (!b) continue;
-    if (b->pins > 0) {
-      last_error = "cannot unregister an object still in use on a device";
-      return SFX_ERR_REGISTRATION;
-    }
     if (b->dirty) {
       // synchronous write-back: the host object is the only copy left afterwards
       std::string err;
@@ -241,6 +268,34 @@ int Runtime::unreg(uint64_t hid) {
     }
     drop_block(b, false, nullptr, 0);
   }
+  return SFX_OK;
+}
+
+int Runtime::unreg(uint64_t hid) {
+  std::unique_lock<std::mutex> lk(mu_);
+  auto it = handles_.find(hid);
+  if (it == handles_.end()) {
+    last_error = "object is not registered";
+    return SFX_ERR_REGISTRATION;
+  }
+  Handle* h = it->second;
+  if (h->active < h->slots.size()) {
+    // handles.py:179-182
+    last_error = "cannot unregister an object with pending accesses";
+    return SFX_ERR_REGISTRATION;
+  }
+  for (Block* b : h->blocks)
+    if (b && b->pins > 0) {
+      last_error = "cannot unregister an object still in use on a device";
+      return SFX_ERR_REGISTRATION;
+    }
+  int rc = retire_blocks(h);
+  if (rc) return rc;
+  for (auto r = host_ranges_.begin(); r != host_ranges_.end(); ++r)
+    if (r->second == h) {
+      host_ranges_.erase(r);
+      break;
+    }
   handles_.erase(it);
   return SFX_OK;
 }
@@ -286,6 +341,11 @@ int Runtime::validate(const sfx_task_desc& d, const sfx_access* acc, std::string
       return SFX_ERR_CONFIG;
     }
     hs[k] = it->second;
+    if (hs[k]->superseded) {
+      err = fmt("handle %llu: its object was registered by another graph since (one live registration per host "
+                "buffer); register it again in this graph", (unsigned long long)acc[k].hid);
+      return SFX_ERR_REGISTRATION;
+    }
     for (uint32_t j = 0; j < k; ++j)
       if (hs[j] == hs[k]) {
         err = "task declares the same object twice";  // graph.py:134-137
@@ -1364,6 +1424,12 @@ int Runtime::extern_done(uint64_t tid, int status, const char* msg) {
   }
   release(t);
   complete(t);
+  return SFX_OK;
+}
+
+int Runtime::fail(const std::string& msg) {
+  std::unique_lock<std::mutex> lk(mu_);
+  poison(SFX_ERR_ENGINE_FAILED, msg);
   return SFX_OK;
 }
 

@@ -118,6 +118,7 @@ struct Handle {
   int shared_dev = -1;
   int group_dev = -1;   // device of the active atomic/commutative group
   int home = -1;        // owner hint (2-D block-cyclic distribution)
+  bool superseded = false;  // its host memory was registered by another graph (see reg)
 };
 
 struct Access {
@@ -296,6 +297,7 @@ class Runtime {
   int stats(int dev, sfx_dev_stats* out);
   int extern_poll(uint64_t* tids, uint64_t cap, uint64_t* n, double timeout_s);
   int extern_done(uint64_t tid, int status, const char* msg);
+  int fail(const std::string& msg);
   int resident(int dev, uint64_t* hids, uint64_t cap, uint64_t* n);
   int block_state(uint64_t hid, int dev, int32_t* st, int32_t* host_valid);
   int trace(uint32_t gid, sfx_event* buf, uint64_t cap, uint64_t* n);
@@ -308,6 +310,7 @@ class Runtime {
 
  private:
   int validate(const sfx_task_desc& d, const sfx_access* acc, std::string& err);
+  int retire_blocks(Handle* h);  // write dirty copies home (synchronously), drop every block
   void bind(Task* t, Handle* h, uint32_t mode);
   void push_ready(Task* t, int wid);
   int place(Task* t);
@@ -366,6 +369,9 @@ class Runtime {
   void extern_handoff(Task* t);
   std::vector<std::unique_ptr<Device>> devs_;
   std::unordered_map<uint64_t, Handle*> handles_;
+  // live handles by host start address (cross-graph aliasing check in reg)
+  std::multimap<uintptr_t, Handle*> host_ranges_;
+  uint64_t max_handle_bytes_ = 0;
   std::vector<std::unique_ptr<Handle>> handle_store_;
   std::unordered_map<uint32_t, std::unique_ptr<Graph>> graphs_;
   std::unordered_map<uint64_t, Task*> tasks_by_tid_;

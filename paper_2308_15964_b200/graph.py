@@ -91,12 +91,25 @@ _STATE = {0: TaskState.INSERTED, 1: TaskState.READY, 2: TaskState.EXECUTING, 3: 
 
 
 class _Entry:
-    __slots__ = ("hid", "obj", "desc")
+    __slots__ = ("hid", "obj", "desc", "parent")
 
-    def __init__(self, hid, obj, desc):
+    def __init__(self, hid, obj, desc, parent=None):
         self.hid = hid
         self.obj = obj
         self.desc = desc
+        self.parent = parent  # array-view element: the array it belongs to (kept alive)
+
+
+def _element_of(buf, index):
+    """The device operand of element ``index`` of an array view (access.py)."""
+    if isinstance(buf, np.ndarray):
+        if not -buf.shape[0] <= index < buf.shape[0]:
+            raise IndexError(f"array view index {index} out of range")
+        return buf[index:index + 1] if buf.ndim == 1 else buf[index]
+    if isinstance(buf, (list, tuple)):
+        return buf[index]
+    raise ConfigurationError(
+        f"array views need a numpy array or a list of device-movable objects, got {type(buf).__name__}")
 
 
 class TaskViewer:
@@ -230,15 +243,26 @@ class TaskGraph:
         return self
 
     # -- registration (graph.py:68-73, handles.py:140-182) --------------------
-    def _register(self, obj) -> _Entry:
+    def _register(self, obj, key=None, parent=None) -> _Entry:
         desc = memory.describe(obj)
         hid = _next_hid()
         N.check(N.lib.sfx_register(self._h, self._gid, hid, desc.ptr, desc.nbytes, desc.rows, desc.cols,
                                    desc.ld, desc.dtype), self._h)
-        e = _Entry(hid, obj, desc)
-        self._entries[id(obj)] = e
+        e = _Entry(hid, obj, desc, parent)
+        self._entries[id(obj) if key is None else key] = e
         self._by_hid[hid] = e
         return e
+
+    def element_hid(self, buf, index) -> int:
+        """Handle of element ``index`` of ``buf`` (an array-view access), registered
+        on first use under the identity (buf, index) -- reference graph.py:140-148."""
+        key = (id(buf), int(index))
+        e = self._entries.get(key)
+        if e is None:
+            if self.engine is None:
+                raise ConfigurationError("attach the graph to an engine before inserting")
+            e = self._register(_element_of(buf, int(index)), key=key, parent=buf)
+        return e.hid
 
     def register(self, obj, nbytes: int = 0):
         if self.engine is None:
@@ -294,14 +318,21 @@ class TaskGraph:
             if spec.__class__ is not AccessSpec:
                 if not isinstance(spec, AccessSpec):
                     raise ConfigurationError(f"accesses must be built with the access helpers, got {spec!r}")
-            if spec.view is not None:
-                raise ConfigurationError("array-view accesses are host-task constructs (oracle only)")
+            code = _MODE_CODE[spec.mode]
+            if spec.view is not None:  # one handle per selected element (graph.py:140-148)
+                for element in spec.view:
+                    hid = self.element_hid(spec.obj, element)
+                    if hid in hids:
+                        raise DuplicateAccessError(f"task declares element {element} twice")
+                    hids.append(hid)
+                    modes.append(code)
+                continue
             e = entries.get(id(spec.obj))
             hid = e.hid if e is not None else self.hid_of(spec.obj)
             if hid in hids:
                 raise DuplicateAccessError(f"task declares {type(spec.obj).__name__} twice")
             hids.append(hid)
-            modes.append(_MODE_CODE[spec.mode])
+            modes.append(code)
         with _id_lock:  # _reserve_tids swaps the counter under this lock
             tid = next(_tid_counter)
         if name is not None:
@@ -445,15 +476,15 @@ class TaskGraph:
         return True
 
     # -- device flush (graph.py:258-260) -----------------------------------------
-    def flush_to_host(self, obj, keep_device: bool = False) -> TaskViewer:
-        """Insert a flush of ``obj`` to its host buffer.
+    def flush_to_host(self, obj, keep_device: bool = False, element=None) -> TaskViewer:
+        """Insert a flush of ``obj`` (or of its array-view ``element``) to its host buffer.
 
         Default = the reference's semantics: a host write, so every device copy
         is dropped afterwards.  ``keep_device=True`` only cleans the dirty copy
         (read-mode flush) and keeps device copies valid.
         """
         self._flush_batch()
-        hid = self.hid_of(obj)
+        hid = self.hid_of(obj) if element is None else self.element_hid(obj, element)
         tid = _next_tid()
         self._names[tid] = "flush"
         self._tids.append(tid)
@@ -461,8 +492,11 @@ class TaskGraph:
         return TaskViewer(self, tid)
 
     def flush_all(self, keep_device: bool = True) -> None:
-        for e in list(self._entries.values()):
-            self.flush_to_host(e.obj, keep_device=keep_device)
+        for key, e in list(self._entries.items()):
+            if isinstance(key, tuple):
+                self.flush_to_host(e.parent, keep_device=keep_device, element=key[1])
+            else:
+                self.flush_to_host(e.obj, keep_device=keep_device)
 
     # -- export -----------------------------------------------------------------
     def _label(self, tid) -> str:

@@ -76,7 +76,16 @@ try:
         except sf.EngineFailedError as exc:
             out["mismatch"] = type(exc.__cause__).__name__
     g2.engine.stop()
-    # 6. insertion validation
+    # 6. ADVICE r1: send(X) then recv(X) on the SAME buffer on both ranks (a swap):
+    #    sends complete once posted (payload staged), so the recv behind each
+    #    send can run and the exchange does not deadlock
+    sw = np.full(6, float(10 + rank))
+    g.send(sw, dest=1 - rank, tag=6)
+    g.recv(sw, src=1 - rank, tag=6)
+    g.task(sf.write(sw), device=sf.ops.noop)
+    assert g.wait_all(timeout=30)
+    out["swap"] = float(sw[0])
+    # 7. insertion validation
     errs = []
     for kw in ({"dest": 5, "tag": 0}, {"dest": 1 - rank, "tag": -1}, {"dest": 1 - rank, "tag": 1 << 30}):
         try:

@@ -81,6 +81,7 @@ def test_comm_tasks_between_two_processes():
         assert out[rank]["bcast"] == 777
         assert out[rank]["validation"] == ["config", "config", "config", "serialization"]
     assert out[1]["fifo"] == [1, 2, 3]
+    assert out[0]["swap"] == 11.0 and out[1]["swap"] == 10.0
     assert out[1]["mismatch"] == "CommProtocolError"
 
 

@@ -569,3 +569,88 @@ def test_atomic_members_joining_two_device_groups_serialise():
         assert [c.value for c in cells] == want
     finally:
         eng.stop()
+
+
+def test_random_programs_on_array_elements_match_reference(random_programs):
+    """Array views (reference access.py:103-129): the reference's random programs
+    with every cell an ELEMENT of one int64 array, accessed through
+    write_array / read_array / commutative_write_array / ...  Each element is its
+    own handle, so the dependency edges and the values equal the reference's for
+    the same programs on separate cells (tests/golden/random_programs.json)."""
+    amode = {"read": sf.read_array, "write": sf.write_array, "atomic": sf.atomic_write_array,
+             "commute": sf.commutative_write_array, "maybe": sf.maybe_write_array}
+    eng = sim_engine(1, 1)
+    try:
+        for p in random_programs[:60]:
+            X = np.arange(1, p["n_cells"] + 1, dtype=np.int64)
+            g = sf.TaskGraph().compute_on(eng)
+            tids = []
+            with g.gated():
+                for m, target, reads, a, b in p["tasks"]:
+                    acc = [amode[m](X, [target])]
+                    if reads:
+                        acc.append(sf.read_array(X, reads))
+                    tids.append(g.task(*acc, device=sf.ops.cell(m, a, b)).task_id)
+            assert g.wait_all(timeout=30)
+            assert edge_indices(g, tids) == sorted(map(tuple, p["edges"]))
+            for i in range(p["n_cells"]):
+                g.flush_to_host(X, element=i)
+            assert g.wait_all(timeout=30)
+            assert X.tolist() == p["sequential"]
+    finally:
+        eng.stop()
+
+
+def test_array_view_errors_and_whole_object_independence():
+    eng = sim_engine(1, 1)
+    try:
+        g = sf.TaskGraph().compute_on(eng)
+        X = np.zeros(4, np.int64)
+        with pytest.raises(sf.DuplicateAccessError):
+            sf.read_array(X, [1, 1])
+        with pytest.raises(sf.DuplicateAccessError):
+            g.task(sf.write_array(X, [2]), sf.read_array(X, [2]), device=sf.ops.noop)
+        with pytest.raises(IndexError):
+            g.task(sf.write_array(X, [7]), device=sf.ops.noop)
+        # element handles are distinct from the whole-object handle (reference
+        # registry keys (id(obj)) vs (id(obj), element)): no edge between them
+        t1 = g.task(sf.write_array(X, [0]), device=sf.ops.cell("write", 2, 1)).task_id
+        t2 = g.task(sf.write(X), device=sf.ops.noop).task_id
+        assert g.wait_all(timeout=10)
+        assert (t1, t2) not in {(s, d) for s, d, _ in g.edges()}
+    finally:
+        eng.stop()
+
+
+def test_object_in_two_graphs_hands_over_through_the_host():
+    """One live handle per host buffer across graphs: registering an object in a
+    second graph retires the first graph's handle (its dirty device copy is
+    written home first), so the second graph sees the first one's result; the
+    first graph can no longer use the object; a busy object cannot move."""
+    eng = sim_engine(2, 2)
+    try:
+        c = sf.Cell(5)
+        g1 = sf.TaskGraph().compute_on(eng)
+        g1.task(sf.write(c), device=sf.ops.cell("write", 3, 1))  # 16, dirty on a device
+        assert g1.wait_all(timeout=10)
+        g2 = sf.TaskGraph().compute_on(eng)
+        g2.task(sf.write(c), device=sf.ops.cell("write", 2, 0))  # 2 * 16
+        g2.flush_to_host(c)
+        assert g2.wait_all(timeout=10)
+        assert c.value == 32
+        with pytest.raises(sf.RegistrationError):
+            g1.task(sf.read(c), device=sf.ops.noop)
+        # a busy object: g3 holds pending work on d (paused engine), g4 may not take it
+        d = sf.Cell(1)
+        g3 = sf.TaskGraph().compute_on(eng)
+        eng.pause()
+        try:
+            g3.task(sf.write(d), device=sf.ops.cell("write", 1, 1))
+            g4 = sf.TaskGraph().compute_on(eng)
+            with pytest.raises(sf.RegistrationError):
+                g4.task(sf.read(d), device=sf.ops.noop)
+        finally:
+            eng.resume()
+        assert g3.wait_all(timeout=10)
+    finally:
+        eng.stop()
