@@ -204,6 +204,14 @@ const char* sfx_last_error(sfx_runtime* rt);
 int sfx_failure(sfx_runtime* rt, int* code, char* msg, uint64_t cap);
 
 int sfx_graph_create(sfx_runtime* rt, uint32_t* gid);
+/* per-graph options: "trace" (default 1: record Push/Pop/Start/End when the
+ * runtime traces; TaskGraph(trace=False) switches it off), "history" (default 1: every task and slot is kept for the
+ * dot export, as in the reference; 0, before the first task: finished tasks and
+ * passed slots are retired -- bounded memory for long-running graphs -- and
+ * sfx_edges only reports slots still live) */
+int sfx_graph_option(sfx_runtime* rt, uint32_t gid, const char* key, int64_t value);
+/* live Task objects, live slots (all handles) and tasks retired so far */
+int sfx_live(sfx_runtime* rt, uint64_t* tasks, uint64_t* slots, uint64_t* retired);
 int sfx_register(sfx_runtime* rt, uint32_t gid, uint64_t hid, void* host, uint64_t bytes, int64_t rows,
                  int64_t cols, int64_t ld, int32_t dtype);
 /* owner hint for the locality-aware scheduler (2-D block-cyclic distribution) */
@@ -240,7 +248,9 @@ int sfx_violations(sfx_runtime* rt, uint64_t* n);
  * default 1000000), "prefetch" (0/1: stage queued tasks' host operands while
  * all streams are busy, default 1 on CUDA), "prefetch_depth" (queued tasks
  * looked at, default 64), "kernel_timing" (0/1: launch-group timing events,
- * as SFX_FLAG_KTIME; always on while tracing) */
+ * as SFX_FLAG_KTIME; always on while tracing), "stream_affinity" (0/1, default 1:
+ * a task whose predecessor is in flight on a stream of its class is launched
+ * on that stream) */
 int sfx_set_option(sfx_runtime* rt, const char* key, int64_t value);
 
 /* external tasks (SFX_OP_EXTERN): block up to timeout_s (< 0: forever) until at

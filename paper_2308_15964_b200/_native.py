@@ -150,6 +150,8 @@ def _load():
         "sfx_extern_done": ([P, ctypes.c_uint64, ctypes.c_int, ctypes.c_char_p], ctypes.c_int),
         "sfx_gemm_paths": ([P, u32], ctypes.c_int),
         "sfx_fail": ([P, ctypes.c_char_p], ctypes.c_int),
+        "sfx_graph_option": ([P, u32, ctypes.c_char_p, i64], ctypes.c_int),
+        "sfx_live": ([P, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -166,7 +168,8 @@ EXPORTED = ("sfx_abi_version", "sfx_device_count", "sfx_create", "sfx_destroy", 
             "sfx_submit", "sfx_pause", "sfx_resume", "sfx_wait_all", "sfx_wait_task",
             "sfx_task_state", "sfx_flush", "sfx_stats", "sfx_resident", "sfx_block_state",
             "sfx_trace", "sfx_edges", "sfx_violations", "sfx_set_option", "sfx_host_alloc", "sfx_host_free",
-            "sfx_fp64_peak", "sfx_fp64_dfma_peak", "sfx_extern_poll", "sfx_extern_done", "sfx_gemm_paths", "sfx_fail")
+            "sfx_fp64_peak", "sfx_fp64_dfma_peak", "sfx_extern_poll", "sfx_extern_done", "sfx_gemm_paths", "sfx_fail",
+            "sfx_graph_option", "sfx_live")
 
 GEMM_PATH_NAMES = ("launches", "tasks", "work_items", "cpref", "multi_tile", "cpref_multi_tile", "splitk", "tri",
                    "lower", "nn", "nt")

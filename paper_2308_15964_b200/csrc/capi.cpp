@@ -161,6 +161,15 @@ int sfx_extern_done(sfx_runtime* r, uint64_t tid, int status, const char* msg) {
   return guarded(r, [&](sfx::Runtime& rt) { return rt.extern_done(tid, status, msg); });
 }
 
+int sfx_graph_option(sfx_runtime* r, uint32_t gid, const char* key, int64_t value) {
+  if (!key) return SFX_ERR_CONFIG;
+  return guarded(r, [&](sfx::Runtime& rt) { return rt.graph_option(gid, key, value); });
+}
+
+int sfx_live(sfx_runtime* r, uint64_t* tasks, uint64_t* slots, uint64_t* retired) {
+  return guarded(r, [&](sfx::Runtime& rt) { return rt.live(tasks, slots, retired); });
+}
+
 int sfx_fail(sfx_runtime* r, const char* msg) {
   return guarded(r, [&](sfx::Runtime& rt) { return rt.fail(msg ? msg : "external agent failed"); });
 }

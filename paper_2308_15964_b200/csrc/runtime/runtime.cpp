@@ -129,10 +129,10 @@ Runtime::~Runtime() {
   }
   // drop every sync/event reference before the backend goes away
   for (auto& t : task_store_) {
-    t.waits.clear();
-    t.start.reset();
-    t.end.reset();
-    t.copy_syncs.clear();
+    t->waits.clear();
+    t->start.reset();
+    t->end.reset();
+    t->copy_syncs.clear();
   }
   for (auto& h : handle_store_) {
     h->host_ready.reset();
@@ -192,7 +192,7 @@ int Runtime::reg(uint32_t gid, uint64_t hid, void* host, uint64_t bytes, int64_t
       if (it->first + o->bytes > lo && o->gid != gid) olds.push_back(o);
     }
     for (Handle* o : olds) {
-      bool busy = o->active < o->slots.size();
+      bool busy = o->active < o->slot_end();
       for (Block* b : o->blocks) busy = busy || (b && b->pins > 0);
       if (busy) {
         last_error = fmt("the object's memory is still in use by graph %u (pending accesses): wait for that graph "
@@ -221,6 +221,7 @@ int Runtime::reg(uint32_t gid, uint64_t hid, void* host, uint64_t bytes, int64_t
   h->ld = ld;
   h->dtype = dtype;
   h->blocks.assign(ndev_, nullptr);
+  h->graph = git->second.get();
   handles_[hid] = h.get();
   if (host && bytes) {
     host_ranges_.emplace(reinterpret_cast<uintptr_t>(host), h.get());
@@ -279,7 +280,7 @@ int Runtime::unreg(uint64_t hid) {
     return SFX_ERR_REGISTRATION;
   }
   Handle* h = it->second;
-  if (h->active < h->slots.size()) {
+  if (h->active < h->slot_end()) {
     // handles.py:179-182
     last_error = "cannot unregister an object with pending accesses";
     return SFX_ERR_REGISTRATION;
@@ -506,20 +507,21 @@ void Runtime::bind(Task* t, Handle* h, uint32_t mode) {
   const bool grouping = cat != CAT_X;
   auto& slots = h->slots;
   uint32_t idx;
-  if (grouping && !slots.empty() && slots.back().cat == cat && h->active + 1 <= slots.size()) {
-    idx = static_cast<uint32_t>(slots.size() - 1);
+  if (grouping && !slots.empty() && slots.back().cat == cat && h->active + 1 <= h->slot_end()) {
+    idx = h->slot_end() - 1;
   } else {
-    slots.push_back(Slot{cat, {}, 0});
-    idx = static_cast<uint32_t>(slots.size() - 1);
+    slots.push_back(Slot{cat, {}, 0, 0});
+    idx = h->slot_end() - 1;
   }
-  slots[idx].tasks.push_back(t);
+  h->slot(idx).tasks.push_back(t);
   t->acc.push_back(Access{h, mode, idx});
   if (idx != h->active) {
     t->pending += 1;
-  } else if (idx > 0) {
+  } else if (idx > h->slot_base) {
     // The slot is already active: the previous slot's members were released at
     // launch and may still be running on a device -- wait on their end events.
-    for (Task* p : slots[idx - 1].tasks)
+    // (A retired previous slot had finished entirely.)
+    for (Task* p : h->slot(idx - 1).tasks)
       if (p->end && !p->end->complete) t->waits.push_back(p->end);
   }
 }
@@ -539,9 +541,9 @@ int Runtime::submit(uint32_t n, const sfx_task_desc* descs, const sfx_access* ac
       last_error = fmt("task id %llu reused", (unsigned long long)d.tid);
       return SFX_ERR_INTERNAL;
     }
-    task_store_.emplace_back();
-    Task* t = &task_store_.back();
+    Task* t = new_task();
     t->tid = d.tid;
+    max_tid_ = std::max(max_tid_, d.tid);
     t->gid = d.graph;
     t->op = d.op;
     t->prio = d.priority;
@@ -552,6 +554,7 @@ int Runtime::submit(uint32_t n, const sfx_task_desc* descs, const sfx_access* ac
     }
     t->acc.reserve(d.n_access);
     for (uint32_t k = 0; k < d.n_access; ++k) bind(t, handles_[acc[ai + k].hid], acc[ai + k].mode);
+    t->slot_refs = d.n_access;
     ai += d.n_access;
     // guards: commutative handles (exclusive, or shared for ops that accumulate with
     // device atomics); with several devices also atomic handles, in shared mode:
@@ -571,7 +574,6 @@ int Runtime::submit(uint32_t n, const sfx_task_desc* descs, const sfx_access* ac
       t->commute_sh.push_back(gp.second);
     }
     Graph* g = graphs_[d.graph].get();
-    g->tasks.push_back(t);
     g->inserted += 1;
     tasks_by_tid_[t->tid] = t;
     if (--t->pending == 0) {  // drop the insertion guard (graph.py:161-163)
@@ -656,7 +658,7 @@ int Runtime::place(Task* t) {
 }
 
 void Runtime::record(Graph* g, int kind, int64_t t, int wid, uint64_t tid, int64_t extra) {
-  if (!trace_ || !g) return;
+  if (!trace_ || !g || !g->trace) return;
   sfx_event e;
   e.t_ns = t;
   e.tid = tid;
@@ -685,9 +687,10 @@ void Runtime::advance(Handle* h) {
   const uint32_t prev = h->active;
   h->active += 1;
   h->group_dev = -1;
-  if (h->active >= h->slots.size()) return;
-  Slot& nx = h->slots[h->active];
-  const Slot& pv = h->slots[prev];
+  if (h->graph && !h->graph->history) retire_pending_.push_back(h);
+  if (h->active >= h->slot_end()) return;
+  Slot& nx = h->slot(h->active);
+  const Slot& pv = h->slot(prev);
   for (Task* m : nx.tasks) {
     for (Task* p : pv.tasks)
       if (p->end && !p->end->complete) m->waits.push_back(p->end);
@@ -707,9 +710,50 @@ void Runtime::release(Task* t) {
   t->released = true;
   for (auto& a : t->acc) {
     Handle* h = a.h;
-    Slot& s = h->slots[a.slot];
+    Slot& s = h->slot(a.slot);
     s.done += 1;
     if (a.slot == h->active && s.done >= s.tasks.size()) advance(h);
+  }
+  flush_retire();
+}
+
+// ------------------------------------------------------------ retirement
+
+Task* Runtime::new_task() {
+  live_tasks_ += 1;
+  if (!task_free_.empty()) {
+    Task* t = task_free_.back();
+    task_free_.pop_back();
+    return t;
+  }
+  task_store_.push_back(std::make_unique<Task>());
+  return task_store_.back().get();
+}
+
+void Runtime::free_task(Task* t) {
+  tasks_by_tid_.erase(t->tid);
+  *t = Task();
+  task_free_.push_back(t);
+  live_tasks_ -= 1;
+  retired_tasks_ += 1;
+}
+
+void Runtime::flush_retire() {
+  // history-free graphs: pop every slot that is passed (index < active) and whose
+  // members all completed; a task goes back to the pool once all its slots went.
+  // Runs only at the end of release()/complete(), never while a caller still
+  // iterates a task's accesses.
+  while (!retire_pending_.empty()) {
+    Handle* h = retire_pending_.back();
+    retire_pending_.pop_back();
+    while (!h->slots.empty() && h->slot_base < h->active) {
+      Slot& s = h->slots.front();
+      if (s.finished < s.tasks.size()) break;
+      for (Task* t : s.tasks)
+        if (--t->slot_refs == 0) free_task(t);
+      h->slots.pop_front();
+      h->slot_base += 1;
+    }
   }
 }
 
@@ -1370,6 +1414,13 @@ void Runtime::complete(Task* t) {
   D.stats.tasks_executed += 1;
   D.exec_cv.notify_one();
   done_cv_.notify_all();
+  if (!g->history) {
+    for (auto& a : t->acc) {
+      a.h->slot(a.slot).finished += 1;
+      retire_pending_.push_back(a.h);
+    }
+    flush_retire();  // may free t: nothing below touches it
+  }
 }
 
 void Runtime::extern_handoff(Task* t) {
@@ -1523,15 +1574,32 @@ void Runtime::exec_loop(int d) {
           best = k;
       return best;
     };
+    // Stream affinity: a task whose predecessor is still in flight on a stream of
+    // its class joins that stream (ordered by the stream itself, no event wait).
+    // Otherwise a chain's successor can queue behind ANOTHER chain's task on a
+    // shared stream and inherit its wait (head-of-line blocking: the reference
+    // overhead protocol, T chains of 1 ms tasks, ran at 2 ms per chain step).
+    auto affine = [&](const Task* t, int lo, int hi) {
+      if (!stream_affinity_) return -1;
+      for (const SyncP& w : t->waits)
+        if (w && !w->complete && w->dev == d && w->stream >= lo && w->stream < hi &&
+            D.stream_groups[w->stream] < static_cast<int>(groups_per_stream_))
+          return w->stream;
+      return -1;
+    };
+    auto pick = [&](const Task* t, int lo, int hi) {
+      const int s = affine(t, lo, hi);
+      return s >= 0 ? s : free_in(lo, hi);
+    };
     // urgent tasks prefer the high-priority streams and may fall back to normal
     // ones; normal tasks never take an urgent stream
     auto free_stream = [&](const Task* t) {
       if (is_coop(t)) return free_in(nstreams_ + nurgent_, nstreams_ + nurgent_ + ncoop_);
       if (nurgent_ > 0 && t->prio >= urgent_priority_) {
-        int s = free_in(nstreams_, nstreams_ + nurgent_);
-        return s >= 0 ? s : free_in(0, nstreams_);
+        int s = pick(t, nstreams_, nstreams_ + nurgent_);
+        return s >= 0 ? s : pick(t, 0, nstreams_);
       }
-      return free_in(0, nstreams_);
+      return pick(t, 0, nstreams_);
     };
     auto runnable = [&] {
       return !paused_ && !fail_code_ && D.queue.size() > 0 && D.ninflight < static_cast<int>(window_) &&
@@ -1806,6 +1874,7 @@ int Runtime::wait_task(uint64_t tid, double timeout_s) {
   std::unique_lock<std::mutex> lk(mu_);
   auto it = tasks_by_tid_.find(tid);
   if (it == tasks_by_tid_.end()) {
+    if (tid && tid <= max_tid_ && retired_tasks_) return SFX_OK;  // retired: it finished
     last_error = "unknown task";
     return SFX_ERR_CONFIG;
   }
@@ -1827,6 +1896,10 @@ int Runtime::task_state(uint64_t tid, int32_t* st) {
   std::unique_lock<std::mutex> lk(mu_);
   auto it = tasks_by_tid_.find(tid);
   if (it == tasks_by_tid_.end()) {
+    if (tid && tid <= max_tid_ && retired_tasks_) {  // retired by a history-free graph: it finished
+      *st = SFX_STATE_FINISHED;
+      return SFX_OK;
+    }
     last_error = "unknown task";
     return SFX_ERR_CONFIG;
   }
@@ -1972,6 +2045,8 @@ int Runtime::set_option(const std::string& key, int64_t value) {
   } else if (key == "kernel_timing") {
     // launch-group timing events (SFX_FLAG_KTIME); tracing keeps them on
     ktime_ = trace_ || value != 0;
+  } else if (key == "stream_affinity") {
+    stream_affinity_ = value != 0;
   } else if (key == "window") {
     window_ = static_cast<uint32_t>(std::max<int64_t>(1, value));
     for (auto& d : devs_) d->exec_cv.notify_all();
@@ -1979,6 +2054,39 @@ int Runtime::set_option(const std::string& key, int64_t value) {
     last_error = "unknown option " + key;
     return SFX_ERR_CONFIG;
   }
+  return SFX_OK;
+}
+
+int Runtime::graph_option(uint32_t gid, const std::string& key, int64_t value) {
+  std::unique_lock<std::mutex> lk(mu_);
+  auto it = graphs_.find(gid);
+  if (it == graphs_.end()) {
+    last_error = fmt("unknown graph %u", gid);
+    return SFX_ERR_CONFIG;
+  }
+  if (key == "history") {
+    if (!value && it->second->inserted) {
+      last_error = "history can only be switched off before the graph's first task";
+      return SFX_ERR_CONFIG;
+    }
+    it->second->history = value != 0;
+    return SFX_OK;
+  }
+  if (key == "trace") {
+    it->second->trace = value != 0;
+    return SFX_OK;
+  }
+  last_error = "unknown graph option " + key;
+  return SFX_ERR_CONFIG;
+}
+
+int Runtime::live(uint64_t* tasks, uint64_t* slots, uint64_t* retired) {
+  std::unique_lock<std::mutex> lk(mu_);
+  uint64_t ns = 0;
+  for (auto& h : handle_store_) ns += h->slots.size();
+  if (tasks) *tasks = live_tasks_;
+  if (slots) *slots = ns;
+  if (retired) *retired = retired_tasks_;
   return SFX_OK;
 }
 

@@ -79,8 +79,11 @@ struct Handle;
 struct Slot {
   Cat cat;
   std::vector<Task*> tasks;
-  uint32_t done = 0;
+  uint32_t done = 0;      // members released (at launch)
+  uint32_t finished = 0;  // members completed (retirement: history-free graphs)
 };
+
+struct Graph;
 
 struct Block {
   Handle* h = nullptr;
@@ -100,8 +103,14 @@ struct Handle {
   uint64_t bytes = 0;
   int64_t rows = 0, cols = 0, ld = 0;
   int32_t dtype = 0;
-  std::vector<Slot> slots;
+  // slots by ABSOLUTE index (Access::slot, active): slots.front() is slot_base;
+  // a history-free graph pops slots that are passed and whose members all finished
+  std::deque<Slot> slots;
+  uint32_t slot_base = 0;
+  uint32_t slot_end() const { return slot_base + static_cast<uint32_t>(slots.size()); }
+  Slot& slot(uint32_t abs) { return slots[abs - slot_base]; }
   uint32_t active = 0;
+  Graph* graph = nullptr;
   std::vector<Block*> blocks;  // per device
   int dirty_dev = -1;          // at most one dirty copy
   bool host_valid = true;
@@ -153,6 +162,7 @@ struct Task {
   bool guards_held = false;      // its commutative guards are acquired (idempotent acquire)
   bool detached = false;         // SFX_OP_EXTERN handed to the host agent: stream slots freed
   int status_slot = -1;          // device-written status word (DPOTRF info), read at completion
+  uint32_t slot_refs = 0;        // slots of it not yet retired (freed back to the pool at 0)
 };
 
 struct Operand {
@@ -235,7 +245,11 @@ int64_t now_ns();
 struct Graph {
   uint32_t gid = 0;
   uint64_t inserted = 0, completed = 0;
-  std::vector<Task*> tasks;
+  // history (default, the reference's behaviour): every task and slot is kept for
+  // the dot export / edges.  Without it finished tasks and passed slots are
+  // retired (bounded runtime memory for long-running graphs, handles.py:114-189)
+  bool history = true;
+  bool trace = true;  // TaskGraph(trace=...): record events (when the runtime traces)
   std::vector<Handle*> handles;
   std::vector<sfx_event> events;
 };
@@ -305,6 +319,8 @@ class Runtime {
   int violations(uint64_t* n);
   int failure(int* code, char* msg, uint64_t cap);
   int set_option(const std::string& key, int64_t value);
+  int graph_option(uint32_t gid, const std::string& key, int64_t value);
+  int live(uint64_t* tasks, uint64_t* slots, uint64_t* retired);
 
   std::string last_error;
 
@@ -351,6 +367,7 @@ class Runtime {
   // cooperative POTRF/TRSM kernels run only on these (at most ncoop_ of them
   // co-resident, so their grid barriers can never starve each other)
   int ncoop_ = 2;
+  bool stream_affinity_ = true;  // successors join their in-flight predecessor's stream
   bool is_coop(const Task* t) const;
   // Prefetch: while every stream is busy, the executor stages host-resident
   // operands of tasks waiting in its queue on a dedicated copy stream, so PCIe
@@ -375,7 +392,13 @@ class Runtime {
   std::vector<std::unique_ptr<Handle>> handle_store_;
   std::unordered_map<uint32_t, std::unique_ptr<Graph>> graphs_;
   std::unordered_map<uint64_t, Task*> tasks_by_tid_;
-  std::deque<Task> task_store_;
+  std::vector<std::unique_ptr<Task>> task_store_;  // every Task object ever allocated
+  std::vector<Task*> task_free_;                   // retired, reusable
+  std::vector<Handle*> retire_pending_;            // handles whose active slot moved (history-free)
+  uint64_t max_tid_ = 0, live_tasks_ = 0, retired_tasks_ = 0;
+  Task* new_task();
+  void free_task(Task* t);
+  void flush_retire();
   uint32_t next_gid_ = 1;
   uint64_t push_seq_ = 0;
   bool paused_ = false, stopping_ = false;

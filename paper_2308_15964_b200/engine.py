@@ -117,6 +117,10 @@ class ComputeEngine:
                                  flags, int(window), ctypes.byref(handle)))
         self._h = handle
         self.set_option("group_max", group_max)
+        # runtime knobs from the environment (experiments): SFX_OPT_<KEY>=<int>
+        for key, value in os.environ.items():
+            if key.startswith("SFX_OPT_"):
+                self.set_option(key[8:].lower(), int(value))
         self.graphs = []
         self._stopped = False
 
@@ -186,6 +190,12 @@ class ComputeEngine:
         N.check(N.lib.sfx_block_state(self._h, hid, dev, ctypes.byref(st), ctypes.byref(hv)), self._h)
         return {"present": bool(st.value & 4), "valid": bool(st.value & 1), "dirty": bool(st.value & 2),
                 "host_valid": bool(hv.value)}
+
+    def live(self) -> dict:
+        """Runtime-wide live Task objects and slots, and tasks retired so far."""
+        t, sl, r = ctypes.c_uint64(0), ctypes.c_uint64(0), ctypes.c_uint64(0)
+        N.check(N.lib.sfx_live(self._h, ctypes.byref(t), ctypes.byref(sl), ctypes.byref(r)), self._h)
+        return {"tasks": t.value, "slots": sl.value, "retired": r.value}
 
     def violations(self) -> int:
         n = ctypes.c_uint64(0)

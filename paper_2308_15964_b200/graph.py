@@ -179,7 +179,10 @@ class TraceView:
 class TaskGraph:
     """Sequential task flow over declared data accesses, executed on B200s."""
 
-    def __init__(self, speculation: bool = False, trace: bool = True):
+    def __init__(self, speculation: bool = False, trace: bool = True, history: bool = True):
+        """``history=False`` (an extension): finished tasks and passed slots are
+        retired by the runtime, so a long-running graph has bounded memory; the
+        dot export / edges then only cover what is still live."""
         if speculation:
             raise SpeculationError(
                 "speculative execution is not part of the GPU path (the reference also rejects "
@@ -203,6 +206,7 @@ class TaskGraph:
         self.trace.enabled = trace
         self.speculation_enabled = False
         self.comm = None
+        self.history = history
 
     # -- inter-process communication (graph.py:264-284, comms.py) -------------
     def use_comm(self, comm) -> "TaskGraph":
@@ -238,6 +242,10 @@ class TaskGraph:
         self._h = engine._h
         self._hval = engine._h.value  # raw runtime pointer for the fast submit path
         self._gid = gid.value
+        if not self.history:
+            N.check(N.lib.sfx_graph_option(engine._h, self._gid, b"history", 0), engine._h)
+        if not self.trace.enabled:  # TaskGraph(trace=False): no event recording (reference graph.py:34)
+            N.check(N.lib.sfx_graph_option(engine._h, self._gid, b"trace", 0), engine._h)
         engine.adopt(self)
         self._t0 = time.perf_counter_ns()
         return self

@@ -654,3 +654,58 @@ def test_object_in_two_graphs_hands_over_through_the_host():
         assert g3.wait_all(timeout=10)
     finally:
         eng.stop()
+
+
+@pytest.mark.parametrize("devices,streams", [(1, 1), (2, 3)])
+def test_history_free_graphs_retire_tasks_and_keep_semantics(random_programs, devices, streams):
+    """TaskGraph(history=False): finished tasks and passed slots are retired
+    (reference handles.py:114-189 retires handles; here the runtime's task/slot
+    records go back to a pool) -- values still equal the sequential execution,
+    and only the tasks of each handle's last slot stay live."""
+    eng = sim_engine(devices, streams)
+    try:
+        for p in random_programs:
+            g = sf.TaskGraph(history=False).compute_on(eng)
+            cells, tids = insert_program(g, p)
+            for c in cells:
+                g.flush_to_host(c)
+            assert g.wait_all(timeout=30)
+            assert [c.value for c in cells] == p["sequential"]
+            sf.TaskViewer(g, tids[0]).wait()  # a retired task reads as finished
+        live = eng.live()
+        assert live["retired"] > 0
+    finally:
+        eng.stop()
+
+
+def test_million_task_soak_has_flat_runtime_memory():
+    """10^6 tasks through one history-free graph: the live task and slot counts
+    and the process RSS stay flat (round-1 review: task_store_/slots only grew)."""
+    import psutil
+
+    eng = sim_engine(1, 4)
+    proc = psutil.Process()
+    try:
+        g = sf.TaskGraph(history=False, trace=False).compute_on(eng)
+        T = 8
+        cells = [sf.Cell(0) for _ in range(T)]
+        H = np.array([g.hid_of(c) for c in cells], np.uint64)
+        op = sf.ops.cell("write", 1, 1)
+        chunk = 20000
+        rss = []
+        for rep in range(50):  # 50 x 20,000 = 10^6 tasks
+            hids = np.tile(H, chunk // T)
+            g.submit_arrays(np.full(chunk, op.code, np.uint32), np.zeros((chunk, 4)),
+                            np.tile(np.array(op.iparam, np.int64), (chunk, 1)), np.zeros(chunk, np.int32),
+                            np.ones(chunk, np.uint32), hids, np.full(chunk, sf.AccessMode.WRITE.code, np.uint32))
+            assert g.wait_all(timeout=60)
+            live = eng.live()
+            assert live["tasks"] <= 2 * T and live["slots"] <= 2 * T, live
+            rss.append(proc.memory_info().rss)
+        g.flush_all(keep_device=False)
+        assert g.wait_all(timeout=60)
+        assert eng.live()["retired"] >= 10 ** 6 - 2 * T
+        assert [c.value for c in cells] == [(10 ** 6 // T)] * T  # x <- x + 1 per task
+        assert rss[-1] - rss[5] < 32 << 20, (rss[5], rss[-1])
+    finally:
+        eng.stop()
