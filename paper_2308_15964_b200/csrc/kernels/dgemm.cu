@@ -62,6 +62,9 @@ struct GemmGroup {
   long long ldc;
   int ntasks;
   int ksplit;  // > 1: split-K, partial products are atomically added into C (beta == 1)
+  int tri_split;  // TRI only: K-weighted split -- output column tile bn (whose k-range
+                  // is [0, (bn+1)*BN) under the triangular mask) is cut into bn+1
+                  // slices of BN/BK k-steps, atomically added (beta == 1)
   int tri;     // NN only: B is an upper-triangular block with a reciprocal diagonal
                // (B[k][n] = 0 for k > n, 1/B[k][k] on the diagonal) -- the inverse
                // blocks a store_inverses DPOTRF leaves in its tile's upper triangle
@@ -86,13 +89,35 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
   uint64_t* cfull = empty + STAGES;
   uint64_t* cempty = cfull + 1;
 
-  const int total = p.ntasks * p.tiles_per_task * p.ksplit;
+  const int tri_row = p.tiles_n * (p.tiles_n + 1) / 2;  // TRI split: work items per row of output tiles
+  const int total = p.tri_split ? p.ntasks * (p.tiles_per_task / p.tiles_n) * tri_row
+                                : p.ntasks * p.tiles_per_task * p.ksplit;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ktiles_all = (p.K + BK - 1) / BK;
   const int kchunk = (ktiles_all + p.ksplit - 1) / p.ksplit;
 
   // linear work index -> (task, m0, n0, k-slice); lower = triangular enumeration (bm >= bn)
   auto coords = [&](int lin, int& task, int& m0, int& n0, int& kt0, int& kt1) {
+    if (TRI && p.tri_split) {
+      // (task, bm) rows of tri_row items; item w -> column tile bn (triangular
+      // root) and slice w - bn(bn+1)/2 of BN/BK k-steps: every item has the same
+      // length, so the CTAs stay balanced (a uniform split-K leaves the long
+      // right-hand column tiles 8x the work of the left ones)
+      const int rows = p.tiles_per_task / p.tiles_n;
+      const int w = lin % tri_row;
+      const int rb = lin / tri_row;
+      task = rb / rows;
+      const int bm = rb - task * rows;
+      int bn = static_cast<int>((sqrtf(8.0f * w + 1.0f) - 1.0f) * 0.5f);
+      while ((bn + 1) * (bn + 2) / 2 <= w) ++bn;
+      while (bn * (bn + 1) / 2 > w) --bn;
+      const int slice = w - bn * (bn + 1) / 2;
+      m0 = bm * BM;
+      n0 = bn * BN;
+      kt0 = slice * (BN / BK);
+      kt1 = min(ktiles_all, kt0 + BN / BK);
+      return;
+    }
     const int ks = lin % p.ksplit;
     lin /= p.ksplit;
     kt0 = ks * kchunk;
@@ -174,6 +199,14 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
   asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
   const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warp grid, warp tile 64 x 32
   const int g = lane >> 2, t = lane & 3;
+  const int sw = TRANS_B ? 0 : (t >> 1);  // NN: k order within a pair (see the B loads)
+  // output columns (within the warp's 32) of this thread's accumulator pair P =
+  // 0..3 (two adjacent columns each): NT: fragment j = P, columns 8P + 2t (+1);
+  // NN (column permutation of the B loads): columns 8t + 2P (+1), i.e. a row's 8
+  // values of one thread are contiguous
+#define PCOL(P) (TRANS_B ? 8 * (P) + 2 * t : 8 * t + 2 * (P))
+#define ACCX(i, P) (TRANS_B ? acc[i][P][0] : acc[i][2 * ((P)&1)][(P) >> 1])
+#define ACCY(i, P) (TRANS_B ? acc[i][P][1] : acc[i][2 * ((P)&1) + 1][(P) >> 1])
   int it = 0, cn = 0;
   for (int lin = blockIdx.x; lin < total; lin += gridDim.x) {
     int task, m0, n0, kt0, kt1;
@@ -189,8 +222,9 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
       ptx::mbar_wait(&full[s], (it / STAGES) & 1);
       const uint32_t aS = ptx::smem_u32(sA) + s * A_STAGE;
       const uint32_t bS = ptx::smem_u32(sB) + s * B_STAGE;
-      // operands (true k = 4t + 2h + e): ordered shared loads; the DMMAs are
-      // not volatile, so ptxas can slide this half's DMMAs past the next loads
+      // operands (true k = sigma(t, h, e) = 4t + 2h + (e ^ sw)): ordered shared
+      // loads; the DMMAs are not volatile, so ptxas can slide this half's DMMAs
+      // past the next loads
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         double a[8][2], b[4][2];
@@ -198,8 +232,8 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
         for (int i = 0; i < 8; ++i) {
           const int r = wm * 64 + 8 * i + g;  // r % 8 == g
           const double2 v = ptx::lds128(aS + r * 128 + (((2 * t + h) ^ g) << 4));
-          a[i][0] = v.x;
-          a[i][1] = v.y;
+          a[i][0] = sw ? v.y : v.x;
+          a[i][1] = sw ? v.x : v.y;
         }
         if (TRANS_B) {
 #pragma unroll
@@ -210,18 +244,31 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
             b[j][1] = v.y;
           }
         } else {
+          // NN: B stored [K][N] in 16-column TMA boxes (128B swizzle).  Thread
+          // (g, t) owns warp columns 4g..4g+3 (fragment j, local column c ->
+          // warp column 4c + j), so its operands of one k are 4 consecutive
+          // doubles: two LDS.128 per sub-step instead of four LDS.64.  Threads
+          // t >= 2 take the two k of each pair in the opposite order (sw), which
+          // puts the rows one quarter-warp reads on swizzle phases p ^ {0,1,4,5}:
+          // no bank conflict.
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int n = wn * 32 + 8 * j + g;
-            const int q = n >> 4, nn = n & 15;
+          for (int e = 0; e < 2; ++e) {
+            const int k = 4 * t + 2 * h + (e ^ sw);
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int k = 4 * t + 2 * h + e;
-              b[j][e] = ptx::lds64(bS + q * 2048 + k * 128 + (((nn >> 1) ^ (k & 7)) << 4) + (nn & 1) * 8);
-              if (TRI) {
+            for (int jp = 0; jp < 2; ++jp) {
+              const int n = wn * 32 + 4 * g + 2 * jp;
+              const int nn = n & 15;
+              const double2 v = ptx::lds128(bS + (n >> 4) * 2048 + k * 128 + (((nn >> 1) ^ (k & 7)) << 4));
+              double b0 = v.x, b1 = v.y;
+              if (TRI) {  // masked only on the k-steps that cross the diagonal
                 const int kg = kt * BK + k, ng = n0 + n;
-                b[j][e] = kg > ng ? 0.0 : (kg == ng ? 1.0 / b[j][e] : b[j][e]);
+                if (kt * BK + BK > n0 + wn * 32) {
+                  b0 = kg > ng ? 0.0 : (kg == ng ? 1.0 / b0 : b0);
+                  b1 = kg > ng + 1 ? 0.0 : (kg == ng + 1 ? 1.0 / b1 : b1);
+                }
               }
+              b[2 * jp][e] = b0;
+              b[2 * jp + 1][e] = b1;
             }
           }
         }
@@ -254,18 +301,18 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
     // Interior tiles batch all 32 C loads before any FMA/store so the loads
     // overlap (one HBM round trip per tile instead of one per fragment).
     double* const Cbase = p.t[task].C;
-    if (p.ksplit > 1) {
+    if (p.ksplit > 1 || (TRI && p.tri_split)) {
       // split-K partial sum: C += alpha * acc (beta == 1 enforced by the launcher)
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int row = m0 + wm * 64 + 8 * i + g;
         if (row >= p.M) continue;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int col = n0 + wn * 32 + 8 * j + 2 * t;
+        for (int P = 0; P < 4; ++P) {
+          const int col = n0 + wn * 32 + PCOL(P);
           double* cp = Cbase + static_cast<long long>(row) * p.ldc + col;
-          if (col < p.N && (!p.lower || row >= col)) atomicAdd(cp, p.alpha * acc[i][j][0]);
-          if (col + 1 < p.N && (!p.lower || row >= col + 1)) atomicAdd(cp + 1, p.alpha * acc[i][j][1]);
+          if (col < p.N && (!p.lower || row >= col)) atomicAdd(cp, p.alpha * ACCX(i, P));
+          if (col + 1 < p.N && (!p.lower || row >= col + 1)) atomicAdd(cp + 1, p.alpha * ACCY(i, P));
         }
       }
       continue;
@@ -273,20 +320,19 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
     const bool interior = !p.lower && m0 + BM <= p.M && n0 + BN <= p.N;
     if (interior && p.cpref) {
       // C from the prefetch buffer: element (r, c) of the tile sits in box q = c / 16
-      // at r * 128 + (((c % 16) / 2) ^ (r % 8)) * 16 + (c % 2) * 8 -- a warp's 32
-      // 16-byte reads cover every 128-byte row segment once (4 wavefronts, no conflict)
+      // at r * 128 + (((c % 16) / 2) ^ (r % 8)) * 16 + (c % 2) * 8
       ptx::mbar_wait(cfull, cn & 1);
       const uint32_t cS = ptx::smem_u32(sC);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int r = wm * 64 + 8 * i + g;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int c = wn * 32 + 8 * j + 2 * t;
+        for (int P = 0; P < 4; ++P) {
+          const int c = wn * 32 + PCOL(P);
           const double2 cv = ptx::lds128(cS + (c >> 4) * (BM * 128) + r * 128 + ((((c & 15) >> 1) ^ g) << 4));
           double2 v;
-          v.x = fma(p.beta, cv.x, p.alpha * acc[i][j][0]);
-          v.y = fma(p.beta, cv.y, p.alpha * acc[i][j][1]);
+          v.x = fma(p.beta, cv.x, p.alpha * ACCX(i, P));
+          v.y = fma(p.beta, cv.y, p.alpha * ACCY(i, P));
           *reinterpret_cast<double2*>(Cbase + static_cast<long long>(m0 + r) * p.ldc + n0 + c) = v;
         }
       }
@@ -302,26 +348,26 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
 #pragma unroll
           for (int i = 0; i < 2; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              cv[i][j] = *reinterpret_cast<const double2*>(
+            for (int P = 0; P < 4; ++P)
+              cv[i][P] = *reinterpret_cast<const double2*>(
                   Cbase + static_cast<long long>(m0 + wm * 64 + 8 * (2 * half + i) + g) * p.ldc + n0 + wn * 32 +
-                  8 * j + 2 * t);
+                  PCOL(P));
         }
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int P = 0; P < 4; ++P) {
             const int ii = 2 * half + i;
             double2 v;
             if (p.beta != 0.0) {
-              v.x = fma(p.beta, cv[i][j].x, p.alpha * acc[ii][j][0]);
-              v.y = fma(p.beta, cv[i][j].y, p.alpha * acc[ii][j][1]);
+              v.x = fma(p.beta, cv[i][P].x, p.alpha * ACCX(ii, P));
+              v.y = fma(p.beta, cv[i][P].y, p.alpha * ACCY(ii, P));
             } else {
-              v.x = p.alpha * acc[ii][j][0];
-              v.y = p.alpha * acc[ii][j][1];
+              v.x = p.alpha * ACCX(ii, P);
+              v.y = p.alpha * ACCY(ii, P);
             }
             *reinterpret_cast<double2*>(Cbase + static_cast<long long>(m0 + wm * 64 + 8 * ii + g) * p.ldc + n0 +
-                                        wn * 32 + 8 * j + 2 * t) = v;
+                                        wn * 32 + PCOL(P)) = v;
           }
       }
       continue;
@@ -332,29 +378,33 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
       if (row >= p.M) continue;
       double* crow = Cbase + static_cast<long long>(row) * p.ldc;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int col = n0 + wn * 32 + 8 * j + 2 * t;
+      for (int P = 0; P < 4; ++P) {
+        const int col = n0 + wn * 32 + PCOL(P);
+        const double x = ACCX(i, P), y = ACCY(i, P);
         const bool ok0 = col < p.N && (!p.lower || row >= col);
         const bool ok1 = col + 1 < p.N && (!p.lower || row >= col + 1);
         if (ok0 && ok1) {
           double2* cp = reinterpret_cast<double2*>(crow + col);
           double2 v;
           if (p.beta == 0.0) {
-            v.x = p.alpha * acc[i][j][0];
-            v.y = p.alpha * acc[i][j][1];
+            v.x = p.alpha * x;
+            v.y = p.alpha * y;
           } else {
             double2 o = *cp;
-            v.x = fma(p.beta, o.x, p.alpha * acc[i][j][0]);
-            v.y = fma(p.beta, o.y, p.alpha * acc[i][j][1]);
+            v.x = fma(p.beta, o.x, p.alpha * x);
+            v.y = fma(p.beta, o.y, p.alpha * y);
           }
           *cp = v;
         } else {
-          if (ok0) crow[col] = (p.beta == 0.0 ? 0.0 : p.beta * crow[col]) + p.alpha * acc[i][j][0];
-          if (ok1) crow[col + 1] = (p.beta == 0.0 ? 0.0 : p.beta * crow[col + 1]) + p.alpha * acc[i][j][1];
+          if (ok0) crow[col] = (p.beta == 0.0 ? 0.0 : p.beta * crow[col]) + p.alpha * x;
+          if (ok1) crow[col + 1] = (p.beta == 0.0 ? 0.0 : p.beta * crow[col + 1]) + p.alpha * y;
         }
       }
     }
   }
+#undef PCOL
+#undef ACCX
+#undef ACCY
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
@@ -507,7 +557,10 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
   // Small launches (the critical-path GEMMs inside TRSM/POTRF) split K so that
   // they still cover the SMs: each slice keeps >= 8 K-steps of 16.
   p.ksplit = 1;
-  if (beta == 1.0) {
+  // the full-inverse TRSM (square TRI product, beta = 1 into a zeroed X): K-weighted
+  // slices instead of a uniform split-K
+  p.tri_split = (TRI && beta == 1.0 && N == K && N % BN == 0 && M % BM == 0) ? 1 : 0;
+  if (beta == 1.0 && !p.tri_split) {
     const int tiles = p.tiles_per_task * n, ksteps = (K + BK - 1) / BK;
     while (tiles * p.ksplit * 2 <= num_sms() && ksteps / (p.ksplit * 2) >= 8) p.ksplit *= 2;
   }
@@ -515,14 +568,14 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
   if (p.cpref)
     for (int i = 0; i < n; ++i)
       if (!make_tmap_f64_2d(&p.t[i].c, d[i].C, N, M, d[i].ldc, 16, BM, true)) return cudaErrorInvalidValue;
-  const int total = p.tiles_per_task * n * p.ksplit;
+  const int total = p.tri_split ? n * tm * (tn * (tn + 1) / 2) : p.tiles_per_task * n * p.ksplit;
   // persistent CTAs, at most tiles_per_cta() output tiles each: the operand
   // ring streams the next tile during the epilogue, while SMs still free up
   // often enough for high-priority (critical-path) kernels to get in
   const int per = tiles_per_cta(total, K);
   const int grid = (total + per - 1) / per;
   count_launch();
-  count_gemm_path(p.cpref != 0, per, p.ksplit, TRI, lower, TB, n, total);
+  count_gemm_path(p.cpref != 0, per, p.tri_split ? 2 : p.ksplit, TRI, lower, TB, n, total);
   dgemm_dmma_kernel<TB, G, TRI><<<grid, THREADS, SMEM_BYTES, stream>>>(p);
   return cudaGetLastError();
 }
