@@ -172,6 +172,14 @@ class ComputeEngine:
             return n
         return 0
 
+    def worker_stride(self) -> int:
+        """Trace worker ids are device * stride + stream (all stream classes of a GPU:
+        normal, high-priority, cooperative, prefetch)."""
+        n = self.streams_per_device
+        urgent = max(2, n // 4) if n >= 2 else 0
+        coop = 0 if self.backend == "sim" else 2
+        return n + urgent + coop
+
     def stats(self, dev: int = 0) -> dict:
         st = N.DevStats()
         N.check(N.lib.sfx_stats(self._h, dev, ctypes.byref(st)), self._h)

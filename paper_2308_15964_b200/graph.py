@@ -24,13 +24,18 @@ import numpy as np
 from . import _native as N
 
 try:  # CPython fast path for single-task submits (csrc/pyext/sfxfast.c); ctypes otherwise
-    from ._sfxfast import submit1 as _fast_submit1
+    from . import _sfxfast
+    _fast_submit1 = _sfxfast.submit1
+    _fast_task = _sfxfast.task
 except ImportError:  # pragma: no cover - the build makes it next to libsfx.so
-    _fast_submit1 = None
+    _sfxfast = _fast_submit1 = _fast_task = None
 from . import memory
 from . import ops as ops_mod
 from .access import _CODES as _MODE_CODE
 from .access import AccessMode, AccessSpec
+
+if _sfxfast is not None:
+    _sfxfast.bind_types(AccessSpec, ops_mod.Op)
 from .errors import (
     ConfigurationError,
     DuplicateAccessError,
@@ -45,6 +50,8 @@ _id_lock = threading.Lock()
 
 
 def _next_tid() -> int:
+    if _sfxfast is not None:  # one process-global counter with the native fast path
+        return _sfxfast.reserve_tids(1)
     with _id_lock:
         return next(_tid_counter)
 
@@ -52,6 +59,8 @@ def _next_tid() -> int:
 def _reserve_tids(n: int) -> int:
     """First of ``n`` consecutive process-global task ids."""
     global _tid_counter
+    if _sfxfast is not None:
+        return _sfxfast.reserve_tids(n)
     with _id_lock:
         first = next(_tid_counter)
         _tid_counter = itertools.count(first + n)
@@ -190,7 +199,9 @@ class TaskGraph:
         self.engine = None
         self._h = None
         self._gid = None
-        self._entries = {}  # id(obj) -> _Entry
+        self._entries = {}  # id(obj) (or (id(obj), element)) -> _Entry
+        self._hid_by_id = {}  # id(obj) -> hid of whole objects (the native fast path's lookup)
+        self._hval = None
         self._by_hid = {}
         self._names = {}
         self._name_ranges = []  # (first tid, count, name) of array submissions
@@ -258,6 +269,8 @@ class TaskGraph:
                                    desc.ld, desc.dtype), self._h)
         e = _Entry(hid, obj, desc, parent)
         self._entries[id(obj) if key is None else key] = e
+        if key is None:
+            self._hid_by_id[id(obj)] = hid
         self._by_hid[hid] = e
         return e
 
@@ -286,6 +299,7 @@ class TaskGraph:
         self._flush_batch()
         N.check(N.lib.sfx_unregister(self._h, e.hid), self._h)
         del self._entries[id(obj)]
+        self._hid_by_id.pop(id(obj), None)
         del self._by_hid[e.hid]
 
     def hid_of(self, obj) -> int:
@@ -302,6 +316,17 @@ class TaskGraph:
 
     # -- insertion (graph.py:77-166) -------------------------------------------
     def task(self, *accesses, host=None, device=None, priority: int = 0, name=None):
+        # native fast path (csrc/pyext/sfxfast.c): every object already registered,
+        # no array views -> access codes, handle ids, a task id and the submit in C;
+        # anything else (first use, views, errors) takes the Python path below
+        if _fast_task is not None and host is None and self._hval is not None and self._batch is None:
+            tid = _fast_task(self._hval, self._gid, self._hid_by_id, self._tids, accesses, device, priority)
+            if tid > 0:
+                if name is not None:
+                    self._names[tid] = name
+                return TaskViewer(self, tid)
+            if tid < -1:
+                N.check(tid, self._h)
         if __debug__:
             ident = threading.get_ident()
             if self._inserter_ident != ident:
@@ -341,8 +366,7 @@ class TaskGraph:
                 raise DuplicateAccessError(f"task declares {type(spec.obj).__name__} twice")
             hids.append(hid)
             modes.append(code)
-        with _id_lock:  # _reserve_tids swaps the counter under this lock
-            tid = next(_tid_counter)
+        tid = _next_tid()
         if name is not None:
             self._names[tid] = name
         self._tids.append(tid)
@@ -540,7 +564,7 @@ class TaskGraph:
 
         return generate_dot(self, path, show_deps)
 
-    def generate_trace_svg(self, path=None, show_dep_arrows: bool = False) -> str:
+    def generate_trace_svg(self, path=None, show_dep_arrows: bool = False, out=None) -> str:
         from .trace import generate_trace_svg
 
-        return generate_trace_svg(self, path, show_dep_arrows)
+        return generate_trace_svg(self, path, show_dep_arrows, out)

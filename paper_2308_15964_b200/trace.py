@@ -70,7 +70,53 @@ def build_ready_steps(events):
     return steps
 
 
-def render_trace_svg(graph, show_dep_arrows: bool = False) -> str:
+def _union_ns(intervals):
+    """Total length of the union of [start, end] intervals (group members share one
+    start/end pair, and launch groups on one stream may overlap their waits)."""
+    total, cur_s, cur_e = 0, None, None
+    for start, end in sorted(intervals):
+        if cur_e is None or start > cur_e:
+            if cur_e is not None:
+                total += cur_e - cur_s
+            cur_s, cur_e = start, end
+        else:
+            cur_e = max(cur_e, end)
+    if cur_e is not None:
+        total += cur_e - cur_s
+    return total
+
+
+def idle_report(graph, events=None):
+    """Per-lane and per-GPU idle time (reference trace.py:292-300 prints one idle
+    scalar per worker; a lane here is one CUDA stream of one GPU, and a GPU is
+    busy while any of its streams runs a task).  Times from the tasks' CUDA
+    start/end events; span = first to last event of the graph.  Returns
+    {"span_ms", "lanes": {label: (busy_ms, idle_ms)}, "gpus": {d: (busy_ms, idle_ms)}}."""
+    events = graph.trace.export_events() if events is None else events
+    lanes = build_lanes(events)
+    t_lo = min([e[1] for e in events], default=0)
+    t_hi = max([e[1] for e in events], default=0)
+    span = max(t_hi - t_lo, 1)
+    nstreams = graph.engine.worker_stride() if graph.engine else 1
+    out = {"span_ms": span / 1e6, "lanes": {}, "gpus": {}}
+    per_dev = {}
+    for wid in sorted(lanes):
+        iv = [(a, b) for a, b, _ in lanes[wid]]
+        busy = _union_ns(iv)
+        out["lanes"][f"gpu{wid // nstreams} s{wid % nstreams}"] = (busy / 1e6, (span - busy) / 1e6)
+        per_dev.setdefault(wid // nstreams, []).extend(iv)
+    for d, iv in sorted(per_dev.items()):
+        busy = _union_ns(iv)
+        out["gpus"][d] = (busy / 1e6, (span - busy) / 1e6)
+    return out
+
+
+def render_trace_svg(graph, show_dep_arrows: bool = False, out=None) -> str:
+    """Timeline SVG: one lane per (GPU, stream) with the tasks' CUDA-event
+    intervals, the ready-count curve beneath; prints the idle metric per lane
+    and per GPU to ``out`` (stdout by default), like the reference's extension."""
+    import sys
+
     events = graph.trace.export_events()
     lanes = build_lanes(events)
     steps = build_ready_steps(events)
@@ -93,7 +139,7 @@ def render_trace_svg(graph, show_dep_arrows: bool = False) -> str:
              f'viewBox="0 0 {width} {height}">',
              f'<rect x="0" y="0" width="{width}" height="{height}" fill="white"/>']
     pos = {}
-    nstreams = max(1, graph.engine.streams_per_device) if graph.engine else 1
+    nstreams = graph.engine.worker_stride() if graph.engine else 1
     for i, wid in enumerate(wids):
         y = lane_y(i)
         parts.append(f'<text x="6" y="{y + lane_h * 0.7:.1f}" font-size="11" font-family="sans-serif">'
@@ -121,11 +167,18 @@ def render_trace_svg(graph, show_dep_arrows: bool = False) -> str:
                  f'ready tasks (max {max_count})</text>')
     parts.append(f'<polyline points="{" ".join(pts)}" fill="none" stroke="#c44" stroke-width="1.2"/>')
     parts.append("</svg>")
+    rep = idle_report(graph, events)
+    out = sys.stdout if out is None else out
+    for label, (busy, idle) in rep["lanes"].items():
+        print(f"[trace] {label}: idle {idle:.3f} ms of {rep['span_ms']:.3f} ms", file=out)
+    for d, (busy, idle) in rep["gpus"].items():
+        print(f"[trace] gpu{d} (any stream busy): idle {idle:.3f} ms of {rep['span_ms']:.3f} ms "
+              f"({100.0 * busy / max(rep['span_ms'], 1e-12):.1f} % busy)", file=out)
     return "\n".join(parts) + "\n"
 
 
-def generate_trace_svg(graph, path=None, show_dep_arrows: bool = False) -> str:
-    text = render_trace_svg(graph, show_dep_arrows)
+def generate_trace_svg(graph, path=None, show_dep_arrows: bool = False, out=None) -> str:
+    text = render_trace_svg(graph, show_dep_arrows, out)
     if path is not None:
         with open(path, "w", encoding="utf-8") as fh:
             fh.write(text)

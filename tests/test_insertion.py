@@ -30,6 +30,7 @@ def _capture(graph):
 
     graph.submit_arrays = submit_arrays
     graph._submit_one = submit_one
+    graph._hval = None  # no native task() fast path: every task goes through _submit_one
     return seq
 
 
