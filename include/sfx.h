@@ -250,7 +250,10 @@ int sfx_violations(sfx_runtime* rt, uint64_t* n);
  * looked at, default 64), "kernel_timing" (0/1: launch-group timing events,
  * as SFX_FLAG_KTIME; always on while tracing), "stream_affinity" (0/1, default 1:
  * a task whose predecessor is in flight on a stream of its class is launched
- * on that stream) */
+ * on that stream), "deterministic" (0/1, default 0: no order-dependent FP64
+ * accumulation -- the particle ops run one-sided atomic-free kernels under
+ * exclusive commutative guards and no DGEMM splits K; with one stream and the
+ * FIFO scheduler repeated runs are bitwise identical) */
 int sfx_set_option(sfx_runtime* rt, const char* key, int64_t value);
 
 /* external tasks (SFX_OP_EXTERN): block up to timeout_s (< 0: forever) until at

@@ -473,6 +473,12 @@ namespace {
 
 }  // namespace
 
+namespace {
+thread_local bool t_deterministic = false;
+}
+void set_deterministic_launches(bool on) { t_deterministic = on; }
+bool deterministic_launches() { return t_deterministic; }
+
 // launch-configuration counters (sfx_gemm_paths): which kernel path ran, so the
 // parity tests can prove that they exercised the benchmarked configuration
 std::atomic<unsigned long long> g_gemm_paths[SFX_GEMM_PATHS];
@@ -559,8 +565,9 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
   p.ksplit = 1;
   // the full-inverse TRSM (square TRI product, beta = 1 into a zeroed X): K-weighted
   // slices instead of a uniform split-K
-  p.tri_split = (TRI && beta == 1.0 && N == K && N % BN == 0 && M % BM == 0) ? 1 : 0;
-  if (beta == 1.0 && !p.tri_split) {
+  const bool det = deterministic_launches();
+  p.tri_split = (!det && TRI && beta == 1.0 && N == K && N % BN == 0 && M % BM == 0) ? 1 : 0;
+  if (beta == 1.0 && !p.tri_split && !det) {
     const int tiles = p.tiles_per_task * n, ksteps = (K + BK - 1) / BK;
     while (tiles * p.ksplit * 2 <= num_sms() && ksteps / (p.ksplit * 2) >= 8) p.ksplit *= 2;
   }

@@ -16,6 +16,13 @@ inline void count_launch() { g_kernel_launches.fetch_add(1, std::memory_order_re
 // DGEMM launch-path counters (SFX_GEMM_* in sfx.h)
 extern std::atomic<unsigned long long> g_gemm_paths[];
 
+// Deterministic mode (runtime option "deterministic"): set by the backend around
+// a task's launches on the launching thread.  Launchers then avoid every
+// order-dependent FP64 accumulation: no split-K atomics in the DGEMMs (TRSM,
+// POTRF's inverse doubling included), one-sided atomic-free particle kernels.
+void set_deterministic_launches(bool on);
+bool deterministic_launches();
+
 bool make_tmap_f64_2d(CUtensorMap* tm, const double* base, uint64_t inner, uint64_t outer, uint64_t ld,
                       uint32_t box_inner, uint32_t box_outer, bool swizzle128);
 

@@ -182,6 +182,88 @@ __device__ __forceinline__ void run_block(const P2PArgs& A, int ba, int bb, doub
   }
 }
 
+// ---- deterministic one-sided evaluation (runtime option "deterministic") ----
+// Every target is owned by ONE thread of ONE CTA, which walks all sources of the
+// other side in a fixed order (staged through shared memory, broadcast reads)
+// and finally adds its sums into F with a plain read-modify-write: no atomics,
+// so the result is bitwise repeatable.  A pair task is two passes in one
+// launch (CTAs for the targets of side i with sources j, then the reverse); it
+// costs the one-directional 21 FP64 ops per ORDERED interaction instead of
+// 11.5, the price of the fixed order.  The runtime runs commutative members
+// one at a time in this mode (exclusive guards), so the plain update is safe.
+constexpr int DET_THREADS = 256;
+constexpr int DET_TPT = 2;  // targets per thread
+constexpr int DET_BLK = DET_THREADS * DET_TPT;
+constexpr int DET_CHUNK = 256;  // sources staged per round
+
+struct DetArgs {
+  const double* pt;  // targets: 4 x nt
+  const double* ps;  // sources: 4 x ns
+  double* ft;
+  long long ld_pt, ld_ps, ld_ft;
+  int nt, ns;
+  int self;  // the source set is the target set: skip a == b
+  double eps2;
+};
+
+__global__ void __launch_bounds__(DET_THREADS) p2p_det_kernel(DetArgs A0, DetArgs A1, int nblk0) {
+  __shared__ double sx[DET_CHUNK], sy[DET_CHUNK], sz[DET_CHUNK], sq[DET_CHUNK];
+  const bool second = static_cast<int>(blockIdx.x) >= nblk0;
+  const DetArgs& A = second ? A1 : A0;
+  const int blk = second ? blockIdx.x - nblk0 : blockIdx.x;
+  double x[DET_TPT], y[DET_TPT], z[DET_TPT], q[DET_TPT], fx[DET_TPT], fy[DET_TPT], fz[DET_TPT], pt[DET_TPT];
+  int ia[DET_TPT];
+#pragma unroll
+  for (int u = 0; u < DET_TPT; ++u) {
+    ia[u] = blk * DET_BLK + u * DET_THREADS + threadIdx.x;
+    const bool ok = ia[u] < A.nt;
+    const int t = ok ? ia[u] : 0;
+    x[u] = A.pt[t];
+    y[u] = A.pt[A.ld_pt + t];
+    z[u] = A.pt[2 * A.ld_pt + t];
+    q[u] = A.pt[3 * A.ld_pt + t];
+    fx[u] = fy[u] = fz[u] = pt[u] = 0.0;
+  }
+  for (int c0 = 0; c0 < A.ns; c0 += DET_CHUNK) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < DET_CHUNK; e += DET_THREADS) {
+      const int j = c0 + e;
+      const bool ok = j < A.ns;
+      sx[e] = ok ? A.ps[j] : FAR;
+      sy[e] = ok ? A.ps[A.ld_ps + j] : FAR;
+      sz[e] = ok ? A.ps[2 * A.ld_ps + j] : FAR;
+      sq[e] = ok ? A.ps[3 * A.ld_ps + j] : 0.0;
+    }
+    __syncthreads();
+    const int cn = min(DET_CHUNK, A.ns - c0);
+    for (int e = 0; e < cn; ++e) {
+      const double bx = sx[e], by = sy[e], bz = sz[e], bq = sq[e];
+#pragma unroll
+      for (int u = 0; u < DET_TPT; ++u) {
+        const double dx = x[u] - bx, dy = y[u] - by, dz = z[u] - bz;
+        const double r2 = fma(dx, dx, fma(dy, dy, fma(dz, dz, A.eps2)));
+        double w = rsqrt_fast(r2);
+        if (A.self && c0 + e == ia[u]) w = 0.0;
+        const double pb = bq * w;
+        const double s = q[u] * pb * w * w;
+        pt[u] += pb;
+        fx[u] = fma(s, dx, fx[u]);
+        fy[u] = fma(s, dy, fy[u]);
+        fz[u] = fma(s, dz, fz[u]);
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < DET_TPT; ++u) {
+    const int t = ia[u];
+    if (t >= A.nt) continue;
+    A.ft[t] += fx[u];
+    A.ft[A.ld_ft + t] += fy[u];
+    A.ft[2 * A.ld_ft + t] += fz[u];
+    A.ft[3 * A.ld_ft + t] += pt[u];
+  }
+}
+
 constexpr int MAX_GROUP = 32;
 
 // One launch for up to MAX_GROUP tasks of the same op (grouped by the
@@ -271,6 +353,20 @@ cudaError_t launch_p2p_group(const P2PDesc* d, int ntasks, bool self, double eps
 
 cudaError_t launch_p2p(const double* Pi, long long ldpi, int ni, const double* Pj, long long ldpj, int nj, double* Fi,
                        long long ldfi, double* Fj, long long ldfj, bool self, double eps2, cudaStream_t s) {
+  if (deterministic_launches()) {
+    if (ni <= 0 || (!self && nj <= 0)) return cudaSuccess;
+    DetArgs a0{Pi, self ? Pi : Pj, Fi, ldpi, self ? ldpi : ldpj, ldfi, ni, self ? ni : nj, self ? 1 : 0, eps2};
+    DetArgs a1 = a0;
+    const int nb0 = (ni + DET_BLK - 1) / DET_BLK;
+    int blocks = nb0;
+    if (!self) {
+      a1 = DetArgs{Pj, Pi, Fj, ldpj, ldpi, ldfj, nj, ni, 0, eps2};
+      blocks += (nj + DET_BLK - 1) / DET_BLK;
+    }
+    count_launch();
+    p2p_det_kernel<<<blocks, DET_THREADS, 0, s>>>(a0, a1, nb0);
+    return cudaGetLastError();
+  }
   P2PDesc d{Pi, ldpi, ni, Pj, ldpj, nj, Fi, ldfi, Fj, ldfj};
   return launch_p2p_group(&d, 1, self, eps2, s);
 }

@@ -293,6 +293,13 @@ class CudaBackend : public Backend {
   }
 
   int launch(int d, int stream, const OpLaunch& op, std::string& err) override {
+    set_deterministic_launches(op.deterministic);
+    const int rc = launch_op(d, stream, op, err);
+    set_deterministic_launches(false);
+    return rc;
+  }
+
+  int launch_op(int d, int stream, const OpLaunch& op, std::string& err) {
     cudaStream_t s = devs_[d]->streams[stream];
     const Operand* o = op.o;
     auto f64 = [](const Operand& x) { return static_cast<double*>(x.dptr); };
@@ -402,6 +409,13 @@ class CudaBackend : public Backend {
   }
 
   int launch_group(int d, int stream, const std::vector<OpLaunch>& ops, std::string& err) override {
+    set_deterministic_launches(ops[0].deterministic);
+    const int rc = launch_group_op(d, stream, ops, err);
+    set_deterministic_launches(false);
+    return rc;
+  }
+
+  int launch_group_op(int d, int stream, const std::vector<OpLaunch>& ops, std::string& err) {
     const OpLaunch& f = ops[0];
     if (ops.size() > 1 && (f.op == SFX_OP_DGEMM || f.op == SFX_OP_DSYRK)) {
       std::vector<GemmDesc> g(ops.size());

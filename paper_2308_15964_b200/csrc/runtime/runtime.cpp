@@ -564,7 +564,7 @@ int Runtime::submit(uint32_t n, const sfx_task_desc* descs, const sfx_access* ac
     std::vector<std::pair<Handle*, uint8_t>> guards;
     for (auto& a : t->acc) {
       if (a.mode == SFX_COMMUTATIVE_WRITE)
-        guards.emplace_back(a.h, accumulates_atomically(t->op) ? 1 : 0);
+        guards.emplace_back(a.h, shared_accum(t->op) ? 1 : 0);
       else if (a.mode == SFX_ATOMIC_WRITE && ndev_ > 1)
         guards.emplace_back(a.h, 1);
     }
@@ -1149,7 +1149,7 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
     b->dirty = true;
     h->dirty_dev = d;
     h->host_valid = false;
-    if (m == SFX_COMMUTATIVE_WRITE && !accumulates_atomically(t->op)) h->commute_last = t->end;
+    if (m == SFX_COMMUTATIVE_WRITE && !shared_accum(t->op)) h->commute_last = t->end;
     if (m == SFX_WRITE || m == SFX_MAYBE_WRITE) b->ready = t->end;
   }
 
@@ -1161,6 +1161,7 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
     fprintf(stderr, " waits=%zu\n", t->waits.size());
   }
   op.op = t->op;
+  op.deterministic = deterministic_;
   op.n = static_cast<int>(std::min<size_t>(t->acc.size(), 8));
   if (t->op == SFX_OP_DPOTRF && t->status_slot < 0) t->status_slot = be_->status_alloc(d);
   op.status_slot = t->status_slot;
@@ -1253,7 +1254,7 @@ bool Runtime::groupable(const Task* t) const {
     case SFX_OP_ZERO:
     case SFX_OP_P2P_PAIR:  // grouped mutual P2P kernel; commutative guards in shared mode
     case SFX_OP_P2P_SELF:
-      return group_max_ > 1;
+      return group_max_ > 1 && !deterministic_;  // deterministic: one-sided kernel per task
     default:
       return false;
   }
@@ -2045,6 +2046,8 @@ int Runtime::set_option(const std::string& key, int64_t value) {
   } else if (key == "kernel_timing") {
     // launch-group timing events (SFX_FLAG_KTIME); tracing keeps them on
     ktime_ = trace_ || value != 0;
+  } else if (key == "deterministic") {
+    deterministic_ = value != 0;
   } else if (key == "stream_affinity") {
     stream_affinity_ = value != 0;
   } else if (key == "window") {

@@ -176,6 +176,7 @@ struct OpLaunch {
   uint32_t op = 0;
   int n = 0;
   int status_slot = -1;  // Backend::status_alloc slot the kernel reports into (DPOTRF info)
+  bool deterministic = false;  // Runtime deterministic mode: order-independent launches
   Operand o[8];
   double fp[4];
   int64_t ip[4];
@@ -368,6 +369,12 @@ class Runtime {
   // co-resident, so their grid barriers can never starve each other)
   int ncoop_ = 2;
   bool stream_affinity_ = true;  // successors join their in-flight predecessor's stream
+  // deterministic mode: no order-dependent FP64 accumulation anywhere -- ops that
+  // normally accumulate with device atomics run one-sided kernels under
+  // exclusive guards, DGEMMs never split K (OpLaunch::deterministic); with one
+  // stream and FIFO order repeated runs are bitwise identical
+  bool deterministic_ = false;
+  bool shared_accum(uint32_t op) const { return !deterministic_ && accumulates_atomically(op); }
   bool is_coop(const Task* t) const;
   // Prefetch: while every stream is busy, the executor stages host-resident
   // operands of tasks waiting in its queue on a dedicated copy stream, so PCIe

@@ -72,7 +72,7 @@ class ComputeEngine:
 
     def __init__(self, team, scheduler=None, device_memory=None, *, backend: str = "cuda",
                  trace: bool = True, window: int = 0, ordinals=None, arena_align: int = 0,
-                 group_max: int = 32, kernel_timing: bool = False):
+                 group_max: int = 32, kernel_timing: bool = False, deterministic: bool = False):
         if isinstance(team, (list, tuple)):
             team = WorkerTeam(team)
         devices = team.device_indexes()
@@ -117,6 +117,8 @@ class ComputeEngine:
                                  flags, int(window), ctypes.byref(handle)))
         self._h = handle
         self.set_option("group_max", group_max)
+        if deterministic:  # no order-dependent FP64 accumulation (runtime option, sfx.h)
+            self.set_option("deterministic", 1)
         # runtime knobs from the environment (experiments): SFX_OPT_<KEY>=<int>
         for key, value in os.environ.items():
             if key.startswith("SFX_OPT_"):

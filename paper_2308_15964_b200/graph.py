@@ -219,6 +219,13 @@ class TaskGraph:
         self.comm = None
         self.history = history
 
+    def set_trace(self, enabled: bool) -> "TaskGraph":
+        """Switch event recording on or off for the tasks inserted from now on."""
+        self.trace.enabled = bool(enabled)
+        if self.engine is not None:
+            N.check(N.lib.sfx_graph_option(self._h, self._gid, b"trace", 1 if enabled else 0), self._h)
+        return self
+
     # -- inter-process communication (graph.py:264-284, comms.py) -------------
     def use_comm(self, comm) -> "TaskGraph":
         """Bind to a communicator (comms.TorchComm) for send/recv/broadcast tasks."""
