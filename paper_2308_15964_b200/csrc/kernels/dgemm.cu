@@ -34,6 +34,17 @@
 namespace sfx {
 namespace {
 
+// NN B-operand layout.  Default (0): four LDS.64 per sub-step, 2-way bank
+// conflicted.  1: column-permuted operands, two conflict-free LDS.128 per
+// sub-step -- measured SLOWER on C2 (roofline frac 0.876-0.882 vs 0.903-0.908,
+// tools/r2c_ab.sh; ncu: 1.3 M vs 5.1 M bank conflicts per launch but DMMA pipe
+// 88.2 % vs 90.4 % of active cycles: the LDS path is not the limit, the k-pair
+// swaps (FSEL) and the longer operand live ranges cost more).  Kept for A/B.
+#ifndef SFX_NN_COLPERM
+#define SFX_NN_COLPERM 0
+#endif
+constexpr bool NN_COLPERM = SFX_NN_COLPERM != 0;
+
 constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3;
 constexpr int CONSUMER_WARPS = 8;
 // one producer warpgroup (4 warps, one elected TMA lane) + two DMMA warpgroups;
@@ -72,6 +83,8 @@ struct GemmGroup {
   int tiles_n, tiles_per_task;
   int lower;
   int cpref;  // C tiles of interior output tiles are prefetched by TMA (beta != 0, ksplit == 1, !lower)
+  int zero;     // always 0 at run time (the compiler cannot know): see the stage release
+  int release;  // stage release: 0 = data-dependent arrive (default), 1 = fence.acq_rel.cta (A/B experiments)
   double alpha, beta;
 };
 
@@ -199,14 +212,14 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
   asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
   const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warp grid, warp tile 64 x 32
   const int g = lane >> 2, t = lane & 3;
-  const int sw = TRANS_B ? 0 : (t >> 1);  // NN: k order within a pair (see the B loads)
+  const int sw = (TRANS_B || !NN_COLPERM) ? 0 : (t >> 1);  // NN: k order within a pair (see the B loads)
   // output columns (within the warp's 32) of this thread's accumulator pair P =
   // 0..3 (two adjacent columns each): NT: fragment j = P, columns 8P + 2t (+1);
   // NN (column permutation of the B loads): columns 8t + 2P (+1), i.e. a row's 8
   // values of one thread are contiguous
-#define PCOL(P) (TRANS_B ? 8 * (P) + 2 * t : 8 * t + 2 * (P))
-#define ACCX(i, P) (TRANS_B ? acc[i][P][0] : acc[i][2 * ((P)&1)][(P) >> 1])
-#define ACCY(i, P) (TRANS_B ? acc[i][P][1] : acc[i][2 * ((P)&1) + 1][(P) >> 1])
+#define PCOL(P) ((TRANS_B || !NN_COLPERM) ? 8 * (P) + 2 * t : 8 * t + 2 * (P))
+#define ACCX(i, P) ((TRANS_B || !NN_COLPERM) ? acc[i][P][0] : acc[i][2 * ((P)&1)][(P) >> 1])
+#define ACCY(i, P) ((TRANS_B || !NN_COLPERM) ? acc[i][P][1] : acc[i][2 * ((P)&1) + 1][(P) >> 1])
   int it = 0, cn = 0;
   for (int lin = blockIdx.x; lin < total; lin += gridDim.x) {
     int task, m0, n0, kt0, kt1;
@@ -225,6 +238,7 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
       // operands (true k = sigma(t, h, e) = 4t + 2h + (e ^ sw)): ordered shared
       // loads; the DMMAs are not volatile, so ptxas can slide this half's DMMAs
       // past the next loads
+      uint32_t dep = 0;  // OR of the high words of every operand loaded in the second half
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         double a[8][2], b[4][2];
@@ -232,6 +246,7 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
         for (int i = 0; i < 8; ++i) {
           const int r = wm * 64 + 8 * i + g;  // r % 8 == g
           const double2 v = ptx::lds128(aS + r * 128 + (((2 * t + h) ^ g) << 4));
+          if (h == 1) dep |= static_cast<uint32_t>(__double2hiint(v.x));
           a[i][0] = sw ? v.y : v.x;
           a[i][1] = sw ? v.x : v.y;
         }
@@ -240,8 +255,26 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
           for (int j = 0; j < 4; ++j) {
             const int r = wn * 32 + 8 * j + g;
             const double2 v = ptx::lds128(bS + r * 128 + (((2 * t + h) ^ g) << 4));
+            if (h == 1) dep |= static_cast<uint32_t>(__double2hiint(v.x));
             b[j][0] = v.x;
             b[j][1] = v.y;
+          }
+        } else if (!NN_COLPERM) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int n = wn * 32 + 8 * j + g;
+            const int q = n >> 4, nn = n & 15;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int k = 4 * t + 2 * h + e;
+              double v = ptx::lds64(bS + q * 2048 + k * 128 + (((nn >> 1) ^ (k & 7)) << 4) + (nn & 1) * 8);
+              if (h == 1) dep |= static_cast<uint32_t>(__double2hiint(v));
+              if (TRI) {
+                const int kg = kt * BK + k, ng = n0 + n;
+                v = kg > ng ? 0.0 : (kg == ng ? 1.0 / v : v);
+              }
+              b[j][e] = v;
+            }
           }
         } else {
           // NN: B stored [K][N] in 16-column TMA boxes (128B swizzle).  Thread
@@ -259,6 +292,7 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
               const int n = wn * 32 + 4 * g + 2 * jp;
               const int nn = n & 15;
               const double2 v = ptx::lds128(bS + (n >> 4) * 2048 + k * 128 + (((nn >> 1) ^ (k & 7)) << 4));
+              if (h == 1) dep |= static_cast<uint32_t>(__double2hiint(v.x));
               double b0 = v.x, b1 = v.y;
               if (TRI) {  // masked only on the k-steps that cross the diagonal
                 const int kg = kt * BK + k, ng = n0 + n;
@@ -280,18 +314,24 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
             for (int j = 0; j < 4; ++j) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i][e], b[j][e]);
           if (h == 1 && e == 0) {
             // Release the stage (one arrive per warp) only once every shared load
-            // this warp issued from it has COMPLETED.  An mbarrier arrive does not
-            // wait for in-flight ld.shared results: arriving right after the last
-            // load let the producer's next TMA overwrite rows the warp had not read
-            // yet (round 1: rows 56-63 of C tiles = the last A fragment, wrong by
-            // ~1e-4 relative, only with 2 output tiles per CTA where the producer
-            // runs ahead into the next tile; tools/c2_check.py).  The fence makes
-            // each lane wait for its outstanding loads (MEMBAR.ALL.CTA), __syncwarp
-            // orders the lanes before lane 0 arrives.  Placed after the first half
-            // of this k-step's DMMAs, which need those registers anyway.
-            ptx::fence_cta();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&empty[s]);
+            // this warp issued from it has COMPLETED: an mbarrier arrive does not
+            // wait for in-flight ld.shared results, and arriving right after the
+            // last load let the producer's next TMA overwrite rows not yet read
+            // (round 1: rows 56-63 of C tiles wrong by ~1e-4, only with 2 output
+            // tiles per CTA; tools/c2_check.py).  The arrive's ADDRESS depends on
+            // every operand loaded in this half (dep & zero == 0 at run time, but
+            // the compiler cannot fold it), so the instruction computing it waits
+            // on the warp's load scoreboards -- for all 32 lanes, scoreboards are
+            // per warp -- and no fence is needed.  release == 1: the previous
+            // fence.acq_rel.cta + __syncwarp variant (MEMBAR, also waits for the
+            // epilogue's global stores), kept for A/B measurements.
+            if (p.release == 1) {
+              ptx::fence_cta();
+              __syncwarp();
+              if (lane == 0) ptx::mbar_arrive(&empty[s]);
+            } else if (lane == 0) {
+              ptx::mbar_arrive_addr(ptx::smem_u32(&empty[s]) + (dep & static_cast<uint32_t>(p.zero)));
+            }
           }
         }
       }
@@ -556,6 +596,9 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
   p.beta = beta;
   p.lower = lower ? 1 : 0;
   p.tri = tri ? 1 : 0;
+  p.zero = 0;
+  static const int release_mode = getenv("SFX_GEMM_RELEASE") ? atoi(getenv("SFX_GEMM_RELEASE")) : 0;
+  p.release = release_mode;
   const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
   p.tiles_n = tn;
   p.tiles_per_task = lower ? tm * (tm + 1) / 2 : tm * tn;

@@ -72,6 +72,14 @@ bool fullinv_supported(int n);
 size_t fullinv_workspace_bytes(int n);
 cudaError_t launch_dpotrf_fullinv(double* A, long long lda, int n, int* info, void* workspace, size_t ws_bytes,
                                   cudaStream_t s);
+// dataflow DPOTRF (potrf_flow.cu): one cooperative launch, 64x64 block tasks
+// ordered by flags; store_inv 0 = LAPACK 'L', 1 = 64x64 diagonal-block inverses,
+// 2 = full inv(L)^T in the strict upper triangle.  workspace: a zero-initialised
+// stream scratch (the flags live at its top and are cleared by every launch)
+bool flow_supported(int n);
+size_t flow_workspace_bytes(int n);
+cudaError_t launch_dpotrf_flow(double* A, long long lda, int n, int* info, void* workspace, size_t ws_bytes,
+                               cudaStream_t s, int store_inv);
 cudaError_t launch_dtrsm_fullinv(const double* L, long long ldl, double* B, long long ldb, int M, int n, void* scratch,
                                  size_t bytes, cudaStream_t s);
 cudaError_t launch_dtrsm_coop_group(const TrsmDesc* d, int ntasks, int M, int n, void* workspace, size_t ws_bytes,

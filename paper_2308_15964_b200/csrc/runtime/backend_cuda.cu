@@ -383,7 +383,12 @@ class CudaBackend : public Backend {
         break;
       case SFX_OP_DPOTRF: {
         int* info = status_ptr(d, op.status_slot);
-        if (op.ip[0] == 2 && devs_[d]->scratch[stream] && fullinv_supported(static_cast<int>(o[0].rows)))
+        static const bool old_potrf = getenv("SFX_POTRF") && !strcmp(getenv("SFX_POTRF"), "coop");  // A/B only
+        if (!old_potrf && devs_[d]->scratch[stream] && flow_supported(static_cast<int>(o[0].rows)) &&
+            o[0].ld % 2 == 0)
+          e = launch_dpotrf_flow(f64(o[0]), o[0].ld, static_cast<int>(o[0].rows), info, devs_[d]->scratch[stream],
+                                 kScratchBytes, s, op.ip[0]);
+        else if (op.ip[0] == 2 && devs_[d]->scratch[stream] && fullinv_supported(static_cast<int>(o[0].rows)))
           e = launch_dpotrf_fullinv(f64(o[0]), o[0].ld, static_cast<int>(o[0].rows), info, devs_[d]->scratch[stream],
                                     kScratchBytes, s);
         else if (devs_[d]->scratch[stream] && coop_supported(static_cast<int>(o[0].rows), static_cast<int>(o[0].rows)))

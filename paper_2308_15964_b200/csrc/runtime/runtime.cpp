@@ -1384,12 +1384,13 @@ void Runtime::complete(Task* t) {
                                   (unsigned long long)t->tid, info));
   }
   Graph* g = graphs_[t->gid].get();
+  auto when = [&](Sync* sy) { return sy->t_resolved ? sy->t_ns : be_->event_time_ns(t->dev, sy->event); };
   if (ktime_ && t->start && t->end) {
     D.stats.timed_tasks += 1;
     if (!t->end->group_timed) {
       t->end->group_timed = true;
-      const int64_t t0 = be_->event_time_ns(t->dev, t->start->event);
-      const int64_t t1 = be_->event_time_ns(t->dev, t->end->event);
+      const int64_t t0 = when(t->start.get());
+      const int64_t t1 = when(t->end.get());
       const int64_t dt = t1 - t0;
       if (dt > 0) D.kintervals.emplace_back(t0, t1);
       D.stats.timed_groups += 1;
@@ -1397,8 +1398,8 @@ void Runtime::complete(Task* t) {
     }
   }
   if (trace_ && t->start && t->end) {
-    t->t_start = be_->event_time_ns(t->dev, t->start->event);
-    t->t_end = be_->event_time_ns(t->dev, t->end->event);
+    t->t_start = when(t->start.get());
+    t->t_end = when(t->end.get());
     const int wid = t->dev * (nstreams_ + nurgent_ + ncoop_) + t->stream;
     record(g, SFX_EV_START, t->t_start, wid, t->tid);
     record(g, SFX_EV_END, t->t_end, wid, t->tid);
@@ -1819,6 +1820,7 @@ void Runtime::comp_loop(int d) {
     Task* t = D.inflight.front();
     void* ev = t->end->event;
     SyncP keep = t->end;
+    SyncP keep_start = t->start;
     if (debug_staging())
       fprintf(stderr, "[sfx] comp wait task=%llu recorded=%d inflight=%zu\n", (unsigned long long)t->tid,
               t->end->recorded.load() ? 1 : 0, D.inflight.size());
@@ -1826,6 +1828,14 @@ void Runtime::comp_loop(int d) {
     std::string err;
     int rc = be_->event_sync(d, ev, err);
     if (debug_staging()) fprintf(stderr, "[sfx] comp synced task=%llu rc=%d\n", (unsigned long long)t->tid, rc);
+    // event timestamps (cudaEventElapsedTime) resolved here, before the lock: the
+    // inserter and the executors are not held up by them (once per launch group)
+    if (!rc && ktime_ && keep_start && !keep->t_resolved) {
+      keep->t_ns = be_->event_time_ns(d, keep->event);
+      keep_start->t_ns = be_->event_time_ns(d, keep_start->event);
+      keep_start->t_resolved = true;
+      keep->t_resolved = true;
+    }
     lk.lock();
     if (debug_staging()) fprintf(stderr, "[sfx] comp locked task=%llu\n", (unsigned long long)t->tid);
     const int64_t tc0 = now_ns();

@@ -69,6 +69,8 @@ struct Sync {
   bool complete = false;       // guarded by the runtime mutex
   bool group_counted = false;  // launch group already retired from its stream
   bool group_timed = false;    // launch group duration already accumulated (KTIME)
+  int64_t t_ns = 0;            // host-clock time of the event, resolved by the completion
+  bool t_resolved = false;     // thread OUTSIDE the runtime mutex (only it touches these)
   ~Sync();
 };
 using SyncP = std::shared_ptr<Sync>;
