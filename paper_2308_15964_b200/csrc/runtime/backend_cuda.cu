@@ -226,6 +226,15 @@ class CudaBackend : public Backend {
     }
     return true;
   }
+  int event_query(int, void* ev, std::string& err) override {
+    const cudaError_t e = cudaEventQuery(ev_of(ev));
+    if (e == cudaSuccess) return 1;
+    if (e == cudaErrorNotReady) {
+      cudaGetLastError();
+      return 0;
+    }
+    return cuda_err(e, "kernel execution", err);
+  }
   int64_t event_time_ns(int d, void* ev) override {
     float ms = 0;
     if (cudaEventElapsedTime(&ms, devs_[d]->base, ev_of(ev)) != cudaSuccess) {

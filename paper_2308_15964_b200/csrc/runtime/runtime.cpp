@@ -1808,8 +1808,20 @@ void Runtime::exec_loop(int d) {
 }
 
 void Runtime::comp_loop(int d) {
+  // Completion: a snapshot of the in-flight launch groups is polled OUTSIDE the
+  // runtime lock (cudaEventQuery; a blocking sync on the oldest one only when
+  // none has finished), their event times are resolved there too, and every
+  // finished task is then completed in ONE lock section -- in any order across
+  // streams, so a long group on one stream does not hold up the unpinning and
+  // guard hand-over of groups that finished on others.
   be_->bind_thread(d);
   Device& D = *devs_[d];
+  struct Item {
+    Task* t;
+    SyncP end, start;
+  };
+  std::vector<Item> snap;
+  std::vector<Sync*> done_syncs;
   std::unique_lock<std::mutex> lk(mu_);
   while (true) {
     D.comp_cv.wait(lk, [&] { return stopping_ || !D.inflight.empty(); });
@@ -1817,35 +1829,78 @@ void Runtime::comp_loop(int d) {
       if (stopping_) return;
       continue;
     }
-    Task* t = D.inflight.front();
-    void* ev = t->end->event;
-    SyncP keep = t->end;
-    SyncP keep_start = t->start;
-    if (debug_staging())
-      fprintf(stderr, "[sfx] comp wait task=%llu recorded=%d inflight=%zu\n", (unsigned long long)t->tid,
-              t->end->recorded.load() ? 1 : 0, D.inflight.size());
+    snap.clear();
+    const size_t K = std::min<size_t>(D.inflight.size(), 512);
+    for (size_t i = 0; i < K; ++i) {
+      Task* t = D.inflight[i];
+      snap.push_back(Item{t, t->end, t->start});
+    }
     lk.unlock();
     std::string err;
-    int rc = be_->event_sync(d, ev, err);
-    if (debug_staging()) fprintf(stderr, "[sfx] comp synced task=%llu rc=%d\n", (unsigned long long)t->tid, rc);
-    // event timestamps (cudaEventElapsedTime) resolved here, before the lock: the
-    // inserter and the executors are not held up by them (once per launch group)
-    if (!rc && ktime_ && keep_start && !keep->t_resolved) {
-      keep->t_ns = be_->event_time_ns(d, keep->event);
-      keep_start->t_ns = be_->event_time_ns(d, keep_start->event);
-      keep_start->t_resolved = true;
-      keep->t_resolved = true;
+    int rc = 0;
+    // distinct end points in snapshot order (members of a group share one)
+    done_syncs.clear();
+    Sync* last = nullptr;
+    bool any = false;
+    for (size_t i = 0; i < snap.size() && !rc; ++i) {
+      Sync* e = snap[i].end.get();
+      if (e == last) continue;
+      last = e;
+      const int q = be_->event_query(d, e->event, err);
+      if (q < 0) rc = q;
+      if (q == 1) {
+        done_syncs.push_back(e);
+        any = true;
+      }
+    }
+    if (!rc && !any) {  // nothing finished yet: block on the oldest
+      rc = be_->event_sync(d, snap[0].end->event, err);
+      if (!rc) done_syncs.push_back(snap[0].end.get());
+    }
+    if (!rc && ktime_) {
+      for (const Item& it : snap) {
+        Sync* e = it.end.get();
+        if (!it.start || e->t_resolved ||
+            std::find(done_syncs.begin(), done_syncs.end(), e) == done_syncs.end())
+          continue;
+        e->t_ns = be_->event_time_ns(d, e->event);
+        it.start->t_ns = be_->event_time_ns(d, it.start->event);
+        it.start->t_resolved = true;
+        e->t_resolved = true;
+      }
     }
     lk.lock();
-    if (debug_staging()) fprintf(stderr, "[sfx] comp locked task=%llu\n", (unsigned long long)t->tid);
     const int64_t tc0 = now_ns();
-    D.inflight.pop_front();
-    if (rc) poison(SFX_ERR_CUDA, err);
-    if (t->op == SFX_OP_EXTERN && !rc) {
-      extern_handoff(t);  // its host copy is current: over to the agent
+    if (rc) {
+      // the context reports an error: fail the engine; the oldest task is retired
+      // so that waiters are woken (the engine is poisoned either way)
+      poison(SFX_ERR_CUDA, err);
+      Task* t = D.inflight.front();
+      D.inflight.pop_front();
+      if (t->op == SFX_OP_EXTERN) {
+        extern_handoff(t);
+      } else {
+        complete(t);
+      }
       continue;
     }
-    complete(t);
+    // rebuild the front of the deque: finished tasks leave, the rest keep order
+    std::vector<Task*> keep;
+    std::vector<Task*> fin;
+    for (size_t i = 0; i < snap.size(); ++i) {
+      Task* t = D.inflight.front();
+      D.inflight.pop_front();
+      const bool fd = std::find(done_syncs.begin(), done_syncs.end(), snap[i].end.get()) != done_syncs.end();
+      (fd ? fin : keep).push_back(t);
+    }
+    for (size_t i = keep.size(); i-- > 0;) D.inflight.push_front(keep[i]);
+    for (Task* t : fin) {
+      if (t->op == SFX_OP_EXTERN) {
+        extern_handoff(t);  // its host copy is current: over to the agent
+        continue;
+      }
+      complete(t);
+    }
     D.stats.t_complete_ns += now_ns() - tc0;
   }
 }

@@ -214,6 +214,8 @@ class Backend {
   virtual int event_sync(int d, void* ev, std::string& err) = 0;
   // true once the recorded work before ev has executed (sim: always)
   virtual bool event_done(int d, void* ev) = 0;
+  // 1 = done, 0 = not yet, < 0 = error (err set): the completion thread's poll
+  virtual int event_query(int d, void* ev, std::string& err) { return event_done(d, ev) ? 1 : 0; }
   // CLOCK_MONOTONIC ns of a completed timing event
   virtual int64_t event_time_ns(int d, void* ev) = 0;
   virtual int copy_h2d(int d, int stream, uint64_t dst_off, const void* src, uint64_t n, std::string& err) = 0;
