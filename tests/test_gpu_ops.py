@@ -323,3 +323,33 @@ def test_commutative_chains_scale_linearly():
         assert t4 / t1 < 8.0, (t1, t4)
     finally:
         eng.stop()
+
+
+def test_read_mode_flush_keeps_the_device_copy(gpu_engine):
+    """flush_to_host(keep_device=True) (reference graph.py:258-260,
+    device.py:282-326): the host buffer receives the device result, the device copy
+    stays valid and clean, and a later reader on the GPU stages nothing; the default
+    (write-mode) flush drops the device copy, so the next reader stages again."""
+    b = 256
+    T = sf.pinned_zeros((b, b))
+    C = sf.pinned_zeros((b, b))
+    g = sf.TaskGraph().compute_on(gpu_engine)
+    g.task(sf.write(T), device=sf.ops.fill_uniform(71, 0, 0, b))
+    g.flush_to_host(T, keep_device=True)
+    assert g.wait_all(timeout=60)
+    assert np.array_equal(T, inputs.uniform_tile(71, 0, 0, b, b, b))
+    hid = g.hid_of(T)
+    st = gpu_engine.block_state(hid)
+    assert st["present"] and st["valid"] and not st["dirty"] and st["host_valid"]
+    h2d0 = gpu_engine.stats(0)["bytes_to_device"]
+    g.task(sf.read(T), sf.write(C), device=sf.ops.syrk_sub)
+    assert g.wait_all(timeout=60)
+    # only C was staged: T's device copy was reused
+    assert gpu_engine.stats(0)["bytes_to_device"] - h2d0 == b * b * 8
+    g.flush_to_host(T)  # write-mode: device copies dropped
+    assert g.wait_all(timeout=60)
+    assert not gpu_engine.block_state(hid)["present"] or not gpu_engine.block_state(hid)["valid"]
+    h2d1 = gpu_engine.stats(0)["bytes_to_device"]
+    g.task(sf.read(T), sf.write(C), device=sf.ops.syrk_sub)
+    assert g.wait_all(timeout=60)
+    assert gpu_engine.stats(0)["bytes_to_device"] - h2d1 == b * b * 8  # T staged again
