@@ -138,7 +138,18 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
     task = lin / p.tiles_per_task;
     const int tile = lin - task * p.tiles_per_task;
     int bm, bn;
-    if (p.lower) {
+    if (TRI && p.ksplit == 1) {
+      // unsplit TRI product (grouped full-inverse TRSMs): column tile bn spans
+      // (bn+1) K-units, so hand out the longest columns first over ALL tasks of
+      // the launch (CTAs are dispatched in blockIdx order): the tail is short tiles
+      const int rows = p.tiles_per_task / p.tiles_n;
+      const int per_col = p.ntasks * rows;
+      const int bnr = (task * p.tiles_per_task + tile) / per_col;
+      const int rem = (task * p.tiles_per_task + tile) - bnr * per_col;
+      bn = p.tiles_n - 1 - bnr;
+      task = rem / rows;
+      bm = rem - task * rows;
+    } else if (p.lower) {
       bm = static_cast<int>((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
       while ((bm + 1) * (bm + 2) / 2 <= tile) ++bm;
       while (bm * (bm + 1) / 2 > tile) --bm;

@@ -469,6 +469,29 @@ class CudaBackend : public Backend {
       cudaError_t e = launch_p2p_group(pd.data(), static_cast<int>(pd.size()), self, f.fp[0], devs_[d]->streams[stream]);
       return cuda_err(e, "grouped p2p launch", err);
     }
+    if (ops.size() > 1 && f.op == SFX_OP_DTRSM && f.ip[0] == 2) {
+      // grouped full-inverse TRSMs: X_i = B_i W_i^T for every member in ONE TRI-masked
+      // DGEMM launch (beta = 0, no split-K: no scratch memset, no atomics), then
+      // each X_i copied back over B_i
+      const size_t one = static_cast<size_t>(f.o[1].rows) * f.o[1].cols * 8;
+      double* X = static_cast<double*>(trsm_scratch(d, stream, one * ops.size()));
+      if (!X) {
+        err = "grouped trsm scratch allocation failed";
+        return SFX_ERR_CUDA;
+      }
+      const long long ldx = f.o[1].cols;
+      std::vector<GemmDesc> g(ops.size());
+      for (size_t i = 0; i < ops.size(); ++i)
+        g[i] = GemmDesc{static_cast<const double*>(ops[i].o[1].dptr), ops[i].o[1].ld,
+                        static_cast<const double*>(ops[i].o[0].dptr), ops[i].o[0].ld, X + i * (one / 8), ldx};
+      const int M = static_cast<int>(f.o[1].rows), n = static_cast<int>(f.o[1].cols);
+      cudaError_t e = launch_dgemm_group(g.data(), static_cast<int>(g.size()), M, n, n, 1.0, 0.0, false, false,
+                                         devs_[d]->streams[stream], true);
+      for (size_t i = 0; i < ops.size() && e == cudaSuccess; ++i)
+        e = cudaMemcpy2DAsync(ops[i].o[1].dptr, ops[i].o[1].ld * 8, X + i * (one / 8), ldx * 8, ldx * 8, M,
+                              cudaMemcpyDeviceToDevice, devs_[d]->streams[stream]);
+      return cuda_err(e, "grouped full-inverse dtrsm launch", err);
+    }
     if (ops.size() > 1 && f.op == SFX_OP_DTRSM && f.ip[0]) {
       std::vector<TrsmDesc> td(ops.size());
       for (size_t i = 0; i < ops.size(); ++i)

@@ -1244,7 +1244,9 @@ bool Runtime::groupable(const Task* t) const {
   // generators: grouping anything else would serialise independent tasks on one stream
   switch (t->op) {
     case SFX_OP_DTRSM:  // grouped cooperative TRSM, or grouped inverse-block GEMM sweeps
-      if (t->ip[0] == 2) return false;  // full inverse: one parallel DGEMM per task, own scratch
+      // full inverse: a group is ONE unsplit TRI-masked DGEMM over all its members
+      // (a lone TRSM keeps the K-weighted split: lower latency on the panel chain)
+      if (t->ip[0] == 2) return group_max_ > 1;
       return group_max_ > 1 && (is_coop(t) || (t->ip[0] && t->acc[0].h->rows % 64 == 0));
     case SFX_OP_DGEMM:
     case SFX_OP_DSYRK:

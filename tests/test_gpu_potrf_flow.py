@@ -112,3 +112,30 @@ def test_flow_and_cooperative_kernels_agree():
     assert np.abs(Lf - Lc).max() / np.abs(Lc).max() <= 1e-12
     Wf, Wc = np.triu(outs["flow"], 1), np.triu(outs["coop"], 1)
     assert np.abs(Wf - Wc).max() / np.abs(Wc).max() <= 1e-10
+
+
+def test_grouped_full_inverse_trsms_match_numpy():
+    # independent TRSMs of one panel launch as ONE unsplit TRI-masked DGEMM (beta = 0)
+    b, m = 512, 6
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, 2), trace=False, group_max=8)
+    try:
+        A0 = inputs.spd_tile(65, 0, 0, b, b, b)
+        L = A0.copy()
+        Bs0 = [inputs.uniform_tile(66 + i, 0, 0, b, b, b) for i in range(m)]
+        Bs = [x.copy() for x in Bs0]
+        g = sf.TaskGraph().compute_on(eng)
+        g.task(sf.write(L), device=sf.ops.potrf_fullinv)
+        p0 = sf.gemm_paths()
+        with g.gated():  # all TRSMs ready at once: one launch group
+            for B in Bs:
+                g.task(sf.read(L), sf.write(B), device=sf.ops.trsm_fullinv)
+        g.flush_all(keep_device=False)
+        assert g.wait_all(timeout=120)
+        p1 = sf.gemm_paths()
+        assert p1["tri"] - p0["tri"] == 1 and p1["tasks"] - p0["tasks"] == m, (p0, p1)
+        assert p1["splitk"] == p0["splitk"]
+        Lw = np.tril(L)
+        for B0, X in zip(Bs0, Bs):
+            assert np.linalg.norm(X @ Lw.T - B0) / (np.linalg.norm(Lw) * np.linalg.norm(X)) <= 1e-13
+    finally:
+        eng.stop()
