@@ -73,7 +73,7 @@ struct GemmGroup {
   long long ldc;
   int ntasks;
   int ksplit;  // > 1: split-K, partial products are atomically added into C (beta == 1)
-  int tri_split;  // TRI only: K-weighted split -- output column tile bn (whose k-range
+  int tri_split;  // TRI only, > 0: K-weighted split into items of tri_split units (column tile bn's k-range
                   // is [0, (bn+1)*BN) under the triangular mask) is cut into bn+1
                   // slices of BN/BK k-steps, atomically added (beta == 1)
   int tri;     // NN only: B is an upper-triangular block with a reciprocal diagonal
@@ -102,9 +102,18 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
   uint64_t* cfull = empty + STAGES;
   uint64_t* cempty = cfull + 1;
 
-  const int tri_row = p.tiles_n * (p.tiles_n + 1) / 2;  // TRI split: work items per row of output tiles
-  const int total = p.tri_split ? p.ntasks * (p.tiles_per_task / p.tiles_n) * tri_row
-                                : p.ntasks * p.tiles_per_task * p.ksplit;
+  // TRI split: per row of output tiles, column tile bn spans (bn+1) K-units of
+  // BN/BK k-steps; it is cut into items of U = tri_split units (the last one
+  // shorter when U does not divide bn+1): tri_full U-unit items per row, then
+  // tri_part shorter ones
+  const int U = p.tri_split > 0 ? p.tri_split : 1;
+  int tri_full = 0, tri_part = 0;
+  for (int c = 0; c < p.tiles_n; ++c) {
+    tri_full += (c + 1) / U;
+    tri_part += ((c + 1) % U) != 0;
+  }
+  const int tri_rows = p.ntasks * (p.tiles_per_task / p.tiles_n);
+  const int total = p.tri_split ? tri_rows * (tri_full + tri_part) : p.ntasks * p.tiles_per_task * p.ksplit;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ktiles_all = (p.K + BK - 1) / BK;
   const int kchunk = (ktiles_all + p.ksplit - 1) / p.ksplit;
@@ -112,23 +121,33 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
   // linear work index -> (task, m0, n0, k-slice); lower = triangular enumeration (bm >= bn)
   auto coords = [&](int lin, int& task, int& m0, int& n0, int& kt0, int& kt1) {
     if (TRI && p.tri_split) {
-      // (task, bm) rows of tri_row items; item w -> column tile bn (triangular
-      // root) and slice w - bn(bn+1)/2 of BN/BK k-steps: every item has the same
-      // length, so the CTAs stay balanced (a uniform split-K leaves the long
-      // right-hand column tiles 8x the work of the left ones)
+      // all full items of every row first (CTAs are dispatched in blockIdx order,
+      // so the shorter items fill the tail)
       const int rows = p.tiles_per_task / p.tiles_n;
-      const int w = lin % tri_row;
-      const int rb = lin / tri_row;
+      int rb, bn, q;
+      if (lin < tri_rows * tri_full) {
+        rb = lin / tri_full;
+        int f = lin - rb * tri_full;
+        bn = 0;
+        while (f >= (bn + 1) / U) {
+          f -= (bn + 1) / U;
+          ++bn;
+        }
+        q = f;  // units [qU, qU + U)
+      } else {
+        const int l2 = lin - tri_rows * tri_full;
+        rb = l2 / tri_part;
+        int f = l2 - rb * tri_part;
+        bn = 0;
+        while (((bn + 1) % U) == 0 || f-- > 0) ++bn;  // the f-th column with a remainder
+        q = (bn + 1) / U;
+      }
       task = rb / rows;
       const int bm = rb - task * rows;
-      int bn = static_cast<int>((sqrtf(8.0f * w + 1.0f) - 1.0f) * 0.5f);
-      while ((bn + 1) * (bn + 2) / 2 <= w) ++bn;
-      while (bn * (bn + 1) / 2 > w) --bn;
-      const int slice = w - bn * (bn + 1) / 2;
       m0 = bm * BM;
       n0 = bn * BN;
-      kt0 = slice * (BN / BK);
-      kt1 = min(ktiles_all, kt0 + BN / BK);
+      kt0 = q * U * (BN / BK);
+      kt1 = min(min(ktiles_all, kt0 + U * (BN / BK)), (bn + 1) * (BN / BK));
       return;
     }
     const int ks = lin % p.ksplit;
@@ -629,7 +648,17 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
   if (p.cpref)
     for (int i = 0; i < n; ++i)
       if (!make_tmap_f64_2d(&p.t[i].c, d[i].C, N, M, d[i].ldc, 16, BM, true)) return cudaErrorInvalidValue;
-  const int total = p.tri_split ? n * tm * (tn * (tn + 1) / 2) : p.tiles_per_task * n * p.ksplit;
+  // K-weighted TRI split: one-unit items (BN/BK k-steps each), or two-unit items
+  // (half the atomic epilogues) once one-unit items would fill the SMs more than
+  // once over
+  if (p.tri_split) {
+    const int units = tm * n * (tn * (tn + 1) / 2);
+    p.tri_split = units > num_sms() ? 2 : 1;
+  }
+  int tri_items = 0;  // per row of output tiles: full items + shorter items (see the kernel)
+  for (int c = 0; c < tn; ++c) tri_items += (c + 1) / (p.tri_split ? p.tri_split : 1) +
+                                          (((c + 1) % (p.tri_split ? p.tri_split : 1)) != 0);
+  const int total = p.tri_split ? n * tm * tri_items : p.tiles_per_task * n * p.ksplit;
   // persistent CTAs, at most tiles_per_cta() output tiles each: the operand
   // ring streams the next tile during the epilogue, while SMs still free up
   // often enough for high-priority (critical-path) kernels to get in
