@@ -210,9 +210,25 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
         const CUtensorMap* tmB = &p.t[task].b;
         ptx::prefetch_tmap(tmA);
         ptx::prefetch_tmap(tmB);
+        // this tile's C goes into the prefetch buffer once the previous epilogue
+        // released it: issued at k-step kt0 + STAGES (the consumers have begun this
+        // tile, so the previous epilogue is over and cempty will not block), it has
+        // the rest of the mainloop to land; issued after the last k-step (round 1)
+        // it arrived late: the consumers' cfull waits were ~2 % of their time
+        const bool want_c = p.cpref && m0 + BM <= p.M && n0 + BN <= p.N;
+        const int kc = kt1 - kt0 > STAGES ? kt0 + STAGES : kt1;
+        auto load_c = [&]() {
+          if (cn > 0) ptx::mbar_wait(cempty, (cn - 1) & 1);
+          ptx::mbar_arrive_expect_tx(cfull, C_BUF);
+          const CUtensorMap* tmC = &p.t[task].c;
+#pragma unroll
+          for (int q = 0; q < BN / 16; ++q) ptx::tma_load_2d(sC + q * (BM * 128), tmC, n0 + 16 * q, m0, cfull);
+          ++cn;
+        };
         for (int kt = kt0; kt < kt1; ++kt, ++it) {
           const int s = it % STAGES;
           if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          if (want_c && kt == kc) load_c();
           ptx::mbar_arrive_expect_tx(&full[s], A_STAGE + B_STAGE);
           ptx::tma_load_2d(sA + s * A_STAGE, tmA, kt * BK, m0, &full[s]);
           if (TRANS_B) {
@@ -223,16 +239,7 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
               ptx::tma_load_2d(sB + s * B_STAGE + q * 2048, tmB, n0 + 16 * q, kt * BK, &full[s]);
           }
         }
-        // this tile's C, once the previous epilogue released the buffer; it lands
-        // while the consumers work through the last STAGES k-steps
-        if (p.cpref && m0 + BM <= p.M && n0 + BN <= p.N) {
-          if (cn > 0) ptx::mbar_wait(cempty, (cn - 1) & 1);
-          ptx::mbar_arrive_expect_tx(cfull, C_BUF);
-          const CUtensorMap* tmC = &p.t[task].c;
-#pragma unroll
-          for (int q = 0; q < BN / 16; ++q) ptx::tma_load_2d(sC + q * (BM * 128), tmC, n0 + 16 * q, m0, cfull);
-          ++cn;
-        }
+        if (want_c && kc == kt1) load_c();
       }
     }
     return;
