@@ -56,7 +56,7 @@ constexpr int B_STAGE = BN * BK * 8;  // 16 KiB
 // of 16 x 128 doubles, 128B swizzle) while the consumers are still in the
 // mainloop, so the epilogue reads C from shared memory instead of waiting on HBM
 constexpr int C_BUF = BM * BN * 8;  // 128 KiB
-constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + C_BUF + 2 * STAGES * 8 + 16 + 1024;
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + C_BUF + 2 * STAGES * 8 + 24 + 1024;
 static_assert(SMEM_BYTES <= 232448, "dynamic shared memory per CTA");
 
 // One launch covers G independent tile tasks of identical shape (grouped
@@ -84,6 +84,7 @@ struct GemmGroup {
   int lower;
   int cpref;  // C tiles of interior output tiles are prefetched by TMA (beta != 0, ksplit == 1, !lower)
   int zero;     // always 0 at run time (the compiler cannot know): see the stage release
+  int stagger;  // warpgroup 1 starts a k-step behind warpgroup 0 (SFX_GEMM_STAGGER=0: off, A/B)
   int release;  // stage release: 0 = data-dependent arrive (default), 1 = fence.acq_rel.cta (A/B experiments)
   double alpha, beta;
 };
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
   uint64_t* empty = full + STAGES;
   uint64_t* cfull = empty + STAGES;
   uint64_t* cempty = cfull + 1;
+  uint64_t* stagger = cempty + 1;  // warpgroup 1 starts one k-step behind warpgroup 0
 
   // TRI split: per row of output tiles, column tile bn spans (bn+1) K-units of
   // BN/BK k-steps; it is cut into items of U = tri_split units (the last one
@@ -192,6 +194,7 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
     }
     ptx::mbar_init(cfull, 1);
     ptx::mbar_init(cempty, CONSUMER_WARPS * 32);
+    ptx::mbar_init(stagger, CONSUMER_WARPS / 2);
     ptx::fence_mbar_init();
   }
   __syncthreads();
@@ -269,6 +272,13 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
 
     for (int kt = kt0; kt < kt1; ++kt, ++it) {
       const int s = it % STAGES;
+      // Staggered warpgroups: the two DMMA warpgroups (rows 0-63 / 64-127 of the
+      // tile, one warp of each per SMSP) would otherwise reach every tile's
+      // epilogue together and leave the DMMA pipe idle through it.  Warpgroup 1
+      // starts once warpgroup 0 has finished its first k-step; the lag persists,
+      // so each epilogue runs beside the other warpgroup's mainloop.
+      if (it == 1 && wm == 0 && lane == 0 && p.stagger) ptx::mbar_arrive(stagger);
+      if (it == 0 && wm == 1 && p.stagger) ptx::mbar_wait(stagger, 0);
       ptx::mbar_wait(&full[s], (it / STAGES) & 1);
       const uint32_t aS = ptx::smem_u32(sA) + s * A_STAGE;
       const uint32_t bS = ptx::smem_u32(sB) + s * B_STAGE;
@@ -636,6 +646,8 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
   p.zero = 0;
   static const int release_mode = getenv("SFX_GEMM_RELEASE") ? atoi(getenv("SFX_GEMM_RELEASE")) : 0;
   p.release = release_mode;
+  static const int stagger_mode = getenv("SFX_GEMM_STAGGER") ? atoi(getenv("SFX_GEMM_STAGGER")) : 1;
+  p.stagger = stagger_mode;
   const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
   p.tiles_n = tn;
   p.tiles_per_task = lower ? tm * (tm + 1) / 2 : tm * tn;
