@@ -45,7 +45,13 @@ namespace {
 #endif
 constexpr bool NN_COLPERM = SFX_NN_COLPERM != 0;
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3;
+#ifndef SFX_GEMM_STAGES
+#define SFX_GEMM_STAGES 3
+#endif
+#ifndef SFX_GEMM_CBUF
+#define SFX_GEMM_CBUF 1
+#endif
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = SFX_GEMM_STAGES;
 constexpr int CONSUMER_WARPS = 8;
 // one producer warpgroup (4 warps, one elected TMA lane) + two DMMA warpgroups;
 // setmaxnreg moves registers from the producer to the consumers (40 / 232).
@@ -55,7 +61,7 @@ constexpr int B_STAGE = BN * BK * 8;  // 16 KiB
 // C prefetch buffer: the producer TMA-loads the next epilogue's C tile (8 boxes
 // of 16 x 128 doubles, 128B swizzle) while the consumers are still in the
 // mainloop, so the epilogue reads C from shared memory instead of waiting on HBM
-constexpr int C_BUF = BM * BN * 8;  // 128 KiB
+constexpr int C_BUF = SFX_GEMM_CBUF ? BM * BN * 8 : 0;  // 128 KiB
 constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + C_BUF + 2 * STAGES * 8 + 24 + 1024;
 static_assert(SMEM_BYTES <= 232448, "dynamic shared memory per CTA");
 
@@ -84,7 +90,7 @@ struct GemmGroup {
   int lower;
   int cpref;  // C tiles of interior output tiles are prefetched by TMA (beta != 0, ksplit == 1, !lower)
   int zero;     // always 0 at run time (the compiler cannot know): see the stage release
-  int stagger;  // warpgroup 1 starts a k-step behind warpgroup 0 (SFX_GEMM_STAGGER=0: off, A/B)
+  int stagger;  // warpgroup 1 starts this many k-steps behind warpgroup 0 (SFX_GEMM_STAGGER, 0: off)
   int release;  // stage release: 0 = data-dependent arrive (default), 1 = fence.acq_rel.cta (A/B experiments)
   double alpha, beta;
 };
@@ -277,7 +283,7 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
       // epilogue together and leave the DMMA pipe idle through it.  Warpgroup 1
       // starts once warpgroup 0 has finished its first k-step; the lag persists,
       // so each epilogue runs beside the other warpgroup's mainloop.
-      if (it == 1 && wm == 0 && lane == 0 && p.stagger) ptx::mbar_arrive(stagger);
+      if (it == p.stagger && wm == 0 && lane == 0 && p.stagger) ptx::mbar_arrive(stagger);
       if (it == 0 && wm == 1 && p.stagger) ptx::mbar_wait(stagger, 0);
       ptx::mbar_wait(&full[s], (it / STAGES) & 1);
       const uint32_t aS = ptx::smem_u32(sA) + s * A_STAGE;
@@ -489,6 +495,8 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
       }
     }
   }
+  // a CTA whose whole work is shorter than the stagger still releases warpgroup 1
+  if (wm == 0 && lane == 0 && p.stagger && it <= p.stagger) ptx::mbar_arrive(stagger);
 #undef PCOL
 #undef ACCX
 #undef ACCY
@@ -634,7 +642,7 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
     p.t[i].C = d[i].C;
   }
   // split-K decided below; the C prefetch needs beta != 0, no split and a full tile
-  const bool want_cpref = beta != 0.0 && !lower && M >= BM && N >= BN;
+  const bool want_cpref = C_BUF > 0 && beta != 0.0 && !lower && M >= BM && N >= BN;
   p.ldc = d[0].ldc;
   p.M = M;
   p.N = N;
@@ -647,7 +655,9 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
   static const int release_mode = getenv("SFX_GEMM_RELEASE") ? atoi(getenv("SFX_GEMM_RELEASE")) : 0;
   p.release = release_mode;
   static const int stagger_mode = getenv("SFX_GEMM_STAGGER") ? atoi(getenv("SFX_GEMM_STAGGER")) : 1;
-  p.stagger = stagger_mode;
+  // at most STAGES - 1: warpgroup 0 cannot run further ahead (every stage needs
+  // both warpgroups' release before the producer refills it)
+  p.stagger = stagger_mode < 0 ? 0 : (stagger_mode > STAGES - 1 ? STAGES - 1 : stagger_mode);
   const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
   p.tiles_n = tn;
   p.tiles_per_task = lower ? tm * (tm + 1) / 2 : tm * tn;
