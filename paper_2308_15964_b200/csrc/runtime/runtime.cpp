@@ -678,7 +678,7 @@ void Runtime::push_ready(Task* t, int wid) {
   record(graphs_[t->gid].get(), SFX_EV_PUSH, t->t_push, wid, t->tid);
   devs_[d]->queue.push(t);
   devs_[d]->prefetch_pending = true;
-  devs_[d]->exec_cv.notify_one();
+  devs_[d]->wake_exec();
 }
 
 void Runtime::advance(Handle* h) {
@@ -1416,7 +1416,7 @@ void Runtime::complete(Task* t) {
     D.stream_inflight[t->stream] -= 1;
   }
   D.stats.tasks_executed += 1;
-  D.exec_cv.notify_one();
+  D.wake_exec();
   done_cv_.notify_all();
   if (!g->history) {
     for (auto& a : t->acc) {
@@ -1440,7 +1440,7 @@ void Runtime::extern_handoff(Task* t) {
   t->detached = true;
   extern_ready_.push_back(t);
   extern_cv_.notify_all();
-  D.exec_cv.notify_one();
+  D.wake_exec();
 }
 
 int Runtime::extern_poll(uint64_t* tids, uint64_t cap, uint64_t* n, double timeout_s) {
@@ -1609,9 +1609,11 @@ void Runtime::exec_loop(int d) {
       return !paused_ && !fail_code_ && D.queue.size() > 0 && D.ninflight < static_cast<int>(window_) &&
              free_stream(D.queue.peek()) >= 0;
     };
-    D.exec_cv.wait(lk, [&] {
-      return stopping_ || runnable() || (prefetch_ && D.prefetch_pending && !paused_ && !fail_code_);
-    });
+    while (!(stopping_ || runnable() || (prefetch_ && D.prefetch_pending && !paused_ && !fail_code_))) {
+      D.exec_sleeping = true;
+      D.exec_cv.wait(lk);
+      D.exec_sleeping = false;
+    }
     if (stopping_) return;
     if (!runnable()) {
       // every stream is busy: stage operands of queued tasks meanwhile

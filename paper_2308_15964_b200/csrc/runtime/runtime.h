@@ -290,6 +290,16 @@ struct Device {
   std::vector<int> stream_groups;    // launch groups in flight per stream
   int ninflight = 0;
   std::condition_variable exec_cv, comp_cv;
+  // the executor sleeps on exec_cv: per-task wake-ups (push, completion) signal it
+  // only while it sleeps and only once per sleep (no futex storm from a burst of
+  // pushes, and none at all while it is busy); guarded by the runtime mutex
+  bool exec_sleeping = false;
+  void wake_exec() {
+    if (exec_sleeping) {
+      exec_sleeping = false;
+      exec_cv.notify_one();
+    }
+  }
   std::thread exec_thread, comp_thread;
   sfx_dev_stats stats{};
   std::vector<std::pair<int64_t, int64_t>> kintervals;  // KTIME group [start, end] not yet folded into busy_ns
