@@ -76,7 +76,7 @@ def parse():
                     help="launch-group size for the Cholesky legs (tools/chol_sweep.py: 8 best for b=1024)")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-check", action="store_true")
-    ap.add_argument("--e2e-skew", type=int, default=-1, help="insert_gemm skew on the e2e leg (-1: 2*nt, 0: FIFO)")
+    ap.add_argument("--e2e-skew", type=int, default=-1, help="insert_gemm skew on the e2e leg (-1: nt, 0: FIFO)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--overhead-n", type=int, default=1000)
@@ -531,10 +531,11 @@ def main_gemm(args, dist):
     # ---- e2e: host-resident inputs through the public API ----
     def e2e_step():
         # wavefront priorities (insert_gemm skew): the k-chains of the C tiles start
-        # staggered over 2*nt waves, so C's staging (2 GiB H2D) and its flush
+        # staggered over nt waves, so C's staging (2 GiB H2D) and its flush
         # (2 GiB D2H) spread over the step instead of piling up in the first and
-        # last waves (tools/e2e_probe.py: 25.7 -> 28.3 TFLOP/s)
-        alg.insert_gemm(g, A, B, C, skew=args.e2e_skew if args.e2e_skew >= 0 else 2 * nt)
+        # last waves (round 1, tools/e2e_probe.py: 25.7 -> 28.3 TFLOP/s with 2*nt;
+        # round 2, tools/e2e_timeline.py + r2x: nt ramps up faster, 29.3-29.8 -> 29.8-30.0)
+        alg.insert_gemm(g, A, B, C, skew=args.e2e_skew if args.e2e_skew >= 0 else nt)
         for t in C.tiles.values():
             g.flush_to_host(t)                      # C back to the host (write-mode flush)
         for M in (A, B):

@@ -1771,9 +1771,10 @@ void Runtime::exec_loop(int d) {
       ordered.reserve(acts.size() + 1);
       for (auto& a : acts)
         if (a.kind == Action::WAIT) ordered.push_back(a);
-      if (gstart) ordered.push_back(Action{Action::RECORD, gstart});
+      if (gstart && !ktime_kernel_only_) ordered.push_back(Action{Action::RECORD, gstart});
       for (auto& a : acts)
         if (a.kind != Action::WAIT) ordered.push_back(a);
+      if (gstart && ktime_kernel_only_) ordered.push_back(Action{Action::RECORD, gstart});
       acts.swap(ordered);
     }
     D.ninflight += static_cast<int>(group.size());
@@ -2119,6 +2120,8 @@ int Runtime::set_option(const std::string& key, int64_t value) {
     deterministic_ = value != 0;
   } else if (key == "stream_affinity") {
     stream_affinity_ = value != 0;
+  } else if (key == "kernel_only_start") {
+    ktime_kernel_only_ = value != 0;
   } else if (key == "window") {
     window_ = static_cast<uint32_t>(std::max<int64_t>(1, value));
     for (auto& d : devs_) d->exec_cv.notify_all();

@@ -383,6 +383,7 @@ class Runtime {
   // co-resident, so their grid barriers can never starve each other)
   int ncoop_ = 2;
   bool stream_affinity_ = true;  // successors join their in-flight predecessor's stream
+  bool ktime_kernel_only_ = false;  // the group's start stamp after its copies (timeline diagnostics)
   // deterministic mode: no order-dependent FP64 accumulation anywhere -- ops that
   // normally accumulate with device atomics run one-sided kernels under
   // exclusive guards, DGEMMs never split K (OpLaunch::deterministic); with one
