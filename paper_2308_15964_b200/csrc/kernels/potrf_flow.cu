@@ -647,14 +647,15 @@ __global__ void __launch_bounds__(THREADS, 1) potrf_flow_kernel(const __grid_con
       prof(k, 1);
       if (tid == 0 && s.bad && g.info && *reinterpret_cast<volatile int*>(g.info) == 0)
         *reinterpret_cast<volatile int*>(g.info) = k * T + s.bad;
-      // X_kk -> s.b (row-major: the B operand of P) and the workspace
+      // X_kk -> s.b (row-major: the B operand of P), L_kk -> s.c; their global
+      // stores (workspace X_kk, the tile's L_kk and inv(L_kk)^T) are issued now and
+      // drain under P's product; ONE fence then publishes fdone[k] together with
+      // pdone[k+1][k] (the queue's P(i,k) tasks have slack: their first consumer
+      // on the chain is P(k+2,k+1), a step later)
       patch_store(s.b, x, pt, true);
-      __syncthreads();
-      store_block(xblk(g, k), T, s.b, false);
-      publish(&fl->fdone[k], 1);
-      // outputs nobody in the launch reads: L_kk, and inv(L_kk)^T in the upper triangle
       patch_store(s.c, a, pt, false);
       __syncthreads();
+      store_block(xblk(g, k), T, s.b, false);
       store_block(blk(g, k, k), g.lda, s.c, true);
       if (g.mode >= 1) {
         double* Akk = blk(g, k, k);
@@ -664,7 +665,10 @@ __global__ void __launch_bounds__(THREADS, 1) potrf_flow_kernel(const __grid_con
         }
       }
       prof(k, 2);
-      if (k + 1 == nb) break;
+      if (k + 1 == nb) {
+        publish(&fl->fdone[k], 1);
+        break;
+      }
       // ---- P(k+1, k) ----
       if (!pre) {
         if (tid == 0) wait_ge(&fl->cnt[(k + 1) * MAXNB + k], k);
@@ -682,7 +686,13 @@ __global__ void __launch_bounds__(THREADS, 1) potrf_flow_kernel(const __grid_con
       frag_store(s.c, f, 1.0, false);  // L_{k+1,k}, row-major
       __syncthreads();
       store_block(blk(g, k + 1, k), g.lda, s.c, false);
-      publish(&fl->pdone[(k + 1) * MAXNB + k], 1);
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&fl->fdone[k]), "r"(1u) : "memory");
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&fl->pdone[(k + 1) * MAXNB + k]), "r"(1u)
+                     : "memory");
+      }
       prof(k, 4);
       // ---- U(k+1, k+1, k): a = A_{k+1,k+1} - L L^T, never written back ----
       if (!pre) {
