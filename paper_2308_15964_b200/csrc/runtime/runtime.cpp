@@ -1826,7 +1826,7 @@ void Runtime::comp_loop(int d) {
     SyncP end, start;
   };
   std::vector<Item> snap;
-  std::vector<Sync*> done_syncs;
+  std::vector<Task*> keep, fin;
   std::unique_lock<std::mutex> lk(mu_);
   while (true) {
     D.comp_cv.wait(lk, [&] { return stopping_ || !D.inflight.empty(); });
@@ -1844,30 +1844,27 @@ void Runtime::comp_loop(int d) {
     std::string err;
     int rc = 0;
     // distinct end points in snapshot order (members of a group share one)
-    done_syncs.clear();
     Sync* last = nullptr;
     bool any = false;
     for (size_t i = 0; i < snap.size() && !rc; ++i) {
       Sync* e = snap[i].end.get();
-      if (e == last) continue;
+      if (e == last || e->seen_done) continue;
       last = e;
       const int q = be_->event_query(d, e->event, err);
       if (q < 0) rc = q;
       if (q == 1) {
-        done_syncs.push_back(e);
+        e->seen_done = true;
         any = true;
       }
     }
-    if (!rc && !any) {  // nothing finished yet: block on the oldest
+    if (!rc && !any && !snap[0].end->seen_done) {  // nothing finished yet: block on the oldest
       rc = be_->event_sync(d, snap[0].end->event, err);
-      if (!rc) done_syncs.push_back(snap[0].end.get());
+      if (!rc) snap[0].end->seen_done = true;
     }
     if (!rc && ktime_) {
       for (const Item& it : snap) {
         Sync* e = it.end.get();
-        if (!it.start || e->t_resolved ||
-            std::find(done_syncs.begin(), done_syncs.end(), e) == done_syncs.end())
-          continue;
+        if (!it.start || e->t_resolved || !e->seen_done) continue;
         e->t_ns = be_->event_time_ns(d, e->event);
         it.start->t_ns = be_->event_time_ns(d, it.start->event);
         it.start->t_resolved = true;
@@ -1890,13 +1887,12 @@ void Runtime::comp_loop(int d) {
       continue;
     }
     // rebuild the front of the deque: finished tasks leave, the rest keep order
-    std::vector<Task*> keep;
-    std::vector<Task*> fin;
+    keep.clear();
+    fin.clear();
     for (size_t i = 0; i < snap.size(); ++i) {
       Task* t = D.inflight.front();
       D.inflight.pop_front();
-      const bool fd = std::find(done_syncs.begin(), done_syncs.end(), snap[i].end.get()) != done_syncs.end();
-      (fd ? fin : keep).push_back(t);
+      (snap[i].end->seen_done ? fin : keep).push_back(t);
     }
     for (size_t i = keep.size(); i-- > 0;) D.inflight.push_front(keep[i]);
     for (Task* t : fin) {

@@ -71,6 +71,7 @@ struct Sync {
   bool group_timed = false;    // launch group duration already accumulated (KTIME)
   int64_t t_ns = 0;            // host-clock time of the event, resolved by the completion
   bool t_resolved = false;     // thread OUTSIDE the runtime mutex (only it touches these)
+  bool seen_done = false;      // completion thread: this point was observed complete
   ~Sync();
 };
 using SyncP = std::shared_ptr<Sync>;
