@@ -81,6 +81,14 @@ def main():
         res = np.linalg.norm(B @ L.T - B0) / np.linalg.norm(B0)
         print(f"trsm_fullinv n={n}: {med:.1f} us (best {best:.1f}), {n ** 3 / med / 1e6:.2f} TFLOP/s, "
               f"residual {res:.2e}", flush=True)
+        # the other two panel-chain ops, alone: SYRK (lower) and the NT GEMM update
+        C = sf.pinned_empty((n, n))
+        med, best = op_time(eng, g, lambda: g.task(sf.write(C), device=sf.ops.fill_spd(53, 0, 0, n)),
+                            lambda: g.task(sf.read(B), sf.write(C), device=sf.ops.syrk_sub), a.reps)
+        print(f"syrk_sub n={n}: {med:.1f} us (best {best:.1f}), {n ** 3 / med / 1e6:.2f} TFLOP/s", flush=True)
+        med, best = op_time(eng, g, lambda: g.task(sf.write(C), device=sf.ops.fill_spd(53, 0, 0, n)),
+                            lambda: g.task(sf.read(B), sf.read(A), sf.write(C), device=sf.ops.gemm_nt_sub), a.reps)
+        print(f"gemm_nt_sub n={n}: {med:.1f} us (best {best:.1f}), {2 * n ** 3 / med / 1e6:.2f} TFLOP/s", flush=True)
     eng.stop()
 
 
