@@ -353,3 +353,37 @@ def test_read_mode_flush_keeps_the_device_copy(gpu_engine):
     g.task(sf.read(T), sf.write(C), device=sf.ops.syrk_sub)
     assert g.wait_all(timeout=60)
     assert gpu_engine.stats(0)["bytes_to_device"] - h2d1 == b * b * 8  # T staged again
+
+
+def test_million_task_soak_on_the_gpu_has_flat_runtime_memory():
+    """The CUDA backend version of the simulated-backend soak: 10^6 device tasks
+    (int64 cell kernels) through one history-free graph; live tasks/slots stay
+    bounded, the process RSS flat, and every cell ends at its task count."""
+    import psutil
+
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, 8), trace=False, device_memory=1 << 28)
+    proc = psutil.Process()
+    try:
+        g = sf.TaskGraph(history=False, trace=False).compute_on(eng)
+        T = 8
+        cells = [sf.Cell(0) for _ in range(T)]
+        H = np.array([g.hid_of(c) for c in cells], np.uint64)
+        op = sf.ops.cell("write", 1, 1)
+        chunk = 20000
+        rss = []
+        for rep in range(50):  # 50 x 20,000 = 10^6 tasks
+            hids = np.tile(H, chunk // T)
+            g.submit_arrays(np.full(chunk, op.code, np.uint32), np.zeros((chunk, 4)),
+                            np.tile(np.array(op.iparam, np.int64), (chunk, 1)), np.zeros(chunk, np.int32),
+                            np.ones(chunk, np.uint32), hids, np.full(chunk, sf.AccessMode.WRITE.code, np.uint32))
+            assert g.wait_all(timeout=120)
+            live = eng.live()
+            assert live["tasks"] <= 4 * T and live["slots"] <= 4 * T, live
+            rss.append(proc.memory_info().rss)
+        g.flush_all(keep_device=False)
+        assert g.wait_all(timeout=120)
+        assert eng.live()["retired"] >= 10 ** 6 - 4 * T
+        assert [c.value for c in cells] == [(10 ** 6 // T)] * T
+        assert rss[-1] - rss[5] < 64 << 20, (rss[5], rss[-1])
+    finally:
+        eng.stop()
