@@ -286,6 +286,12 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
       if (it == p.stagger && wm == 0 && lane == 0 && p.stagger) ptx::mbar_arrive(stagger);
       if (it == 0 && wm == 1 && p.stagger) ptx::mbar_wait(stagger, 0);
       ptx::mbar_wait(&full[s], (it / STAGES) & 1);
+      if (TRI && kt * BK >= n0 + wn * 32 + 32) {
+        // TRI: every B operand of this warp's columns is below the diagonal in
+        // this k-step (exact zeros): no loads, no DMMAs, just release the stage
+        if (lane == 0) ptx::mbar_arrive(&empty[s]);
+        continue;
+      }
       const uint32_t aS = ptx::smem_u32(sA) + s * A_STAGE;
       const uint32_t bS = ptx::smem_u32(sB) + s * B_STAGE;
       // operands (true k = sigma(t, h, e) = 4t + 2h + (e ^ sw)): ordered shared
@@ -322,9 +328,12 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
               const int k = 4 * t + 2 * h + e;
               double v = ptx::lds64(bS + q * 2048 + k * 128 + (((nn >> 1) ^ (k & 7)) << 4) + (nn & 1) * 8);
               if (h == 1) dep |= static_cast<uint32_t>(__double2hiint(v));
-              if (TRI) {
+              if (TRI && kt * BK + BK > n0 + wn * 32) {  // only k-steps reaching this warp's columns
                 const int kg = kt * BK + k, ng = n0 + n;
-                v = kg > ng ? 0.0 : (kg == ng ? 1.0 / v : v);
+                if (kg > ng)
+                  v = 0.0;
+                else if (kg == ng)
+                  v = __drcp_rn(v);  // the diagonal: 1 / L_nn (IEEE reciprocal, no division slow path)
               }
               b[j][e] = v;
             }
@@ -350,8 +359,8 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
               if (TRI) {  // masked only on the k-steps that cross the diagonal
                 const int kg = kt * BK + k, ng = n0 + n;
                 if (kt * BK + BK > n0 + wn * 32) {
-                  b0 = kg > ng ? 0.0 : (kg == ng ? 1.0 / b0 : b0);
-                  b1 = kg > ng + 1 ? 0.0 : (kg == ng + 1 ? 1.0 / b1 : b1);
+                  b0 = kg > ng ? 0.0 : (kg == ng ? __drcp_rn(b0) : b0);
+                  b1 = kg > ng + 1 ? 0.0 : (kg == ng + 1 ? __drcp_rn(b1) : b1);
                 }
               }
               b[2 * jp][e] = b0;
