@@ -330,10 +330,10 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
               if (h == 1) dep |= static_cast<uint32_t>(__double2hiint(v));
               if (TRI && kt * BK + BK > n0 + wn * 32) {  // only k-steps reaching this warp's columns
                 const int kg = kt * BK + k, ng = n0 + n;
-                if (kg > ng)
-                  v = 0.0;
-                else if (kg == ng)
-                  v = __drcp_rn(v);  // the diagonal: 1 / L_nn (IEEE reciprocal, no division slow path)
+                // selects, no divergent branch: the diagonal gets 1 / L_nn (IEEE
+                // reciprocal, no division slow path), below it exact zeros
+                const double rv = __drcp_rn(v);
+                v = kg > ng ? 0.0 : (kg == ng ? rv : v);
               }
               b[j][e] = v;
             }
