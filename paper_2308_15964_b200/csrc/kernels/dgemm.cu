@@ -682,7 +682,10 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
     const int tiles = p.tiles_per_task * n, ksteps = (K + BK - 1) / BK;
     while (tiles * p.ksplit * 2 <= num_sms() && ksteps / (p.ksplit * 2) >= 8) p.ksplit *= 2;
   }
-  p.cpref = want_cpref && p.ksplit == 1 ? 1 : 0;
+  // the C prefetch serves the direct epilogue only: split-K and TRI-split items
+  // add into C with atomics and never read the buffer (with 2 tiles per CTA the
+  // producer would then wait forever for the buffer's release)
+  p.cpref = want_cpref && p.ksplit == 1 && !p.tri_split ? 1 : 0;
   if (p.cpref)
     for (int i = 0; i < n; ++i)
       if (!make_tmap_f64_2d(&p.t[i].c, d[i].C, N, M, d[i].ldc, 16, BM, true)) return cudaErrorInvalidValue;
