@@ -627,7 +627,14 @@ int tiles_per_cta(int total, int K) {
     return e ? atoi(e) : 0;
   }();
   if (forced > 0) return forced;
-  return total >= 2 * num_sms() && K < 1024 ? 2 : 1;
+  // up to 4 output tiles per persistent CTA once the launch has that many tiles
+  // per SM: the operand ring and the staggered warpgroups carry from tile to tile
+  // (a tile's epilogue under the next tile's mainloop).  Round 1 (no stagger):
+  // 2 tiles for K < 1024, 1 above; round 2 (r3i/r3j): C2 2 -> 3-4 tiles 0.913 ->
+  // 0.919-0.921, C3 1 -> 2-4 tiles 32.2 -> 32.5-32.6 TFLOP/s, C5 33.8 -> 34.2
+  (void)K;
+  const int sms = num_sms();
+  return total >= 4 * sms ? 4 : total >= 3 * sms ? 3 : total >= 2 * sms ? 2 : 1;
 }
 
 template <bool TB, int G, bool TRI = false>
