@@ -83,6 +83,8 @@ Runtime::Runtime(Backend* be, int ndev, int nstreams, uint32_t sched, uint32_t f
       ktime_((flags & (SFX_FLAG_TRACE | SFX_FLAG_KTIME)) != 0) {
   paused_ = (flags & SFX_FLAG_PAUSED) != 0;
   nurgent_ = nstreams >= 2 ? std::max(2, nstreams / 4) : 0;
+  const char* rm = getenv("SFX_SUBMIT_RING");
+  ring_mode_ = !(rm && rm[0] == '0');
 }
 
 int Runtime::init(const uint64_t* arena_bytes, std::string& err) {
@@ -154,6 +156,7 @@ Runtime::~Runtime() {
 
 int Runtime::graph_create(uint32_t* gid) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   auto g = std::make_unique<Graph>();
   g->gid = next_gid_++;
   *gid = g->gid;
@@ -164,6 +167,7 @@ int Runtime::graph_create(uint32_t* gid) {
 int Runtime::reg(uint32_t gid, uint64_t hid, void* host, uint64_t bytes, int64_t rows, int64_t cols, int64_t ld,
                  int32_t dtype) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   auto git = graphs_.find(gid);
   if (git == graphs_.end()) {
     last_error = fmt("unknown graph %u", gid);
@@ -234,6 +238,7 @@ int Runtime::reg(uint32_t gid, uint64_t hid, void* host, uint64_t bytes, int64_t
 
 int Runtime::set_home(uint64_t hid, int dev) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   auto it = handles_.find(hid);
   if (it == handles_.end()) {
     last_error = "set_home: unknown handle";
@@ -274,6 +279,7 @@ int Runtime::retire_blocks(Handle* h) {
 
 int Runtime::unreg(uint64_t hid) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   auto it = handles_.find(hid);
   if (it == handles_.end()) {
     last_error = "object is not registered";
@@ -527,15 +533,73 @@ void Runtime::bind(Task* t, Handle* h, uint32_t mode) {
 }
 
 int Runtime::submit(uint32_t n, const sfx_task_desc* descs, const sfx_access* acc) {
-  std::unique_lock<std::mutex> lk(mu_);
+  if (!ring_mode_ || n > 16) {
+    // batched insertion (insert_gemm / insert_cholesky hand over a block row at a
+    // time): the inserter binds it itself, outside the executors' threads -- a
+    // thousand-task batch drained by an executor would hold up its launches
+    std::unique_lock<std::mutex> lk(mu_);
+    drain_locked();  // keep submission order
+    return submit_bound(n, descs, acc, true);
+  }
+  // validate on the calling thread; queue the valid prefix
+  uint32_t ok = 0;
+  size_t nacc = 0;
+  int rc = 0;
+  for (; ok < n; ++ok) {
+    std::string err;
+    rc = validate(descs[ok], acc + nacc, err);
+    if (rc) {
+      last_error = err;
+      break;
+    }
+    nacc += descs[ok].n_access;
+  }
+  if (ok > 0) {
+    {
+      std::lock_guard<std::mutex> g(ring_mu_);
+      ring_descs_.insert(ring_descs_.end(), descs, descs + ok);
+      ring_acc_.insert(ring_acc_.end(), acc, acc + nacc);
+    }
+    ring_pending_.store(true);
+    if (mu_.try_lock()) {  // nobody busy: bind now
+      drain_locked();
+      mu_.unlock();
+    } else if (sleepers_.load() > 0) {  // an executor is going to sleep: make sure it is bound
+      std::unique_lock<std::mutex> lk(mu_);
+      drain_locked();
+    }
+  }
+  return rc;
+}
+
+void Runtime::drain_locked() {
+  if (!ring_pending_.load()) return;
+  {
+    std::lock_guard<std::mutex> g(ring_mu_);
+    ring_pending_.store(false);
+    ring_descs_spare_.swap(ring_descs_);
+    ring_acc_spare_.swap(ring_acc_);
+  }
+  if (!ring_descs_spare_.empty()) {
+    const int rc = submit_bound(static_cast<uint32_t>(ring_descs_spare_.size()), ring_descs_spare_.data(),
+                                ring_acc_spare_.data(), false);
+    if (rc) poison(rc, "queued submission: " + last_error);
+  }
+  ring_descs_spare_.clear();
+  ring_acc_spare_.clear();
+}
+
+int Runtime::submit_bound(uint32_t n, const sfx_task_desc* descs, const sfx_access* acc, bool check) {
   size_t ai = 0;
   for (uint32_t i = 0; i < n; ++i) {
     const sfx_task_desc& d = descs[i];
-    std::string err;
-    int rc = validate(d, acc + ai, err);
-    if (rc) {
-      last_error = err;
-      return rc;
+    if (check) {
+      std::string err;
+      const int rc = validate(d, acc + ai, err);
+      if (rc) {
+        last_error = err;
+        return rc;
+      }
     }
     if (tasks_by_tid_.count(d.tid)) {
       last_error = fmt("task id %llu reused", (unsigned long long)d.tid);
@@ -1445,6 +1509,7 @@ void Runtime::extern_handoff(Task* t) {
 
 int Runtime::extern_poll(uint64_t* tids, uint64_t cap, uint64_t* n, double timeout_s) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   auto ready = [&] { return stopping_ || fail_code_ != 0 || !extern_ready_.empty(); };
   if (timeout_s < 0)
     extern_cv_.wait(lk, ready);
@@ -1461,6 +1526,7 @@ int Runtime::extern_poll(uint64_t* tids, uint64_t cap, uint64_t* n, double timeo
 
 int Runtime::extern_done(uint64_t tid, int status, const char* msg) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   auto it = tasks_by_tid_.find(tid);
   if (it == tasks_by_tid_.end() || it->second->op != SFX_OP_EXTERN || !it->second->detached) {
     last_error = "extern_done: not an external task handed out by sfx_extern_poll";
@@ -1484,6 +1550,7 @@ int Runtime::extern_done(uint64_t tid, int status, const char* msg) {
 
 int Runtime::fail(const std::string& msg) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   poison(SFX_ERR_ENGINE_FAILED, msg);
   return SFX_OK;
 }
@@ -1609,9 +1676,18 @@ void Runtime::exec_loop(int d) {
       return !paused_ && !fail_code_ && D.queue.size() > 0 && D.ninflight < static_cast<int>(window_) &&
              free_stream(D.queue.peek()) >= 0;
     };
+    drain_locked();  // submissions queued while mu_ was busy
     while (!(stopping_ || runnable() || (prefetch_ && D.prefetch_pending && !paused_ && !fail_code_))) {
       D.exec_sleeping = true;
+      sleepers_.fetch_add(1);
+      if (ring_pending_.load()) {  // queued after the drain above: bind them instead of sleeping
+        sleepers_.fetch_sub(1);
+        D.exec_sleeping = false;
+        drain_locked();
+        continue;
+      }
       D.exec_cv.wait(lk);
+      sleepers_.fetch_sub(1);
       D.exec_sleeping = false;
     }
     if (stopping_) return;
@@ -1910,6 +1986,7 @@ void Runtime::comp_loop(int d) {
 
 int Runtime::pause(bool p) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   paused_ = p;
   if (!p)
     for (auto& d : devs_) d->exec_cv.notify_all();
@@ -1918,6 +1995,7 @@ int Runtime::pause(bool p) {
 
 int Runtime::wait_all(uint32_t gid, double timeout_s) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   auto it = graphs_.find(gid);
   if (it == graphs_.end()) {
     last_error = fmt("unknown graph %u", gid);
@@ -1939,6 +2017,7 @@ int Runtime::wait_all(uint32_t gid, double timeout_s) {
 
 int Runtime::wait_task(uint64_t tid, double timeout_s) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   auto it = tasks_by_tid_.find(tid);
   if (it == tasks_by_tid_.end()) {
     if (tid && tid <= max_tid_ && retired_tasks_) return SFX_OK;  // retired: it finished
@@ -1961,6 +2040,7 @@ int Runtime::wait_task(uint64_t tid, double timeout_s) {
 
 int Runtime::task_state(uint64_t tid, int32_t* st) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   auto it = tasks_by_tid_.find(tid);
   if (it == tasks_by_tid_.end()) {
     if (tid && tid <= max_tid_ && retired_tasks_) {  // retired by a history-free graph: it finished
@@ -1976,6 +2056,7 @@ int Runtime::task_state(uint64_t tid, int32_t* st) {
 
 int Runtime::stats(int dev, sfx_dev_stats* out) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   if (dev < 0 || dev >= ndev_) {
     last_error = "bad device index";
     return SFX_ERR_CONFIG;
@@ -2007,6 +2088,7 @@ int Runtime::stats(int dev, sfx_dev_stats* out) {
 
 int Runtime::resident(int dev, uint64_t* hids, uint64_t cap, uint64_t* n) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   if (dev < 0 || dev >= ndev_) {
     last_error = "bad device index";
     return SFX_ERR_CONFIG;
@@ -2022,6 +2104,7 @@ int Runtime::resident(int dev, uint64_t* hids, uint64_t cap, uint64_t* n) {
 
 int Runtime::block_state(uint64_t hid, int dev, int32_t* st, int32_t* host_valid) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   Handle* h = nullptr;
   for (auto& hp : handle_store_)
     if (hp->hid == hid) h = hp.get();
@@ -2037,6 +2120,7 @@ int Runtime::block_state(uint64_t hid, int dev, int32_t* st, int32_t* host_valid
 
 int Runtime::trace(uint32_t gid, sfx_event* buf, uint64_t cap, uint64_t* n) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   auto it = graphs_.find(gid);
   if (it == graphs_.end()) {
     last_error = "unknown graph";
@@ -2052,6 +2136,7 @@ int Runtime::trace(uint32_t gid, sfx_event* buf, uint64_t cap, uint64_t* n) {
 int Runtime::edges(uint32_t gid, uint64_t* src, uint64_t* dst, uint64_t* hid, uint64_t cap, uint64_t* n) {
   // trace.py:94-102 / 122-127: every member of slot i -> every member of slot i+1
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   auto it = graphs_.find(gid);
   if (it == graphs_.end()) {
     last_error = "unknown graph";
@@ -2078,6 +2163,7 @@ int Runtime::violations(uint64_t* n) {
   // race detection on device timestamps: every edge must satisfy
   // start(dst) >= end(src) (handles.py:88-107 restated for streams)
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   uint64_t bad = 0;
   for (auto& hp : handle_store_) {
     Handle* h = hp.get();
@@ -2098,6 +2184,7 @@ int Runtime::violations(uint64_t* n) {
 
 int Runtime::set_option(const std::string& key, int64_t value) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   if (key == "group_max") {
     group_max_ = static_cast<uint32_t>(std::max<int64_t>(1, std::min<int64_t>(value, 1024)));
   } else if (key == "groups_per_stream") {
@@ -2130,6 +2217,7 @@ int Runtime::set_option(const std::string& key, int64_t value) {
 
 int Runtime::graph_option(uint32_t gid, const std::string& key, int64_t value) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   auto it = graphs_.find(gid);
   if (it == graphs_.end()) {
     last_error = fmt("unknown graph %u", gid);
@@ -2153,6 +2241,7 @@ int Runtime::graph_option(uint32_t gid, const std::string& key, int64_t value) {
 
 int Runtime::live(uint64_t* tasks, uint64_t* slots, uint64_t* retired) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   uint64_t ns = 0;
   for (auto& h : handle_store_) ns += h->slots.size();
   if (tasks) *tasks = live_tasks_;
@@ -2163,6 +2252,7 @@ int Runtime::live(uint64_t* tasks, uint64_t* slots, uint64_t* retired) {
 
 int Runtime::failure(int* code, char* msg, uint64_t cap) {
   std::unique_lock<std::mutex> lk(mu_);
+  drain_locked();
   *code = fail_code_;
   if (msg && cap) {
     strncpy(msg, fail_msg_.c_str(), cap - 1);

@@ -319,6 +319,10 @@ class Runtime {
   int set_home(uint64_t hid, int dev);
   int unreg(uint64_t hid);
   int submit(uint32_t n, const sfx_task_desc* tasks, const sfx_access* acc);
+  // bind + push (check: validate each first); the caller holds mu_
+  int submit_bound(uint32_t n, const sfx_task_desc* tasks, const sfx_access* acc, bool check);
+  // binds the submissions queued by submit() (ring mode); the caller holds mu_
+  void drain_locked();
   int flush(uint32_t gid, uint64_t tid, uint64_t hid, int write_mode);
   int pause(bool p);
   int wait_all(uint32_t gid, double timeout_s);
@@ -403,6 +407,20 @@ class Runtime {
   bool trace_;
   bool ktime_;  // trace_ || SFX_FLAG_KTIME: every launch group gets a timing start event
   std::mutex mu_;
+  // Submission ring (SFX_SUBMIT_RING=0: off).  submit() validates on the calling
+  // thread (the maps it reads are only changed by API calls of that thread) and
+  // queues the descriptors under ring_mu_; whoever holds mu_ next -- an executor
+  // at the top of its loop, any API call, or the inserter itself when mu_ is free
+  // -- binds them in submission order.  The inserter never waits for mu_ while an
+  // executor or a completion thread holds it.  An executor announces its sleep in
+  // sleepers_ before the last look at ring_pending_; an inserter that finds a
+  // sleeper after queueing drains itself (seq_cst both ways: no lost wake-up).
+  bool ring_mode_ = true;
+  std::mutex ring_mu_;
+  std::vector<sfx_task_desc> ring_descs_, ring_descs_spare_;
+  std::vector<sfx_access> ring_acc_, ring_acc_spare_;
+  std::atomic<bool> ring_pending_{false};
+  std::atomic<int> sleepers_{0};
   std::condition_variable done_cv_;
   std::condition_variable extern_cv_;
   std::deque<Task*> extern_ready_;  // SFX_OP_EXTERN tasks whose host buffers are current
