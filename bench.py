@@ -659,7 +659,10 @@ def cholesky_run(sf, alg, ordinals, n, b, streams, group, reps, check, clocks=No
     mem = None
     if len(set(ordinals)) < ndev:
         # logical devices sharing a GPU (host-side scaling runs): split its free HBM
-        mem = [int((torch.cuda.mem_get_info(o)[0] - (6 << 30)) / ordinals.count(o)) for o in ordinals]
+        # (the per-device streams' scratch and the cooperative kernels' workspaces
+        # come out of the headroom left beside the arenas: 2 GiB per logical device)
+        mem = [int((torch.cuda.mem_get_info(o)[0] - (6 << 30) - ordinals.count(o) * (2 << 30)) /
+                   ordinals.count(o)) for o in ordinals]
     eng = sf.create_engine(sf.WorkerTeam.of_devices(ndev, streams), scheduler="prio", trace=False,
                            ordinals=list(ordinals), group_max=group, device_memory=mem)
     M = alg.TiledMatrix(n, b, lower=True)

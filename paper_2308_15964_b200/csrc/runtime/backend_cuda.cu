@@ -56,11 +56,11 @@ class CudaBackend : public Backend {
     }
     if (D.tscratch_bytes[stream] < need) {
       // grow to the next power of two (a grouped TRSM launch needs one tile per
-      // member, so sizes vary from launch to launch: growing step by step meant a
-      // free + stream-ordered allocation on the executor's path for many groups,
-      // and with the default pool release threshold each of them could go back to
-      // the driver -- C3 factorizations took up to 2.7x longer at random)
-      size_t want = size_t(64) << 20;  // one allocation per stream in the usual case
+      // member, so sizes vary from launch to launch); the allocations come from
+      // the device pool that init_device pre-backs and that keeps freed memory
+      // (with the default release threshold, pool growth went back to the driver
+      // on the executor's path: C3 factorizations took up to 2.7x longer at random)
+      size_t want = size_t(1) << 20;
       while (want < need) want <<= 1;
       need = want;
       if (D.tscratch[stream]) cudaFreeAsync(D.tscratch[stream], D.streams[stream]);
@@ -502,8 +502,13 @@ class CudaBackend : public Backend {
       const size_t one = static_cast<size_t>(f.o[1].rows) * f.o[1].cols * 8;
       double* X = static_cast<double*>(trsm_scratch(d, stream, one * ops.size()));
       if (!X) {
-        err = "grouped trsm scratch allocation failed";
-        return SFX_ERR_CUDA;
+        // not enough memory beside the arena for the group's scratch: one TRSM at
+        // a time (each needs a single tile of scratch)
+        for (const OpLaunch& op : ops) {
+          const int rc = launch(d, stream, op, err);
+          if (rc) return rc;
+        }
+        return SFX_OK;
       }
       const long long ldx = f.o[1].cols;
       std::vector<GemmDesc> g(ops.size());
