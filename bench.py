@@ -76,7 +76,15 @@ def parse():
                     help="launch-group size for the Cholesky legs (tools/chol_sweep.py: 8 best for b=1024)")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-check", action="store_true")
-    ap.add_argument("--e2e-skew", type=int, default=-1, help="insert_gemm skew on the e2e leg (-1: nt, 0: FIFO)")
+    ap.add_argument("--e2e-skew", type=int, default=-1, help="insert_gemm skew on the e2e leg (-1: 3 nt, 0: FIFO)")
+    ap.add_argument("--e2e-stage-stream", type=int, default=1,
+                    help="e2e leg: host staging copies on the copy stream (runtime option stage_stream)")
+    ap.add_argument("--e2e-stage-window", type=int, default=0,
+                    help="e2e leg: runtime option stage_window in MiB (0: off)")
+    ap.add_argument("--e2e-flush-priority", type=int, default=0, help="e2e leg: runtime option flush_priority")
+    ap.add_argument("--e2e-skew-block", type=int, default=-1,
+                    help="insert_gemm skew_block on the e2e leg (-1: nt / 2, 0: row-major chain offsets)")
+    ap.add_argument("--e2e-tile-block", type=int, default=0, help="insert_gemm tile_block on the e2e leg (overrides skew)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--overhead-n", type=int, default=1000)
@@ -531,11 +539,19 @@ def main_gemm(args, dist):
     # ---- e2e: host-resident inputs through the public API ----
     def e2e_step():
         # wavefront priorities (insert_gemm skew): the k-chains of the C tiles start
-        # staggered over nt waves, so C's staging (2 GiB H2D) and its flush
-        # (2 GiB D2H) spread over the step instead of piling up in the first and
-        # last waves (round 1, tools/e2e_probe.py: 25.7 -> 28.3 TFLOP/s with 2*nt;
-        # round 2, tools/e2e_timeline.py + r2x: nt ramps up faster, 29.3-29.8 -> 29.8-30.0)
-        alg.insert_gemm(g, A, B, C, skew=args.e2e_skew if args.e2e_skew >= 0 else nt)
+        # staggered, so C's staging (2 GiB H2D) and its flush (2 GiB D2H) spread
+        # over the step instead of piling up in the first and last waves (round 1,
+        # tools/e2e_probe.py: 25.7 -> 28.3 TFLOP/s).  Round 2 (tools/e2e_timeline.py,
+        # profiles/r2_e2e_timeline.md): the chains take their offsets in nt/2 x nt/2
+        # blocks (the first waves share half the rows of A and columns of B: more
+        # tasks per staged tile while PCIe is the bottleneck), spread over 3 nt
+        # waves, and the staging copies run in one FIFO on the copy stream
+        # (stage_stream): 29.8-30.2 -> 30.8-31.2 TFLOP/s.
+        if args.e2e_tile_block:
+            alg.insert_gemm(g, A, B, C, tile_block=args.e2e_tile_block)
+        else:
+            alg.insert_gemm(g, A, B, C, skew=args.e2e_skew if args.e2e_skew >= 0 else 3 * nt,
+                            skew_block=args.e2e_skew_block if args.e2e_skew_block >= 0 else max(1, nt // 2))
         for t in C.tiles.values():
             g.flush_to_host(t)                      # C back to the host (write-mode flush)
         for M in (A, B):
@@ -549,6 +565,9 @@ def main_gemm(args, dist):
     # the launch-group timing events serve the kernel roofline only (device leg);
     # the e2e leg runs the product configuration without them
     eng.set_option("kernel_timing", 0)
+    eng.set_option("stage_stream", args.e2e_stage_stream)
+    eng.set_option("stage_window", args.e2e_stage_window << 20)
+    eng.set_option("flush_priority", args.e2e_flush_priority)
     e2e_step()  # first pass moves everything to the host side
     s0 = eng.stats(0)
     et = []
@@ -568,7 +587,12 @@ def main_gemm(args, dist):
     d2h = (s1["bytes_from_device"] - s0["bytes_from_device"]) // ke
     e2e = {"value": flops * dist.world / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
-           "h2d_gbs": h2d / e2e_s / 1e9, "d2h_gbs": d2h / e2e_s / 1e9}
+           "h2d_gbs": h2d / e2e_s / 1e9, "d2h_gbs": d2h / e2e_s / 1e9,
+           "schedule": ({"tile_block": args.e2e_tile_block} if args.e2e_tile_block else
+                        {"skew": args.e2e_skew if args.e2e_skew >= 0 else 3 * nt,
+                         "skew_block": args.e2e_skew_block if args.e2e_skew_block >= 0 else max(1, nt // 2)})
+           | {"stage_stream": args.e2e_stage_stream, "stage_window_mib": args.e2e_stage_window,
+              "flush_priority": args.e2e_flush_priority, "groups_per_stream": 4}}
     if not args.no_check:
         # the host now holds C = (warmup + steps + 1 + ke) A B (every e2e pass accumulates)
         samples = verify.sample_tiles(nt, 3, seed=2)

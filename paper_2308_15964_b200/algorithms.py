@@ -161,7 +161,7 @@ def _emit(graph, fast):
 
 
 def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: bool = True,
-                priorities=False, tile_block: int = 0, skew: int = 0):
+                priorities=False, tile_block: int = 0, skew: int = 0, skew_block: int = 0):
     """C += A B over tiles, loop order i, j, k.
 
     ``priorities`` (False, True or a row-block height h): block row i gets priority
@@ -176,6 +176,10 @@ def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: boo
     its final flush spread over the run instead of piling up in the first and
     last waves.
 
+    ``skew_block`` = h > 0 (with ``skew``): the chains take their offsets in h x h
+    block order (block-row-major, row-major inside a block) instead of row-major
+    order, so the first waves' chains share h rows of A and h columns of B.
+
     ``tile_block`` = h > 0 (overrides ``priorities``): the C tiles are ranked in
     h x h blocks (block-row-major), each block's tasks one priority level above the
     next block's: a block needs only h rows of A and h columns of B, so when the
@@ -183,7 +187,17 @@ def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: boo
     """
     nt = A.nt
     if skew:
-        off = lambda i, j: int(skew) * (i * nt + j) // (nt * nt)  # noqa: E731
+        if skew_block:
+            hb = int(skew_block)
+
+            def chain_rank(i, j):
+                bi, bj = i // hb, j // hb
+                bh = min(hb, nt - bi * hb)  # rows in this block row
+                bw = min(hb, nt - bj * hb)
+                return bi * hb * nt + bj * hb * bh + (i - bi * hb) * bw + (j - bj * hb)
+            off = lambda i, j: int(skew) * chain_rank(i, j) // (nt * nt)  # noqa: E731
+        else:
+            off = lambda i, j: int(skew) * (i * nt + j) // (nt * nt)  # noqa: E731
     if tile_block:
         h = int(tile_block)
         nbc = (nt + h - 1) // h

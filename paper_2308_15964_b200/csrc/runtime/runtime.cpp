@@ -654,6 +654,7 @@ int Runtime::flush(uint32_t gid, uint64_t tid, uint64_t hid, int write_mode) {
   d.tid = tid;
   d.graph = gid;
   d.op = SFX_OP_FLUSH;
+  d.priority = flush_priority_;
   d.device = -1;
   d.n_access = 1;
   d.iparam[0] = write_mode;
@@ -1146,11 +1147,6 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
       wait_on(b->ready);
     } else {
       D.stats.misses += 1;
-      // the block may have been allocated by an earlier, failed plan over a range
-      // whose previous contents are still being written back on another stream:
-      // the copy into it must wait for that write-back (allocation-time waits
-      // only cover blocks allocated by this plan)
-      wait_pending_wb(d, s, b->off, b->size, acts);
       int src = -1;
       if (h->dirty_dev >= 0 && h->dirty_dev != d) {
         src = h->dirty_dev;
@@ -1161,6 +1157,18 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
             break;
           }
       }
+      // host staging on the copy stream: every H2D of this device in one FIFO
+      // (dispatch order = priority order), so the first groups' operands arrive
+      // first instead of every stream's copies sharing PCIe until all are done
+      const int cs = src < 0 && stage_stream_ ? pf_stream() : -1;
+      const int ws = cs >= 0 ? cs : s;
+      // the block may have been allocated by an earlier, failed plan over a range
+      // whose previous contents are still being written back on another stream:
+      // the copy into it must wait for that write-back (allocation-time waits
+      // only cover blocks allocated by this plan)
+      const size_t a0 = acts.size();
+      wait_pending_wb(d, ws, b->off, b->size, acts);
+      for (size_t q = a0; q < acts.size(); ++q) acts[q].stream = cs;
       if (src >= 0) {
         Block* sb = h->blocks[src];
         wait_on(sb->ready);
@@ -1179,24 +1187,34 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
           err = fmt("handle %llu has no valid copy anywhere", (unsigned long long)h->hid);
           return SFX_ERR_INTERNAL;
         }
-        wait_on(h->host_ready);
+        if (cs < 0) {
+          wait_on(h->host_ready);
+        } else if (h->host_ready && !h->host_ready->complete && !(h->host_ready->dev == d && h->host_ready->stream == cs)) {
+          Action w{Action::WAIT, h->host_ready};
+          w.stream = cs;
+          acts.push_back(w);
+        }
         if (debug_staging())
           fprintf(stderr, "[sfx] stage hid=%llu off=%llu stream=%d task=%llu host_ready=%s\n",
-                  (unsigned long long)h->hid, (unsigned long long)b->off, s, (unsigned long long)t->tid,
-                  !h->host_ready ? "none" : (h->host_ready->complete ? "complete" : (h->host_ready->stream == s ? "same-stream" : "waited")));
+                  (unsigned long long)h->hid, (unsigned long long)b->off, ws, (unsigned long long)t->tid,
+                  !h->host_ready ? "none" : (h->host_ready->complete ? "complete" : (h->host_ready->stream == ws ? "same-stream" : "waited")));
         Action cp{Action::H2D, nullptr};
         cp.host = h->host;
         cp.dst_off = b->off;
         cp.n = h->bytes;
+        cp.stream = cs;
         acts.push_back(cp);
         D.stats.bytes_to_device += h->bytes;
         D.stats.copies_to_device += 1;
       }
-      SyncP cs = new_sync(d, s, false);
-      acts.push_back(Action{Action::RECORD, cs});
-      t->copy_syncs.push_back(cs);
+      SyncP csync = new_sync(d, ws, false);
+      Action rec{Action::RECORD, csync};
+      rec.stream = cs;
+      acts.push_back(rec);
+      if (cs >= 0) acts.push_back(Action{Action::WAIT, csync});  // the group waits on its copy
+      t->copy_syncs.push_back(csync);
       b->valid = true;
-      b->ready = cs;
+      b->ready = csync;
     }
     b->stamp = ++D.clock;
     t->pinned.push_back(b);  // the pass-1 pin is released at completion
@@ -1248,7 +1266,9 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
 int Runtime::issue(int d, int s, const std::vector<Task*>& group, std::vector<Action>& acts,
                    std::vector<OpLaunch>& ops, std::string& err) {
   int rc = 0;
+  const int s_group = s;
   for (Action& a : acts) {
+    s = a.stream >= 0 ? a.stream : s_group;
     switch (a.kind) {
       case Action::WAIT: {
         if (debug_staging())
@@ -1278,6 +1298,7 @@ int Runtime::issue(int d, int s, const std::vector<Task*>& group, std::vector<Ac
     }
     if (rc) return rc;
   }
+  s = s_group;
   if (group.empty()) return 0;
   std::vector<OpLaunch> kern;
   kern.reserve(ops.size());
@@ -1427,6 +1448,7 @@ void Runtime::complete(Task* t) {
   if (!t->detached && t->end && !t->end->group_counted) {
     t->end->group_counted = true;
     D.stream_groups[t->stream] -= 1;
+    D.stage_inflight -= t->end->staged;
   }
   if (t->end) t->end->complete = true;
   if (t->start) t->start->complete = true;
@@ -1498,6 +1520,7 @@ void Runtime::extern_handoff(Task* t) {
   if (t->end && !t->end->group_counted) {
     t->end->group_counted = true;
     D.stream_groups[t->stream] -= 1;
+    D.stage_inflight -= t->end->staged;
   }
   D.ninflight -= 1;
   D.stream_inflight[t->stream] -= 1;
@@ -1672,9 +1695,19 @@ void Runtime::exec_loop(int d) {
       }
       return pick(t, 0, nstreams_);
     };
+    auto staging_bytes = [&](const Task* t) {
+      uint64_t n = 0;
+      for (const Access& a : t->acc)
+        if (!a.h->blocks[d]) n += std::max<uint64_t>((a.h->bytes + align_ - 1) / align_ * align_, align_);
+      return n;
+    };
+    auto stage_ok = [&] {
+      return !stage_window_ || D.stage_inflight == 0 ||
+             D.stage_inflight + staging_bytes(D.queue.peek()) <= stage_window_;
+    };
     auto runnable = [&] {
       return !paused_ && !fail_code_ && D.queue.size() > 0 && D.ninflight < static_cast<int>(window_) &&
-             free_stream(D.queue.peek()) >= 0;
+             free_stream(D.queue.peek()) >= 0 && stage_ok();
     };
     drain_locked();  // submissions queued while mu_ was busy
     while (!(stopping_ || runnable() || (prefetch_ && D.prefetch_pending && !paused_ && !fail_code_))) {
@@ -1720,12 +1753,6 @@ void Runtime::exec_loop(int d) {
     // eviction traffic (C3 with a 3 GiB arena: 25.9 -> 27.3 TFLOP/s).  (It first
     // served as the mitigation of the write-back race fixed in plan() pass 2; with
     // SFX_GROUP_NO_STAGE_LIMIT=1 the limit is off, tools/arena_stress.py stays correct.)
-    auto staging_bytes = [&](const Task* t) {
-      uint64_t n = 0;
-      for (const Access& a : t->acc)
-        if (!a.h->blocks[d]) n += std::max<uint64_t>((a.h->bytes + align_ - 1) / align_ * align_, align_);
-      return n;
-    };
     static const bool no_stage_limit = getenv("SFX_GROUP_NO_STAGE_LIMIT") != nullptr;  // for stress tests
     uint64_t group_stage = staging_bytes(first);
     if (groupable(first) && (no_stage_limit || group_stage <= D.free_bytes)) {
@@ -1847,19 +1874,30 @@ void Runtime::exec_loop(int d) {
     {
       // every stream wait first, then the group's start stamp, then copies:
       // waiting earlier is always safe and keeps start >= every predecessor's end
+      // -- except waits on this group's own staging copies (copy stream, not yet
+      // recorded: they follow their RECORD) and the copy stream's own waits
       std::vector<Action> ordered;
       ordered.reserve(acts.size() + 1);
+      const int pfs = pf_stream();
+      auto hoist = [&](const Action& a) {
+        return a.kind == Action::WAIT && a.stream < 0 &&
+               !(a.sync->dev == d && a.sync->stream == pfs && !a.sync->recorded.load(std::memory_order_acquire));
+      };
       for (auto& a : acts)
-        if (a.kind == Action::WAIT) ordered.push_back(a);
+        if (hoist(a)) ordered.push_back(a);
       if (gstart && !ktime_kernel_only_) ordered.push_back(Action{Action::RECORD, gstart});
       for (auto& a : acts)
-        if (a.kind != Action::WAIT) ordered.push_back(a);
+        if (!hoist(a)) ordered.push_back(a);
       if (gstart && ktime_kernel_only_) ordered.push_back(Action{Action::RECORD, gstart});
       acts.swap(ordered);
     }
     D.ninflight += static_cast<int>(group.size());
     D.stream_inflight[s] += static_cast<int>(group.size());
     D.stream_groups[s] += 1;
+    if (stage_window_) {
+      gend->staged = group_stage;
+      D.stage_inflight += group_stage;
+    }
     const int64_t t_plan1 = now_ns();
     D.stats.t_plan_ns += t_plan1 - t_busy0;
     lk.unlock();
@@ -2200,6 +2238,13 @@ int Runtime::set_option(const std::string& key, int64_t value) {
     urgent_priority_ = value;
   } else if (key == "prefetch") {
     prefetch_ = value != 0 && !be_->is_sim();
+  } else if (key == "stage_stream") {
+    stage_stream_ = value != 0 && !be_->is_sim();
+  } else if (key == "flush_priority") {
+    flush_priority_ = static_cast<int32_t>(value);
+  } else if (key == "stage_window") {
+    stage_window_ = static_cast<uint64_t>(std::max<int64_t>(0, value));
+    for (auto& d : devs_) d->wake_exec();
   } else if (key == "prefetch_depth") {
     prefetch_depth_ = static_cast<int>(std::max<int64_t>(0, value));
   } else if (key == "kernel_timing") {

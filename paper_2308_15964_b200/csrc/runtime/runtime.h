@@ -68,6 +68,7 @@ struct Sync {
   std::atomic<bool> recorded{false};
   bool complete = false;       // guarded by the runtime mutex
   bool group_counted = false;  // launch group already retired from its stream
+  uint64_t staged = 0;         // launch group: bytes it staged from the host (stage window)
   bool group_timed = false;    // launch group duration already accumulated (KTIME)
   int64_t t_ns = 0;            // host-clock time of the event, resolved by the completion
   bool t_resolved = false;     // thread OUTSIDE the runtime mutex (only it touches these)
@@ -192,6 +193,7 @@ struct Action {
   uint64_t dst_off = 0, src_off = 0, n = 0;
   void* host = nullptr;
   int src_dev = -1;
+  int stream = -1;  // >= 0: issued on this stream instead of the group's (host staging stream)
 };
 
 // Device/stream abstraction: CUDA (B200) or host-memory simulation (tests).
@@ -305,6 +307,7 @@ struct Device {
   sfx_dev_stats stats{};
   std::vector<std::pair<int64_t, int64_t>> kintervals;  // KTIME group [start, end] not yet folded into busy_ns
   bool prefetch_pending = false;  // ready queue changed since the last prefetch pass
+  uint64_t stage_inflight = 0;    // host bytes staged by launch groups still in flight
 };
 
 class Runtime {
@@ -400,6 +403,16 @@ class Runtime {
   // operands of tasks waiting in its queue on a dedicated copy stream, so PCIe
   // transfers overlap compute (never evicts; keeps capacity/8 free).
   bool prefetch_ = true;
+  // host -> device staging of task operands on the device's copy stream (one
+  // FIFO in dispatch = priority order) instead of each group's own stream
+  bool stage_stream_ = false;
+  // > 0: a launch group that has to stage operands from the host waits while the
+  // groups in flight already stage this many bytes (keeps the copy FIFO short, so
+  // the next priority level's operands are not queued behind a whole wave's)
+  uint64_t stage_window_ = 0;
+  // priority of flush tasks (the reference's flushes are plain tasks, priority 0);
+  // a high value returns finished tiles while lower-priority work still runs
+  int32_t flush_priority_ = 0;
   int prefetch_depth_ = 64;
   int pf_stream() const { return nstreams_ + nurgent_ + ncoop_; }
   int plan_prefetch(int d, std::vector<Action>& acts);

@@ -272,15 +272,18 @@ def test_full_inverse_rejects_unsupported_sizes(gpu_engine):
         g.task(sf.write(A), device=sf.ops.potrf_fullinv)
 
 
-def test_cholesky_under_a_small_arena_evicts_and_matches_oracle():
+@pytest.mark.parametrize("stage_stream", [0, 1])
+def test_cholesky_under_a_small_arena_evicts_and_matches_oracle(stage_stream):
     """The LRU tile cache on real HBM: a working set 2.7x the arena forces
     evictions with dirty write-backs and re-staging mid-factorization; the factor
-    still matches the oracle."""
+    still matches the oracle.  stage_stream = 1: the host stagings go through the
+    copy stream and must wait for the write-backs of the space they reuse."""
     n, b = 2048, 256
     objs = programs.cholesky_operands(n, b)
     want = {k: v.copy() for k, v in objs.items()}
     programs.run_on_oracle(programs.cholesky_program(n // b), want, workers=4).stop()
     eng = sf.create_engine(sf.WorkerTeam.of_devices(1, 4), device_memory=(36 * b * b * 8) * 10 // 27)
+    eng.set_option("stage_stream", stage_stream)
     try:
         M = alg.TiledMatrix(n, b, lower=True)
         for ij, t in M.tiles.items():
@@ -294,6 +297,40 @@ def test_cholesky_under_a_small_arena_evicts_and_matches_oracle():
         L = M.to_dense(lower_only=True)
         Lw = programs.assemble_lower(want, n, b)
         assert np.abs(L - Lw).max() / np.abs(Lw).max() <= 1e-12
+    finally:
+        eng.stop()
+
+
+@pytest.mark.parametrize("window", [0, 8 << 20])
+def test_staging_on_the_copy_stream_tiled_gemm_matches_numpy(window):
+    """stage_stream = 1 (bench.py's e2e leg): every host->device staging copy in one
+    FIFO on the copy stream, the launch groups waiting on their copies' events --
+    including groups whose later tasks read a tile an earlier task of the same
+    group staged.  window > 0: a group that stages waits while 8 MiB of staging
+    is in flight.  Two passes over host-resident tiles, then numpy."""
+    n, b = 2048, 256
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, 8), device_memory=1 << 30, group_max=16)
+    eng.set_option("stage_stream", 1)
+    eng.set_option("stage_window", window)
+    try:
+        rng = np.random.default_rng(7)
+        A, B, C = (alg.TiledMatrix(n, b) for _ in range(3))
+        for M in (A, B):
+            for t in M.tiles.values():
+                t[...] = rng.standard_normal(t.shape)
+        for t in C.tiles.values():
+            t[...] = 0.0
+        g = sf.TaskGraph().compute_on(eng)
+        for _ in range(2):
+            alg.insert_gemm(g, A, B, C, skew=n // b)
+            for M in (C, A, B):
+                for t in M.tiles.values():
+                    g.flush_to_host(t)
+            assert g.wait_all(timeout=120)
+        want = 2.0 * (A.to_dense() @ B.to_dense())
+        got = C.to_dense()
+        assert np.abs(got - want).max() / np.abs(want).max() <= 1e-12
+        assert eng.stats(0)["copies_to_device"] > 0
     finally:
         eng.stop()
 

@@ -58,6 +58,30 @@ def test_gemm_fast_matches_loop(engine, priorities):
     assert len(slow) == 4 ** 3
 
 
+@pytest.mark.parametrize("skew,skew_block", [(4, 0), (12, 2), (12, 3)])
+def test_gemm_skew_priorities_fast_matches_loop(engine, skew, skew_block):
+    # wavefront priorities (bench.py's e2e leg): task (i, j, k) gets -(k + offset of
+    # chain (i, j)); with skew_block h the chains are ranked in h x h blocks
+    nt = 4
+    A, B, C = (alg.TiledMatrix(nt * 16, 16, pinned=False, sim=True) for _ in range(3))
+    g = sf.TaskGraph().compute_on(engine)
+    seq = _capture(g)
+    alg.insert_gemm(g, A, B, C, fast=False, skew=skew, skew_block=skew_block)
+    slow = _norm(seq)
+    seq.clear()
+    alg.insert_gemm(g, A, B, C, fast=True, skew=skew, skew_block=skew_block)
+    assert _norm(seq) == slow
+    # loop order i, j, k: the chain offsets, in block order when skew_block > 0
+    offs = {}
+    for n, (_, _, _, p, _, _) in enumerate(slow):
+        i, j, k = n // (nt * nt), (n // nt) % nt, n % nt
+        offs.setdefault((i, j), -p - k)
+        assert -p - k == offs[(i, j)]
+    h = skew_block or nt
+    order = sorted(offs, key=lambda ij: (ij[0] // h, ij[1] // h, ij[0], ij[1]) if skew_block else ij)
+    assert [offs[c] for c in order] == [skew * r // (nt * nt) for r in range(nt * nt)]
+
+
 def test_cholesky_fast_matches_loop(engine):
     A = alg.TiledMatrix(80, 16, lower=True, pinned=False, sim=True)
     g = sf.TaskGraph().compute_on(engine)
