@@ -92,6 +92,7 @@ struct GemmGroup {
   int zero;     // always 0 at run time (the compiler cannot know): see the stage release
   int stagger;  // warpgroup 1 starts this many k-steps behind warpgroup 0 (SFX_GEMM_STAGGER, 0: off)
   int release;  // stage release: 0 = data-dependent arrive (default), 1 = fence.acq_rel.cta (A/B experiments)
+  int cstore;   // cpref epilogue: results written back into the C buffer and stored by TMA (per warp)
   double alpha, beta;
 };
 
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
       ptx::mbar_init(&empty[s], CONSUMER_WARPS);
     }
     ptx::mbar_init(cfull, 1);
-    ptx::mbar_init(cempty, CONSUMER_WARPS * 32);
+    ptx::mbar_init(cempty, p.cstore ? CONSUMER_WARPS : CONSUMER_WARPS * 32);
     ptx::mbar_init(stagger, CONSUMER_WARPS / 2);
     ptx::fence_mbar_init();
   }
@@ -230,8 +231,13 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
           if (cn > 0) ptx::mbar_wait(cempty, (cn - 1) & 1);
           ptx::mbar_arrive_expect_tx(cfull, C_BUF);
           const CUtensorMap* tmC = &p.t[task].c;
+          // boxes of 16 columns x 64 rows (the TMA-store epilogue writes each warp's
+          // 64 x 32 block back as two of them)
 #pragma unroll
-          for (int q = 0; q < BN / 16; ++q) ptx::tma_load_2d(sC + q * (BM * 128), tmC, n0 + 16 * q, m0, cfull);
+          for (int q = 0; q < BN / 16; ++q)
+#pragma unroll
+            for (int hh = 0; hh < BM / 64; ++hh)
+              ptx::tma_load_2d(sC + q * (BM * 128) + hh * (64 * 128), tmC, n0 + 16 * q, m0 + 64 * hh, cfull);
           ++cn;
         };
         for (int kt = kt0; kt < kt1; ++kt, ++it) {
@@ -267,6 +273,19 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
 #define ACCX(i, P) ((TRANS_B || !NN_COLPERM) ? acc[i][P][0] : acc[i][2 * ((P)&1)][(P) >> 1])
 #define ACCY(i, P) ((TRANS_B || !NN_COLPERM) ? acc[i][P][1] : acc[i][2 * ((P)&1) + 1][(P) >> 1])
   int it = 0, cn = 0;
+  // TMA-store epilogue: this warp's C-buffer release waits for its bulk store to
+  // have read shared memory -- deferred to the next tile's first k-step, so the
+  // warp goes straight back to its DMMAs
+  bool cpend = false;
+  auto release_c = [&]() {
+    if (cpend) {
+      if (lane == 0) {
+        ptx::bulk_wait_read0();
+        ptx::mbar_arrive(cempty);
+      }
+      cpend = false;
+    }
+  };
   for (int lin = blockIdx.x; lin < total; lin += gridDim.x) {
     int task, m0, n0, kt0, kt1;
     coords(lin, task, m0, n0, kt0, kt1);
@@ -286,6 +305,7 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
       if (it == p.stagger && wm == 0 && lane == 0 && p.stagger) ptx::mbar_arrive(stagger);
       if (it == 0 && wm == 1 && p.stagger) ptx::mbar_wait(stagger, 0);
       ptx::mbar_wait(&full[s], (it / STAGES) & 1);
+      release_c();
       if (TRI && kt * BK >= n0 + wn * 32 + 32) {
         // TRI: every B operand of this warp's columns is below the diagonal in
         // this k-step (exact zeros): no loads, no DMMAs, just release the stage
@@ -423,8 +443,41 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
     if (interior && p.cpref) {
       // C from the prefetch buffer: element (r, c) of the tile sits in box q = c / 16
       // at r * 128 + (((c % 16) / 2) ^ (r % 8)) * 16 + (c % 2) * 8
+      release_c();  // (a tile without k-steps)
       ptx::mbar_wait(cfull, cn & 1);
       const uint32_t cS = ptx::smem_u32(sC);
+      if (p.cstore) {
+        // results back into the buffer (each thread rewrites the elements it read),
+        // then one lane stores the warp's two 16 x 64 boxes by TMA
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = wm * 64 + 8 * i + g;
+#pragma unroll
+          for (int P = 0; P < 4; ++P) {
+            const int c = wn * 32 + PCOL(P);
+            const uint32_t ad = cS + (c >> 4) * (BM * 128) + r * 128 + ((((c & 15) >> 1) ^ g) << 4);
+            const double2 cv = ptx::lds128(ad);
+            double2 v;
+            v.x = fma(p.beta, cv.x, p.alpha * ACCX(i, P));
+            v.y = fma(p.beta, cv.y, p.alpha * ACCY(i, P));
+            ptx::sts128(ad, v);
+          }
+        }
+        ptx::fence_proxy_async();  // generic-proxy writes -> visible to the TMA store
+        __syncwarp();
+        if (lane == 0) {
+          const CUtensorMap* tmC = &p.t[task].c;
+#pragma unroll
+          for (int qq = 0; qq < 2; ++qq) {
+            const int q = 2 * wn + qq;
+            ptx::tma_store_2d(tmC, n0 + 16 * q, m0 + 64 * wm, cS + q * (BM * 128) + wm * (64 * 128));
+          }
+          ptx::bulk_commit();
+        }
+        cpend = true;
+        ++cn;
+        continue;
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int r = wm * 64 + 8 * i + g;
@@ -506,6 +559,8 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
   }
   // a CTA whose whole work is shorter than the stagger still releases warpgroup 1
   if (wm == 0 && lane == 0 && p.stagger && it <= p.stagger) ptx::mbar_arrive(stagger);
+  // outstanding TMA stores read this CTA's shared memory: complete them before exit
+  if (p.cstore && lane == 0) ptx::bulk_wait0();
 #undef PCOL
 #undef ACCX
 #undef ACCY
@@ -695,7 +750,9 @@ cudaError_t launch_group_t(const GemmDesc* d, int n, int M, int N, int K, double
   p.cpref = want_cpref && p.ksplit == 1 && !p.tri_split ? 1 : 0;
   if (p.cpref)
     for (int i = 0; i < n; ++i)
-      if (!make_tmap_f64_2d(&p.t[i].c, d[i].C, N, M, d[i].ldc, 16, BM, true)) return cudaErrorInvalidValue;
+      if (!make_tmap_f64_2d(&p.t[i].c, d[i].C, N, M, d[i].ldc, 16, 64, true)) return cudaErrorInvalidValue;
+  static const int cstore_mode = getenv("SFX_GEMM_TMA_STORE") ? atoi(getenv("SFX_GEMM_TMA_STORE")) : 0;
+  p.cstore = p.cpref && cstore_mode ? 1 : 0;
   // K-weighted TRI split: one-unit items (BN/BK k-steps each), or two-unit items
   // (half the atomic epilogues) once one-unit items would fill the SMs more than
   // once over
