@@ -59,6 +59,9 @@ extern "C" {
                                       non-positive pivot, LAPACK info > 0); the cause
                                       of an engine failure, like the LinAlgError the
                                       oracle's np.linalg.cholesky raises              */
+#define SFX_ERR_USER (-11)        /* a user op's launcher returned non-zero (the cause of
+                                      an engine failure, like a failing device= callable
+                                      in the reference, engine.py:154-157)          */
 
 /* ---- access modes (access.py:16-21) ---- */
 #define SFX_READ 0
@@ -118,6 +121,9 @@ extern "C" {
 #define SFX_OP_ZERO 33         /* A = 0                                                  */
 #define SFX_OP_DACC 34         /* A += B1 + ... + Bk (FP64, same rows x cols, k = 1..7):
                                   the reduction of per-GPU partial accumulators        */
+#define SFX_OP_USER_BASE 256   /* user ops registered with sfx_register_op get the codes
+                                  SFX_OP_USER_BASE .. SFX_OP_USER_BASE + SFX_OP_USER_MAX - 1 */
+#define SFX_OP_USER_MAX 64
 
 /* ---- trace event kinds (trace.py:14-21) ---- */
 #define SFX_EV_PUSH 0
@@ -294,6 +300,32 @@ int sfx_fp64_dfma_peak(int ordinal, double* tflops);
 #define SFX_GEMM_NT 10               /* B stored N x K (Cholesky update, DSYRK)             */
 #define SFX_GEMM_PATHS 11
 int sfx_gemm_paths(uint64_t* out, uint32_t n);
+
+/* ---- user ops: the reference's device= callables (engine.py:144-149) ----
+ * A user op is a host-side LAUNCHER the executor calls, outside the runtime
+ * lock, on the thread that issues the task's stream work; it enqueues its own
+ * kernels on `stream` (a cudaStream_t; NULL on the simulated backend, where
+ * `data` are host pointers and the work runs synchronously).  `views` are the
+ * task's accesses in declaration order, staged and pinned like the built-in
+ * ops' operands -- the DeviceView of src/device.py:119-133 (device, size,
+ * descriptor, data, mode).  Return 0 on success; anything else fails the task
+ * and poisons the engine with SFX_ERR_USER (engine.py:154-157, 227-243).
+ * The runtime waits for the stream work like any op's (end event after the
+ * launcher returns), so the launcher must not synchronise. */
+typedef struct sfx_view {
+  void* data;           /* device pointer of the staged block                    */
+  uint64_t bytes;       /* DeviceView.size                                        */
+  int64_t rows, cols, ld; /* descriptor (elements; ld = row stride)                */
+  int32_t dtype;        /* SFX_DTYPE_* of the registered handle                    */
+  uint32_t mode;        /* SFX_READ ... of this access                             */
+  int32_t device;       /* runtime device index                                    */
+  int32_t reserved;
+} sfx_view;
+typedef int (*sfx_user_launch_fn)(const sfx_view* views, int nviews, void* stream, const double* fparam,
+                                  const int64_t* iparam, void* user);
+/* registers `fn` under `name` (<= 63 chars, unique) process-wide; *op gets the op
+ * code to put in sfx_task_desc.op.  User ops never join launch groups. */
+int sfx_register_op(const char* name, sfx_user_launch_fn fn, void* user, uint32_t* op);
 
 #ifdef __cplusplus
 }

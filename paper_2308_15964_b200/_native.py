@@ -19,6 +19,7 @@ from .errors import (
     RegistrationError,
     SeqflowError,
     StagingError,
+    TaskFailedError,
 )
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -35,6 +36,7 @@ ERR_DUPLICATE = -7
 ERR_REGISTRATION = -8
 ERR_UNSUPPORTED = -9
 ERR_NUMERIC = -10
+ERR_USER = -11
 
 READ, WRITE, ATOMIC_WRITE, COMMUTATIVE_WRITE, MAYBE_WRITE = 0, 1, 2, 3, 4
 
@@ -66,6 +68,7 @@ OP_FILL_SPD = 31
 OP_FILL_PARTICLES = 32
 OP_ZERO = 33
 OP_DACC = 34
+OP_USER_BASE, OP_USER_MAX = 256, 64  # sfx_register_op codes
 
 EV_PUSH, EV_POP, EV_START, EV_END, EV_STAGE_BEGIN, EV_STAGE_END = range(6)
 EV_NAMES = {EV_PUSH: "Push", EV_POP: "Pop", EV_START: "TaskStart", EV_END: "TaskEnd",
@@ -106,6 +109,18 @@ class DevStats(ctypes.Structure):
 class Event(ctypes.Structure):
     _fields_ = [("t_ns", ctypes.c_int64), ("tid", ctypes.c_uint64), ("kind", ctypes.c_int32),
                 ("worker", ctypes.c_int32), ("extra", ctypes.c_int64)]
+
+
+class View(ctypes.Structure):
+    """sfx_view: one staged operand handed to a user op's launcher."""
+    _fields_ = [("data", ctypes.c_void_p), ("bytes", ctypes.c_uint64), ("rows", ctypes.c_int64),
+                ("cols", ctypes.c_int64), ("ld", ctypes.c_int64), ("dtype", ctypes.c_int32),
+                ("mode", ctypes.c_uint32), ("device", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+# int (*)(const sfx_view*, int, void* stream, const double* fparam, const int64_t* iparam, void* user)
+USER_LAUNCH = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(View), ctypes.c_int, ctypes.c_void_p,
+                               ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p)
 
 
 def _load():
@@ -152,6 +167,7 @@ def _load():
         "sfx_fail": ([P, ctypes.c_char_p], ctypes.c_int),
         "sfx_graph_option": ([P, u32, ctypes.c_char_p, i64], ctypes.c_int),
         "sfx_live": ([P, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64)], ctypes.c_int),
+        "sfx_register_op": ([ctypes.c_char_p, P, P, ctypes.POINTER(u32)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -169,7 +185,7 @@ EXPORTED = ("sfx_abi_version", "sfx_device_count", "sfx_create", "sfx_destroy", 
             "sfx_task_state", "sfx_flush", "sfx_stats", "sfx_resident", "sfx_block_state",
             "sfx_trace", "sfx_edges", "sfx_violations", "sfx_set_option", "sfx_host_alloc", "sfx_host_free",
             "sfx_fp64_peak", "sfx_fp64_dfma_peak", "sfx_extern_poll", "sfx_extern_done", "sfx_gemm_paths", "sfx_fail",
-            "sfx_graph_option", "sfx_live")
+            "sfx_graph_option", "sfx_live", "sfx_register_op")
 
 GEMM_PATH_NAMES = ("launches", "tasks", "work_items", "cpref", "multi_tile", "cpref_multi_tile", "splitk", "tri",
                    "lower", "nn", "nt")
@@ -208,6 +224,7 @@ class NotPositiveDefiniteError(SeqflowError, np.linalg.LinAlgError):
 
 
 _ERRORS[ERR_NUMERIC] = NotPositiveDefiniteError
+_ERRORS[ERR_USER] = TaskFailedError  # a user op's launcher failed (a callable's own exception when it raised)
 
 
 def error_for(code: int, msg: str) -> Exception:

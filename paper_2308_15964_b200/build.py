@@ -91,7 +91,31 @@ def build(verbose: bool = False, force: bool = False) -> str:
         if verbose:
             print("linked", os.path.relpath(OUT, ROOT))
     _build_pyext(verbose, force)
+    _build_examples(nvcc, verbose, force)
     return OUT
+
+
+def _build_examples(nvcc, verbose: bool, force: bool) -> None:
+    """User-op examples (examples/*.cu): each its own shared library, loaded
+    with ctypes and registered through sfx_register_op (ops.register)."""
+    exdir = os.path.join(PKG, "examples")
+    if not os.path.isdir(exdir):
+        return
+    hdr = os.path.getmtime(os.path.join(ROOT, "include", "sfx.h"))
+    for f in sorted(os.listdir(exdir)):
+        if not f.endswith(".cu"):
+            continue
+        src = os.path.join(exdir, f)
+        out = os.path.join(PKG, "libsfx_" + f[:-3] + ".so")
+        if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(src), hdr):
+            continue
+        cmd = [nvcc] + ARCH + COMMON + ["-shared", "-cudart", "static", src, "-o", out + ".tmp"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"example build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+        os.replace(out + ".tmp", out)
+        if verbose:
+            print("linked", os.path.relpath(out, ROOT))
 
 
 def _build_pyext(verbose: bool, force: bool) -> None:

@@ -195,6 +195,17 @@ int sfx_violations(sfx_runtime* r, uint64_t* n) {
   return guarded(r, [&](sfx::Runtime& rt) { return rt.violations(n); });
 }
 
+int sfx_register_op(const char* name, sfx_user_launch_fn fn, void* user, uint32_t* op) {
+  if (!op) {
+    g_err = "sfx_register_op: null op out-pointer";
+    return SFX_ERR_CONFIG;
+  }
+  std::string err;
+  const int rc = sfx::register_user_op(name, fn, user, op, err);
+  if (rc) g_err = err;
+  return rc;
+}
+
 int sfx_set_option(sfx_runtime* r, const char* key, int64_t value) {
   return guarded(r, [&](sfx::Runtime& rt) { return rt.set_option(key ? key : "", value); });
 }

@@ -323,7 +323,7 @@ class CudaBackend : public Backend {
       case SFX_OP_FILL_PARTICLES:
         return true;
       default:
-        return false;
+        return user_op(op) != nullptr;
     }
   }
 
@@ -441,9 +441,19 @@ class CudaBackend : public Backend {
         e = launch_p2p(f64(o[0]), o[0].ld, static_cast<int>(o[0].cols), nullptr, 0, 0, f64(o[1]), o[1].ld, nullptr, 0,
                        true, op.fp[0], s);
         break;
-      default:
-        err = "unsupported op";
-        return SFX_ERR_UNSUPPORTED;
+      default: {
+        const UserOp* u = user_op(op.op);
+        if (!u) {
+          err = "unsupported op";
+          return SFX_ERR_UNSUPPORTED;
+        }
+        cudaGetLastError();  // a launch error left by the launcher is its own
+        const int rc = run_user_op(*u, op, d, s, err);
+        if (rc) return rc;
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_err(e, (std::string("user op '") + u->name + "' launch").c_str(), err);
+        break;
+      }
     }
     return cuda_err(e, "kernel launch", err);
   }

@@ -78,10 +78,10 @@ class SimBackend : public Backend {
       case SFX_OP_ZERO:
         return true;
       default:
-        return false;
+        return user_op(op) != nullptr;
     }
   }
-  int launch(int, int, const OpLaunch& op, std::string& err) override {
+  int launch(int d, int, const OpLaunch& op, std::string& err) override {
     switch (op.op) {
       case SFX_OP_NOOP:
         return SFX_OK;
@@ -131,6 +131,7 @@ class SimBackend : public Backend {
         return SFX_OK;
       }
       default:
+        if (const UserOp* u = user_op(op.op)) return run_user_op(*u, op, d, nullptr, err);  // host pointers
         err = "op not available on the simulated backend";
         return SFX_ERR_UNSUPPORTED;
     }

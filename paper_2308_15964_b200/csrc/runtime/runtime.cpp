@@ -70,6 +70,56 @@ static std::string fmt(const char* f, ...) {
   return buf;
 }
 
+// ---- user ops (sfx_register_op) ---------------------------------------------
+static UserOp g_user_ops[SFX_OP_USER_MAX];
+static std::atomic<uint32_t> g_user_count{0};
+static std::mutex g_user_mu;
+
+const UserOp* user_op(uint32_t op) {
+  if (op < SFX_OP_USER_BASE) return nullptr;
+  const uint32_t k = op - SFX_OP_USER_BASE;
+  return k < g_user_count.load(std::memory_order_acquire) ? &g_user_ops[k] : nullptr;
+}
+
+int register_user_op(const char* name, sfx_user_launch_fn fn, void* user, uint32_t* op, std::string& err) {
+  if (!name || !*name || strlen(name) >= sizeof(UserOp::name) || !fn) {
+    err = "sfx_register_op: needs a name of 1..63 characters and a launcher";
+    return SFX_ERR_CONFIG;
+  }
+  std::lock_guard<std::mutex> g(g_user_mu);
+  const uint32_t n = g_user_count.load(std::memory_order_relaxed);
+  for (uint32_t k = 0; k < n; ++k)
+    if (!strcmp(g_user_ops[k].name, name)) {
+      err = fmt("sfx_register_op: an op named '%s' is already registered", name);
+      return SFX_ERR_CONFIG;
+    }
+  if (n >= SFX_OP_USER_MAX) {
+    err = fmt("sfx_register_op: at most %d user ops", SFX_OP_USER_MAX);
+    return SFX_ERR_CONFIG;
+  }
+  UserOp& u = g_user_ops[n];
+  snprintf(u.name, sizeof u.name, "%s", name);
+  u.fn = fn;
+  u.user = user;
+  g_user_count.store(n + 1, std::memory_order_release);  // publishes the entry
+  *op = SFX_OP_USER_BASE + n;
+  return SFX_OK;
+}
+
+int run_user_op(const UserOp& u, const OpLaunch& op, int dev, void* stream, std::string& err) {
+  sfx_view v[8];
+  for (int k = 0; k < op.n; ++k) {
+    const Operand& o = op.o[k];
+    v[k] = sfx_view{o.dptr, o.bytes, o.rows, o.cols, o.ld, o.dtype, o.mode, dev, 0};
+  }
+  const int rc = u.fn(v, op.n, stream, op.fp, op.ip, u.user);
+  if (rc) {
+    err = fmt("user op '%s' failed (launcher returned %d)", u.name, rc);
+    return SFX_ERR_USER;
+  }
+  return SFX_OK;
+}
+
 Runtime::Runtime(Backend* be, int ndev, int nstreams, uint32_t sched, uint32_t flags, uint32_t window,
                  uint64_t align)
     : be_(be),
@@ -501,6 +551,13 @@ int Runtime::validate(const sfx_task_desc& d, const sfx_access* acc, std::string
       if (!need(1)) return SFX_ERR_CONFIG;
       return 0;
     default:
+      if (user_op(d.op)) {  // user ops: up to 8 accesses, the launcher validates the rest
+        if (d.n_access > 8) {
+          err = "a user op takes at most 8 accesses";
+          return SFX_ERR_CONFIG;
+        }
+        return 0;
+      }
       err = fmt("unknown op %u", d.op);
       return SFX_ERR_CONFIG;
   }
@@ -1255,6 +1312,7 @@ int Runtime::plan(int d, int s, Task* t, std::vector<Action>& acts, OpLaunch& op
     op.o[k].cols = h->cols;
     op.o[k].ld = h->ld;
     op.o[k].dtype = h->dtype;
+    op.o[k].mode = t->acc[k].mode;
   }
   for (int k = 0; k < 4; ++k) {
     op.fp[k] = t->fp[k];
@@ -1907,7 +1965,7 @@ void Runtime::exec_loop(int d) {
     D.stats.groups += 1;
     lk.lock();
     if (rc) {
-      poison(SFX_ERR_CUDA, err);
+      poison(rc == SFX_ERR_USER ? SFX_ERR_USER : SFX_ERR_CUDA, err);
       continue;
     }
     const int64_t t_rel0 = now_ns();
@@ -1996,7 +2054,7 @@ void Runtime::comp_loop(int d) {
     if (rc) {
       // the context reports an error: fail the engine; the oldest task is retired
       // so that waiters are woken (the engine is poisoned either way)
-      poison(SFX_ERR_CUDA, err);
+      poison(rc == SFX_ERR_USER ? SFX_ERR_USER : SFX_ERR_CUDA, err);
       Task* t = D.inflight.front();
       D.inflight.pop_front();
       if (t->op == SFX_OP_EXTERN) {

@@ -174,6 +174,7 @@ struct Operand {
   uint64_t bytes = 0;
   int64_t rows = 0, cols = 0, ld = 0;
   int32_t dtype = 0;
+  uint32_t mode = 0;  // the task's access mode for this operand (user ops' views)
 };
 
 struct OpLaunch {
@@ -185,6 +186,18 @@ struct OpLaunch {
   double fp[4];
   int64_t ip[4];
 };
+
+// User ops (sfx_register_op): process-wide table of host-side launchers, written
+// once per code and read without a lock afterwards.
+struct UserOp {
+  char name[64];
+  sfx_user_launch_fn fn;
+  void* user;
+};
+const UserOp* user_op(uint32_t op);  // nullptr unless op is a registered user op
+int register_user_op(const char* name, sfx_user_launch_fn fn, void* user, uint32_t* op, std::string& err);
+// calls the launcher with the staged operands as views; SFX_ERR_USER on failure
+int run_user_op(const UserOp& u, const OpLaunch& op, int dev, void* stream, std::string& err);
 
 // One step of a planned task, issued outside the runtime lock.
 struct Action {

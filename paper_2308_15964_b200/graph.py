@@ -157,8 +157,19 @@ class TaskViewer:
         N.check(rc, g._h)
 
     def get_value(self):
-        """Device ops produce no host value (the reference raises ValueError then)."""
+        """The value a Python device callable returned; built-in and native ops
+        produce no host value (the reference raises ValueError then, task.py:241-262)."""
         self.wait()
+        g = self._graph
+        if self._tid in g._py_vals:
+            return g._py_vals[self._tid]
+        op = g._py_ops.get(self._tid)
+        if op is not None:
+            try:
+                v = g._py_vals[self._tid] = ops_mod.result_of(op)
+                return v
+            except KeyError:
+                pass
         raise ValueError(f"{self._graph._label(self._tid)} produced no value")
 
 
@@ -204,6 +215,8 @@ class TaskGraph:
         self._hval = None
         self._by_hid = {}
         self._names = {}
+        self._py_ops = {}   # tid -> Op of a Python device callable (get_value)
+        self._py_vals = {}  # tid -> its value, once fetched
         self._name_ranges = []  # (first tid, count, name) of array submissions
         self._tids = []
         self._tid_ranges = []   # (first tid, count) of array submissions
@@ -326,11 +339,17 @@ class TaskGraph:
         # native fast path (csrc/pyext/sfxfast.c): every object already registered,
         # no array views -> access codes, handle ids, a task id and the submit in C;
         # anything else (first use, views, errors) takes the Python path below
+        pyop = None
+        if device is not None and device.__class__ is not ops_mod.Op and callable(device):
+            # a Python device callable, as in the reference (engine.py:144-149): a user op
+            device = pyop = ops_mod.python_callable(device)
         if _fast_task is not None and host is None and self._hval is not None and self._batch is None:
             tid = _fast_task(self._hval, self._gid, self._hid_by_id, self._tids, accesses, device, priority)
             if tid > 0:
                 if name is not None:
                     self._names[tid] = name
+                if pyop is not None:
+                    self._py_ops[tid] = pyop
                 return TaskViewer(self, tid)
             if tid < -1:
                 N.check(tid, self._h)
@@ -377,6 +396,8 @@ class TaskGraph:
         if name is not None:
             self._names[tid] = name
         self._tids.append(tid)
+        if pyop is not None:
+            self._py_ops[tid] = pyop
         self._submit_one(tid, device, priority, hids, modes)
         return TaskViewer(self, tid)
 
@@ -495,6 +516,8 @@ class TaskGraph:
         N.lib.sfx_failure(self._h, ctypes.byref(code), msg, 1024)
         text = msg.value.decode(errors="replace")
         cause = N.error_for(code.value, text)
+        if code.value == N.ERR_USER:
+            cause = ops_mod.take_error() or cause  # the callable's own exception
         agent = getattr(self.engine, "_comm_agent", None)
         if agent is not None and agent.error is not None:
             cause = agent.error  # a communication task failed (e.g. CommProtocolError)

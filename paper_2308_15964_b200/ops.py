@@ -148,3 +148,188 @@ trsm_inv = dtrsm(inverse_blocks=True)
 potrf_inv = dpotrf(store_inverses=True)
 trsm_fullinv = dtrsm(inverse_blocks="full")
 potrf_fullinv = dpotrf(store_inverses="full")
+
+
+# -- user ops: the reference's device= callables (src/engine.py:144-149) ----------
+#
+# Two ways to run code of one's own on a task's staged operands:
+#
+#   * a NATIVE launcher (C ABI ``sfx_user_launch_fn`` in include/sfx.h, e.g.
+#     examples/user_daxpy.cu) registered once with ``register(name, fn)``; the
+#     executor thread calls it outside the runtime lock with the operands'
+#     device pointers and the task's stream -- no Python, no GIL on the path;
+#   * a PYTHON callable passed as ``device=`` exactly as in the reference:
+#     ``graph.task(Read(x), Write(y), device=lambda vx, vy: ...)``.  It runs on
+#     the device's executor thread with one ``DeviceView`` per access in
+#     declaration order; with torch imported its work is enqueued on the task's
+#     stream (``torch.cuda.ExternalStream``), so ``vy.array().add_(vx.array())``
+#     runs in the task's place in the dependency order.  This puts the GIL on the
+#     executor's path for those tasks only.
+#
+# A launcher returning non-zero (or a callable raising) fails the task: the
+# engine is poisoned and ``wait_all`` raises EngineFailedError whose
+# ``__cause__`` is the callable's exception (TaskFailedError for a native one),
+# as in the reference (engine.py:154-157, 227-243).
+
+import ctypes as _ct
+import itertools as _it
+import sys as _sys
+import threading as _th
+
+_DT = {N.DTYPE_F64: "float64", N.DTYPE_I64: "int64", N.DTYPE_BYTES: "uint8"}
+_DT_SIZE = {N.DTYPE_F64: 8, N.DTYPE_I64: 8, N.DTYPE_BYTES: 1}
+_registered = {}          # name -> (Op, keep-alive)
+_reg_lock = _th.Lock()
+_py_fns = {}              # key -> callable of a submitted, not yet executed task
+_py_results = {}          # key -> non-None return value
+_py_errors = []           # exceptions raised by callables (first failure wins)
+_py_keys = _it.count(1)
+_py_op = None
+
+
+class DeviceView:
+    """What a user op receives per access (reference src/device.py:119-133):
+    ``device`` (runtime device index), ``size`` (bytes), ``descriptor``
+    ((rows, cols, ld, dtype)), ``mode`` (access code), ``ptr`` (device address;
+    host address on the simulated backend), ``stream`` (cudaStream_t as int,
+    None on the simulated backend) and ``data`` (a writable memoryview of the
+    block on the simulated backend, None on a GPU)."""
+
+    __slots__ = ("device", "offset", "size", "descriptor", "data", "mode", "ptr", "stream")
+
+    def __init__(self, v, stream):
+        self.device = v.device
+        self.offset = 0
+        self.size = v.bytes
+        self.descriptor = (v.rows, v.cols, v.ld, _DT.get(v.dtype, "uint8"))
+        self.mode = v.mode
+        self.ptr = v.data or 0
+        self.stream = stream or None
+        self.data = None
+        if self.stream is None and self.ptr:
+            self.data = memoryview((_ct.c_char * self.size).from_address(self.ptr)).cast("B")
+
+    def __len__(self):
+        return self.size
+
+    @property
+    def __cuda_array_interface__(self):
+        if self.stream is None:
+            raise AttributeError("simulated-backend views are host memory (use .data / .array())")
+        rows, cols, ld, dt = self.descriptor
+        item = {"float64": 8, "int64": 8}.get(dt, 1)
+        return {"shape": (rows, cols), "typestr": {"float64": "<f8", "int64": "<i8"}.get(dt, "|u1"),
+                "data": (self.ptr, self.mode == N.READ), "strides": (ld * item, item), "version": 3,
+                "stream": None}  # the caller already runs on the task's stream
+
+    def array(self):
+        """The operand as a (rows, cols) array with row stride ld: a torch tensor
+        sharing the device block on a GPU, a numpy array over the host block on the
+        simulated backend."""
+        if self.stream is None:
+            import numpy as np
+            rows, cols, ld, dt = self.descriptor
+            item = np.dtype(dt).itemsize
+            return np.ndarray((rows, cols), dtype=dt, buffer=self.data, strides=(ld * item, item))
+        import torch
+        return torch.as_tensor(self, device="cuda")
+
+    def torch_stream(self):
+        import torch
+        return torch.cuda.ExternalStream(self.stream)
+
+
+def _call_python(views, n, stream, fparam, iparam, user):
+    key = iparam[0]
+    fn = _py_fns.pop(key, None)
+    try:
+        if fn is None:
+            raise RuntimeError(f"python device callable #{key} is not registered")
+        vs = [DeviceView(views[k], stream) for k in range(n)]
+        torch = _sys.modules.get("torch")
+        if stream and torch is not None:
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                r = fn(*vs)
+        else:
+            r = fn(*vs)
+        if r is not None:
+            _py_results[key] = r
+        return 0
+    except BaseException as e:  # noqa: BLE001 -- the engine is poisoned with it (engine.py:154-157)
+        _py_errors.append(e)
+        return 1
+
+
+def register(name: str, fn, fparam=(0.0, 0.0, 0.0, 0.0), iparam=(0, 0, 0, 0)) -> Op:
+    """Register a user op under ``name`` and return its Op (``op.params(...)`` makes
+    variants with other scalar parameters).  ``fn`` is a native launcher: a ctypes
+    function pointer (e.g. ``ctypes.CDLL(path).sfx_example_daxpy``) or its address
+    as an int; or a Python callable ``fn(*views) -> int`` with the launcher's
+    signature wrapped for you (views as DeviceView, returns 0 on success)."""
+    with _reg_lock:
+        if name in _registered:
+            raise ValueError(f"user op {name!r} is already registered")
+        keep = None
+        if isinstance(fn, int):
+            addr = fn
+        elif isinstance(fn, _ct._CFuncPtr) and not isinstance(fn, N.USER_LAUNCH):
+            addr = _ct.cast(fn, _ct.c_void_p).value
+            keep = fn
+        elif isinstance(fn, N.USER_LAUNCH):
+            addr, keep = _ct.cast(fn, _ct.c_void_p).value, fn
+        elif callable(fn):
+            def tramp(views, n, stream, fp, ip, user, _fn=fn):
+                try:
+                    return int(_fn(*[DeviceView(views[k], stream) for k in range(n)]) or 0)
+                except BaseException as e:  # noqa: BLE001
+                    _py_errors.append(e)
+                    return 1
+            keep = N.USER_LAUNCH(tramp)
+            addr = _ct.cast(keep, _ct.c_void_p).value
+        else:
+            raise TypeError(f"register: need a launcher or a callable, got {fn!r}")
+        code = _ct.c_uint32(0)
+        N.check(N.lib.sfx_register_op(name.encode(), addr, None, _ct.byref(code)))
+        op = Op(name, code.value, fparam, iparam)
+        _registered[name] = (op, keep)
+        return op
+
+
+def _params(self, fparam=None, iparam=None) -> Op:
+    return Op(self.name, self.code, self.fparam if fparam is None else fparam,
+              self.iparam if iparam is None else iparam)
+
+
+Op.params = _params
+
+
+def python_callable(fn) -> Op:
+    """The Op for one task whose body is the Python callable ``fn`` (graph.task
+    does this for ``device=<callable>``)."""
+    global _py_op
+    if _py_op is None:
+        with _reg_lock:
+            if _py_op is None:
+                keep = N.USER_LAUNCH(_call_python)
+                code = _ct.c_uint32(0)
+                N.check(N.lib.sfx_register_op(b"python_callable", _ct.cast(keep, _ct.c_void_p).value, None,
+                                              _ct.byref(code)))
+                _registered["python_callable"] = (Op("python_callable", code.value), keep)
+                _py_op = code.value
+    key = next(_py_keys)
+    _py_fns[key] = fn
+    return Op(getattr(fn, "__name__", "python_callable"), _py_op, iparam=(key,))
+
+
+def take_error():
+    """The first exception a user callable raised since the last call (or None)."""
+    if not _py_errors:
+        return None
+    e = _py_errors[0]
+    _py_errors.clear()
+    return e
+
+
+def result_of(op: Op):
+    """The non-None value a Python callable task returned (KeyError if none)."""
+    return _py_results.pop(op.iparam[0])
