@@ -517,7 +517,10 @@ class TaskGraph:
         text = msg.value.decode(errors="replace")
         cause = N.error_for(code.value, text)
         if code.value == N.ERR_USER:
-            cause = ops_mod.take_error() or cause  # the callable's own exception
+            user = ops_mod.take_error()  # the callable's own exception
+            if user is not None:
+                cause = user
+                text = f"{text}: {type(user).__name__}: {user}"
         agent = getattr(self.engine, "_comm_agent", None)
         if agent is not None and agent.error is not None:
             cause = agent.error  # a communication task failed (e.g. CommProtocolError)

@@ -219,7 +219,7 @@ class DeviceView:
         rows, cols, ld, dt = self.descriptor
         item = {"float64": 8, "int64": 8}.get(dt, 1)
         return {"shape": (rows, cols), "typestr": {"float64": "<f8", "int64": "<i8"}.get(dt, "|u1"),
-                "data": (self.ptr, self.mode == N.READ), "strides": (ld * item, item), "version": 3,
+                "data": (self.ptr, False), "strides": (ld * item, item), "version": 3,
                 "stream": None}  # the caller already runs on the task's stream
 
     def array(self):
