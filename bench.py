@@ -14,8 +14,9 @@ Workload by GPU count (``--workload auto``, the default):
           tiles over all N GPUs from ONE runtime (rank 0): 2-D block-cyclic
           owner-computes placement, panels pulled peer-to-peer over NVLink
           (strong scaling).  The same run also factors C3 on GPU 0 alone so
-          the line carries its own 1-GPU reference.  Fewer visible GPUs than
-          N is an error (no silent fallback to one GPU).
+          the line carries its own 1-GPU reference; at N >= 8 it adds the
+          north-star C5 leg (65536 / 1024 tiles on all N GPUs and on one).
+          Fewer visible GPUs than N is an error (no silent fallback to one GPU).
 
 Legs of the N = 1 JSON line:
   value         device-resident inputs, FP64 GFLOP/s (CUDA events, max over ranks)
@@ -772,6 +773,26 @@ def main_cholesky(args, dist):
         t1, _, _ = cholesky_run(sf, alg, [ordinals[0]], n, b, args.streams, args.chol_group, 4, False)
         one = {"n_gpus": 1, "value": flops / statistics.mean(t1[2:]) / 1e9, "unit": "GFLOP/s",
                "ms_per_step": 1e3 * statistics.mean(t1[2:])}
+    north = None
+    if ndev >= 8 and not args.no_secondary:
+        # the north-star configuration (BASELINE configs[4], C5): N = 65536 / 1024
+        # tiles over the same devices, with its own 1-GPU reference and residual
+        n5 = 65536
+        f5 = alg.flops_cholesky(n5)
+        t5, d5, r5 = cholesky_run(sf, alg, ordinals, n5, b, args.streams, args.chol_group, 3, not args.no_check)
+        t51, _, _ = cholesky_run(sf, alg, [ordinals[0]], n5, b, args.streams, args.chol_group, 2, False)
+        v5 = f5 / statistics.mean(t5[1:]) / 1e9
+        v51 = f5 / t51[-1] / 1e9
+        north = {"workload": f"tiled Cholesky {n5}x{n5} fp64, {b}x{b} tiles (BASELINE configs[4], C5), "
+                             f"{ndev} GPU(s) from one runtime",
+                 "value": v5, "unit": "GFLOP/s", "ms_per_step": 1e3 * statistics.mean(t5[1:]),
+                 "frac_aggregate_fp64_peak": v5 / 1e3 / (peak_tf * ndev),
+                 "one_gpu_value": v51, "speedup_vs_one_gpu": v5 / v51,
+                 "target": ">= 0.60 of aggregate FP64 peak and >= 6x over 1 GPU (BASELINE north_star)",
+                 "p2p_bytes_per_step": sum(d["bytes_p2p_in"] for d in d5),
+                 "rep_ms": [round(1e3 * x, 2) for x in t5],
+                 "check": None if r5 is None else {"cholesky_residual": r5, "tol": verify.CHOL_RESIDUAL_TOL,
+                                                   "pass": r5 <= verify.CHOL_RESIDUAL_TOL}}
     ntasks = nt + nt * (nt - 1) + nt * (nt - 1) * (nt - 2) // 6  # potrf + trsm + syrk + gemm
     p2p = sum(d["bytes_p2p_in"] for d in delta)
     tasks = sum(d["tasks_executed"] for d in delta)
@@ -794,6 +815,7 @@ def main_cholesky(args, dist):
                      "frac": value / 1e3 / ndev / peak_tf, "traffic": None,
                      "peak_source": "FP64 DMMA peak measured in-run (sfx_fp64_peak), per GPU"},
         "scaling_reference": one,
+        "north_star_C5": north,
         "p2p": {"bytes_per_step": p2p, "gbs": p2p / t / 1e9,
                 "per_gpu_bytes": [d["bytes_p2p_in"] for d in delta]},
         "runtime_host_us_per_task": {k: sum(d[k] for d in delta) / 1e3 / max(tasks, 1)
