@@ -161,7 +161,8 @@ def _emit(graph, fast):
 
 
 def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: bool = True,
-                priorities=False, tile_block: int = 0, skew: int = 0, skew_block: int = 0):
+                priorities=False, tile_block: int = 0, skew: int = 0, skew_block: int = 0,
+                prio_base: int = 0):
     """C += A B over tiles, loop order i, j, k.
 
     ``priorities`` (False, True or a row-block height h): block row i gets priority
@@ -184,6 +185,9 @@ def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: boo
     h x h blocks (block-row-major), each block's tasks one priority level above the
     next block's: a block needs only h rows of A and h columns of B, so when the
     operands start on the host, staging spreads over the whole step.
+
+    ``prio_base`` is added to every task's priority (a stream of products
+    inserted back to back: each later product strictly below the earlier ones).
     """
     nt = A.nt
     if skew:
@@ -211,7 +215,7 @@ def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: boo
         for i in range(nt):
             for j in range(nt):
                 for k in range(nt):
-                    prio = -(k + off(i, j)) if skew else rank(i, j)
+                    prio = (-(k + off(i, j)) if skew else rank(i, j)) + prio_base
                     graph.task(read(A[i, k]), read(B[k, j]), write(C[i, j]), device=ops.gemm_nn,
                                priority=prio, name="gemm")
         return None
@@ -228,6 +232,8 @@ def insert_gemm(graph, A: TiledMatrix, B: TiledMatrix, C: TiledMatrix, fast: boo
             prio = -(kk + np.array([off(i, j) for j in range(nt)], np.int64)[jj]).astype(np.int32)
         else:
             prio = np.repeat(np.array([rank(i, j) for j in range(nt)], np.int32), nt)  # jj-major like hids
+        if prio_base:
+            prio = prio + np.int32(prio_base)
         batch.add_many(ops.gemm_nn, hids, modes, prio, "gemm")
         batch.flush()
     return batch.submit()
