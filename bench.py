@@ -112,7 +112,11 @@ class Dist:
 
             if backend == "nccl":
                 torch.cuda.set_device(self.local)
-            dist.init_process_group(backend)
+            import datetime
+
+            # ranks > 0 of the multi-GPU Cholesky line wait in a barrier while rank 0
+            # drives every GPU (C3, its 1-GPU reference and at N >= 8 the C5 leg)
+            dist.init_process_group(backend, timeout=datetime.timedelta(minutes=30))
             self.pg = dist
 
     def barrier(self):
