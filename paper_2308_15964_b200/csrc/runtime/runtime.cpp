@@ -1400,6 +1400,8 @@ bool Runtime::groupable(const Task* t) const {
     case SFX_OP_P2P_PAIR:  // grouped mutual P2P kernel; commutative guards in shared mode
     case SFX_OP_P2P_SELF:
       return group_max_ > 1 && !deterministic_;  // deterministic: one-sided kernel per task
+    case SFX_OP_NOOP:  // no device work: ready empty tasks share one end event (one record per group)
+      return group_max_ > 1;
     default:
       return false;
   }

@@ -346,7 +346,7 @@ def test_insertion_errors_match_reference():
         with pytest.raises(sf.ConfigurationError, match="oracle"):
             g.task(sf.write(c), host=lambda x: None)
         with pytest.raises(sf.ConfigurationError):
-            g.task(sf.write(c), device=lambda v: None)
+            g.task(sf.write(c), device=42)  # neither an op nor a callable (callables are user ops)
         with pytest.raises(sf.ConfigurationError):
             g.task(sf.write(c))
         with pytest.raises(sf.ConfigurationError):
