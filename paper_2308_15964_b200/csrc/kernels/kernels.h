@@ -113,6 +113,7 @@ cudaError_t launch_fill_spd(double* a, long long rows, long long cols, long long
 cudaError_t launch_fill_particles(double* p, long long n, long long ld, long long seed, long long first,
                                   cudaStream_t s);
 cudaError_t launch_spin(long long ns, cudaStream_t s);
+cudaError_t launch_spin_group(int n, long long ns, cudaStream_t s);
 // failure injection (SFX_OP_FAULT): 0 = invalid launch configuration, 1 = device trap
 cudaError_t launch_fault(int kind, cudaStream_t s);
 // A += sum of n addends (FP64 rows x cols, each with its own ld), n <= 7

@@ -249,6 +249,14 @@ cudaError_t launch_spin(long long ns, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// n same-duration spin tasks of one launch group: one CTA each, all concurrent
+// (the overhead protocol's bodies of n ready chains in one launch)
+cudaError_t launch_spin_group(int n, long long ns, cudaStream_t s) {
+  count_launch();
+  spin_kernel<<<n, 32, 0, s>>>(ns);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_cell(long long* target, const long long* const* reads, int nreads, long long kind, long long a,
                         long long b, cudaStream_t s) {
   CellArgs c;

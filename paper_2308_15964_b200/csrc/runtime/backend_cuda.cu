@@ -505,6 +505,10 @@ class CudaBackend : public Backend {
       cudaError_t e = launch_p2p_group(pd.data(), static_cast<int>(pd.size()), self, f.fp[0], devs_[d]->streams[stream]);
       return cuda_err(e, "grouped p2p launch", err);
     }
+    if (ops.size() > 1 && f.op == SFX_OP_SPIN) {  // members share ip[0] (same_signature)
+      cudaError_t e = launch_spin_group(static_cast<int>(ops.size()), f.ip[0], devs_[d]->streams[stream]);
+      return cuda_err(e, "grouped spin launch", err);
+    }
     if (ops.size() > 1 && f.op == SFX_OP_DTRSM && f.ip[0] == 2) {
       // grouped full-inverse TRSMs: X_i = B_i W_i^T for every member in ONE TRI-masked
       // DGEMM launch (beta = 0, no split-K: no scratch memset, no atomics), then

@@ -1402,6 +1402,8 @@ bool Runtime::groupable(const Task* t) const {
       return group_max_ > 1 && !deterministic_;  // deterministic: one-sided kernel per task
     case SFX_OP_NOOP:  // no device work: ready empty tasks share one end event (one record per group)
       return group_max_ > 1;
+    case SFX_OP_SPIN:  // same-duration spins: one CTA per member in one launch, all concurrent
+      return group_max_ > 1 && !be_->is_sim();  // (the simulated backend would run them one by one)
     default:
       return false;
   }
@@ -1409,7 +1411,8 @@ bool Runtime::groupable(const Task* t) const {
 
 bool Runtime::same_signature(const Task* a, const Task* b) const {
   if (a->op != b->op || a->acc.size() != b->acc.size()) return false;
-  const bool ip_matters = a->op == SFX_OP_DGEMM || a->op == SFX_OP_DTRSM || a->op == SFX_OP_DPOTRF;
+  const bool ip_matters =
+      a->op == SFX_OP_DGEMM || a->op == SFX_OP_DTRSM || a->op == SFX_OP_DPOTRF || a->op == SFX_OP_SPIN;
   for (int k = 0; k < 4; ++k)
     if (a->fp[k] != b->fp[k] || (ip_matters && a->ip[k] != b->ip[k])) return false;
   for (size_t k = 0; k < a->acc.size(); ++k) {
