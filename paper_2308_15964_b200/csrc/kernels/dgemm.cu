@@ -56,13 +56,16 @@ constexpr int CONSUMER_WARPS = 8;
 // one producer warpgroup (4 warps, one elected TMA lane) + two DMMA warpgroups;
 // setmaxnreg moves registers from the producer to the consumers (40 / 232).
 constexpr int THREADS = (CONSUMER_WARPS + 4) * 32;
+// TRI (full-inverse TRSM): the producer warpgroup's three spare warps mask each
+// B stage that crosses the diagonal in shared memory (see the kernel)
+constexpr int MASK_WARPS = 3;
 constexpr int A_STAGE = BM * BK * 8;  // 16 KiB
 constexpr int B_STAGE = BN * BK * 8;  // 16 KiB
 // C prefetch buffer: the producer TMA-loads the next epilogue's C tile (8 boxes
 // of 16 x 128 doubles, 128B swizzle) while the consumers are still in the
 // mainloop, so the epilogue reads C from shared memory instead of waiting on HBM
 constexpr int C_BUF = SFX_GEMM_CBUF ? BM * BN * 8 : 0;  // 128 KiB
-constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + C_BUF + 2 * STAGES * 8 + 24 + 1024;
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + C_BUF + 3 * STAGES * 8 + 24 + 1024;
 static_assert(SMEM_BYTES <= 232448, "dynamic shared memory per CTA");
 
 // One launch covers G independent tile tasks of identical shape (grouped
@@ -110,6 +113,7 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
   uint64_t* cfull = empty + STAGES;
   uint64_t* cempty = cfull + 1;
   uint64_t* stagger = cempty + 1;  // warpgroup 1 starts one k-step behind warpgroup 0
+  uint64_t* mfull = stagger + 1;   // TRI: stage s masked by the producer warpgroup's spare warps
 
   // TRI split: per row of output tiles, column tile bn spans (bn+1) K-units of
   // BN/BK k-steps; it is cut into items of U = tri_split units (the last one
@@ -202,6 +206,8 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
     ptx::mbar_init(cfull, 1);
     ptx::mbar_init(cempty, p.cstore ? CONSUMER_WARPS : CONSUMER_WARPS * 32);
     ptx::mbar_init(stagger, CONSUMER_WARPS / 2);
+    if (TRI)
+      for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&mfull[s], MASK_WARPS);
     ptx::fence_mbar_init();
   }
   __syncthreads();
@@ -256,6 +262,42 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
         }
         if (want_c && kc == kt1) load_c();
       }
+    } else if (TRI && warp > CONSUMER_WARPS) {
+      // ---- TRI operand masking (full-inverse TRSM) ----
+      // B is the POTRF tile carrying W = inv(L)^T in its strict upper triangle and
+      // L below it.  The product needs W: on the k-steps that cross the diagonal,
+      // entries with k > n become 0 and the diagonal L_nn becomes 1 / L_nn.  The
+      // spare producer warps rewrite those entries of the landed stage in shared
+      // memory (same 128B-swizzled box layout the consumers read) and release it
+      // on mfull[s]; the consumers' operand path has no mask code (round 2: the
+      // in-register mask cost the TRI kernel 544 B of spills and a reciprocal in
+      // the DMMA loop).
+      const int mt = (warp - CONSUMER_WARPS - 1) * 32 + lane;
+      int it = 0;
+      for (int lin = blockIdx.x; lin < total; lin += gridDim.x) {
+        int task, m0, n0, kt0, kt1;
+        coords(lin, task, m0, n0, kt0, kt1);
+        for (int kt = kt0; kt < kt1; ++kt, ++it) {
+          const int s = it % STAGES;
+          ptx::mbar_wait(&full[s], (it / STAGES) & 1);
+          const int j = kt * BK - n0;  // tile-relative k of the stage's first row
+          if (j + BK > 0) {            // rows k = j + kk >= n exist for columns n < j + BK
+            double* bst = reinterpret_cast<double*>(sB + s * B_STAGE);
+            const int ncols = min(BN, j + BK);
+            for (int e = mt; e < ncols * BK; e += MASK_WARPS * 32) {
+              const int n = e >> 4, kk = e & (BK - 1);
+              const int k = j + kk;
+              if (k < n) continue;
+              const int nn = n & 15;
+              double* ptr = bst + (((n >> 4) * 2048 + kk * 128 + (((nn >> 1) ^ (kk & 7)) << 4)) >> 3) + (nn & 1);
+              *ptr = k == n ? __drcp_rn(*ptr) : 0.0;
+            }
+            ptx::fence_proxy_async();  // generic writes before the stage's next TMA refill
+          }
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&mfull[s]);
+        }
+      }
     }
     return;
   }
@@ -304,7 +346,7 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
       // so each epilogue runs beside the other warpgroup's mainloop.
       if (it == p.stagger && wm == 0 && lane == 0 && p.stagger) ptx::mbar_arrive(stagger);
       if (it == 0 && wm == 1 && p.stagger) ptx::mbar_wait(stagger, 0);
-      ptx::mbar_wait(&full[s], (it / STAGES) & 1);
+      ptx::mbar_wait(TRI ? &mfull[s] : &full[s], (it / STAGES) & 1);  // TRI: landed AND masked
       release_c();
       if (TRI && kt * BK >= n0 + wn * 32 + 32) {
         // TRI: every B operand of this warp's columns is below the diagonal in
@@ -346,16 +388,9 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int k = 4 * t + 2 * h + e;
-              double v = ptx::lds64(bS + q * 2048 + k * 128 + (((nn >> 1) ^ (k & 7)) << 4) + (nn & 1) * 8);
+              const double v = ptx::lds64(bS + q * 2048 + k * 128 + (((nn >> 1) ^ (k & 7)) << 4) + (nn & 1) * 8);
               if (h == 1) dep |= static_cast<uint32_t>(__double2hiint(v));
-              if (TRI && kt * BK + BK > n0 + wn * 32) {  // only k-steps reaching this warp's columns
-                const int kg = kt * BK + k, ng = n0 + n;
-                // selects, no divergent branch: the diagonal gets 1 / L_nn (IEEE
-                // reciprocal, no division slow path), below it exact zeros
-                const double rv = __drcp_rn(v);
-                v = kg > ng ? 0.0 : (kg == ng ? rv : v);
-              }
-              b[j][e] = v;
+              b[j][e] = v;  // TRI: already masked in shared memory
             }
           }
         } else {
@@ -375,16 +410,8 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_dmma_kernel(const __grid_con
               const int nn = n & 15;
               const double2 v = ptx::lds128(bS + (n >> 4) * 2048 + k * 128 + (((nn >> 1) ^ (k & 7)) << 4));
               if (h == 1) dep |= static_cast<uint32_t>(__double2hiint(v.x));
-              double b0 = v.x, b1 = v.y;
-              if (TRI) {  // masked only on the k-steps that cross the diagonal
-                const int kg = kt * BK + k, ng = n0 + n;
-                if (kt * BK + BK > n0 + wn * 32) {
-                  b0 = kg > ng ? 0.0 : (kg == ng ? __drcp_rn(b0) : b0);
-                  b1 = kg > ng + 1 ? 0.0 : (kg == ng + 1 ? __drcp_rn(b1) : b1);
-                }
-              }
-              b[2 * jp][e] = b0;
-              b[2 * jp + 1][e] = b1;
+              b[2 * jp][e] = v.x;  // TRI: already masked in shared memory
+              b[2 * jp + 1][e] = v.y;
             }
           }
         }
