@@ -710,10 +710,17 @@ def main_gemm(args, dist):
         print(json.dumps(line), flush=True)
 
 
-def cholesky_run(sf, alg, ordinals, n, b, streams, group, reps, check, clocks=None):
+def cholesky_run(sf, alg, ordinals, n, b, streams, group, reps, check, clocks=None, timed_from=None,
+                 e2e_reps=0):
     """Factor C3-style SPD matrices ``reps`` times on the given devices from one
-    runtime (block-cyclic when several); returns per-rep seconds, stats and the
-    residual of the last rep."""
+    runtime (block-cyclic when several); returns per-rep seconds, the runtime
+    counters summed over reps ``timed_from`` .. reps-1 (default: the last rep) and
+    the residual of the last rep.  ``e2e_reps`` > 0 adds an end-to-end leg
+    (returned as a 4th value): the SPD input starts on the HOST (flushed there,
+    device copies dropped), each timed rep stages it on demand, factors and
+    flushes L back to the host."""
+    if timed_from is None:
+        timed_from = reps - 1
     import torch
 
     ndev = len(ordinals)
@@ -747,7 +754,7 @@ def cholesky_run(sf, alg, ordinals, n, b, streams, group, reps, check, clocks=No
                 torch.cuda.synchronize(o)
             if rep == 1 and clocks is not None:
                 clocks.start()
-            if rep == reps - 1:
+            if rep == timed_from:
                 s_before = [eng.stats(d) for d in range(ndev)]
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -759,14 +766,42 @@ def cholesky_run(sf, alg, ordinals, n, b, streams, group, reps, check, clocks=No
             times.append(e0.elapsed_time(e1) / 1e3)
         stats = [eng.stats(d) for d in range(ndev)]
         delta = [{k: s1[k] - s0[k] for k in ("bytes_p2p_in", "copies_p2p_in", "tasks_executed", "t_plan_ns",
-                                             "t_issue_ns", "t_complete_ns", "groups")}
+                                             "t_issue_ns", "t_complete_ns", "groups", "kernel_launches")}
                  for s0, s1 in zip(s_before, stats)]
         if check:
             g.flush_all(keep_device=False)
             g.wait_all()
             res = verify.cholesky_residual(A, M.tiles, n, b)
+        e2e = None
+        if e2e_reps:
+            et = []
+            h2d = d2h = 0
+            for r in range(e2e_reps + 1):  # the first rep is a warm-up
+                alg.insert_fill_spd(g, M, 3)
+                g.flush_all(keep_device=False)  # the input now lives on the host only
+                g.wait_all()
+                for o in set(ordinals):
+                    torch.cuda.synchronize(o)
+                e_before = [eng.stats(d) for d in range(ndev)]
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                alg.insert_cholesky(g, M)       # stages every tile host -> device on demand
+                g.flush_all(keep_device=False)  # L back to the host
+                g.wait_all()
+                e1.record()
+                torch.cuda.synchronize()
+                e_after = [eng.stats(d) for d in range(ndev)]
+                if r >= 1:  # bytes of the timed region only (the fill and input flush are outside)
+                    et.append(e0.elapsed_time(e1) / 1e3)
+                    h2d += sum(a["bytes_to_device"] - z["bytes_to_device"] for z, a in zip(e_before, e_after))
+                    d2h += sum(a["bytes_from_device"] - z["bytes_from_device"] for z, a in zip(e_before, e_after))
+            e2e = {"seconds": statistics.mean(et), "h2d_bytes_per_step": h2d // e2e_reps,
+                   "d2h_bytes_per_step": d2h // e2e_reps}
     finally:
         eng.stop()
+    if e2e_reps:
+        return times, delta, res, e2e
     return times, delta, res
 
 
@@ -798,8 +833,9 @@ def main_cholesky(args, dist):
     peak_tf, _ = sf.fp64_peak(ordinals[0])
     flops = alg.flops_cholesky(n)
     clocks = ClockSampler(ordinals)
-    times, delta, res = cholesky_run(sf, alg, ordinals, n, b, args.streams, args.chol_group,
-                                     args.warmup + args.steps, not args.no_check, clocks)
+    times, delta, res, ce2e = cholesky_run(sf, alg, ordinals, n, b, args.streams, args.chol_group,
+                                           args.warmup + args.steps, not args.no_check, clocks,
+                                           timed_from=args.warmup, e2e_reps=2)
     clk = clocks.stop()
     t = statistics.mean(times[args.warmup:])
     value = flops / t / 1e9
@@ -830,8 +866,9 @@ def main_cholesky(args, dist):
                  "check": None if r5 is None else {"cholesky_residual": r5, "tol": verify.CHOL_RESIDUAL_TOL,
                                                    "pass": r5 <= verify.CHOL_RESIDUAL_TOL}}
     ntasks = nt + nt * (nt - 1) + nt * (nt - 1) * (nt - 2) // 6  # potrf + trsm + syrk + gemm
-    p2p = sum(d["bytes_p2p_in"] for d in delta)
+    p2p = sum(d["bytes_p2p_in"] for d in delta) / args.steps  # delta covers the timed reps
     tasks = sum(d["tasks_executed"] for d in delta)
+    launches = sum(d["kernel_launches"] for d in delta)
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ndev, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
@@ -852,12 +889,17 @@ def main_cholesky(args, dist):
                      "peak_source": "FP64 DMMA peak measured in-run (sfx_fp64_peak), per GPU"},
         "scaling_reference": one,
         "north_star_C5": north,
+        "e2e": {"value": flops / ce2e["seconds"] / 1e9, "unit": "GFLOP/s",
+                "h2d_bytes_per_step": ce2e["h2d_bytes_per_step"], "d2h_bytes_per_step": ce2e["d2h_bytes_per_step"],
+                "ms_per_step": 1e3 * ce2e["seconds"],
+                "how": "SPD input on the host (pinned tiles, device copies dropped); each step stages it on "
+                       "demand, factors on all GPUs and flushes L back (flush_all), 2 steps after 1 warm-up"},
         "p2p": {"bytes_per_step": p2p, "gbs": p2p / t / 1e9,
-                "per_gpu_bytes": [d["bytes_p2p_in"] for d in delta]},
+                "per_gpu_bytes": [d["bytes_p2p_in"] // args.steps for d in delta]},
         "runtime_host_us_per_task": {k: sum(d[k] for d in delta) / 1e3 / max(tasks, 1)
                                      for k in ("t_plan_ns", "t_issue_ns", "t_complete_ns")},
         "rep_ms": [round(1e3 * x, 2) for x in times],
-        "gpu_launches": None,
+        "gpu_launches": launches,  # this process's kernels over the timed factorizations, all GPUs
     }
     print(json.dumps(line), flush=True)
     dist.barrier()
@@ -1030,7 +1072,7 @@ def main_particles(args, dist):
         "roofline": {"bound": "fp64 pipe", "achieved": inter / t, "peak": bound, "unit": "interactions/s",
                      "frac": inter / t / bound, "dfma_peak_tflops_per_gpu": dfma_tf},
         "p2p_bytes": sum(s["bytes_p2p_in"] for s in stats),
-        "gpu_launches": stats[0]["kernel_launches"],
+        "gpu_launches": sum(s["kernel_launches"] for s in stats),
     }
     print(json.dumps(line), flush=True)
     dist.barrier()
