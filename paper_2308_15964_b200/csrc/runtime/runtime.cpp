@@ -1455,6 +1455,12 @@ bool Runtime::acquire_commute(Task* t) {
   return true;
 }
 
+static bool exclusive_guards(const Task* t) {
+  for (size_t k = 0; k < t->commute.size(); ++k)
+    if (t->commute_sh[k]) return false;
+  return true;
+}
+
 static bool shared_on(const Task* t, const Handle* h) {
   for (size_t k = 0; k < t->commute.size(); ++k)
     if (t->commute[k] == h) return t->commute_sh[k] != 0;
@@ -1974,6 +1980,16 @@ void Runtime::exec_loop(int d) {
       continue;
     }
     const int64_t t_rel0 = now_ns();
+    if (!be_->is_sim() && ndev_ == 1)
+      // Exclusive commutative guards pass at LAUNCH on one device, like every other
+      // dependency: the next member's plan waits on commute_last (this task's end
+      // event, set in plan), so members still never overlap on the device, but the
+      // next one is issued without a host round trip through the completion thread
+      // (the reference holds the guard until the body returns, handles.py:249-270;
+      // with several devices the guard stays held to completion: a member placed
+      // elsewhere would pull the handle's data while this one may still run)
+      for (Task* t : group)
+        if (t->guards_held && t->op != SFX_OP_EXTERN && exclusive_guards(t)) release_commute(t);
     if (be_->is_sim()) {
       for (Task* t : group) {
         if (t->op == SFX_OP_EXTERN) {
