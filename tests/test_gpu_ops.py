@@ -424,3 +424,31 @@ def test_million_task_soak_on_the_gpu_has_flat_runtime_memory():
         assert rss[-1] - rss[5] < 64 << 20, (rss[5], rss[-1])
     finally:
         eng.stop()
+
+
+def test_commutative_gemm_accumulation_with_guards_passed_at_launch():
+    """C += A_k B_k as 48 commutative_write DGEMMs over 8 streams, mixed with a few
+    exclusive writes that scale C: exclusive commutative guards pass at launch on
+    one device (the next member waits on the holder's end event), so members must
+    still never overlap -- overlapping read-modify-write epilogues would lose
+    updates.  The sum equals the serial result up to the order of additions."""
+    rng = np.random.default_rng(21)
+    b = 256
+    A = [rng.standard_normal((b, b)) for _ in range(6)]
+    B = [rng.standard_normal((b, b)) for _ in range(6)]
+    C = np.zeros((b, b))
+    want = np.zeros((b, b))
+    eng = sf.create_engine(sf.WorkerTeam.of_devices(1, 8))
+    try:
+        g = sf.TaskGraph().compute_on(eng)
+        for rnd in range(4):
+            for k in range(12):
+                g.task(sf.read(A[k % 6]), sf.read(B[k % 6]), sf.commutative_write(C), device=sf.ops.gemm_nn)
+                want += A[k % 6] @ B[k % 6]
+            g.task(sf.read(A[0]), sf.read(B[0]), sf.write(C), device=sf.ops.dgemm(0.0, 0.5))  # C = 0.5 C
+            want *= 0.5
+        g.flush_to_host(C)
+        assert g.wait_all(timeout=120)
+    finally:
+        eng.stop()
+    assert np.max(np.abs(C - want)) / np.max(np.abs(want)) < 1e-12
