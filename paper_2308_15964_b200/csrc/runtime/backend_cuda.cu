@@ -105,7 +105,7 @@ class CudaBackend : public Backend {
       size_t fr = 0, tot = 0;
       e = cudaMemGetInfo(&fr, &tot);
       if (e) return cuda_err(e, "cudaMemGetInfo", err);
-      const uint64_t reserve = 6ull << 30;
+      const uint64_t reserve = 10ull << 30;  // incl. the scratch pool backed below
       bytes = fr > 2 * reserve ? fr - reserve : fr / 2;
     }
     bytes = (bytes + 255) / 256 * 256;
@@ -118,11 +118,17 @@ class CudaBackend : public Backend {
       if (cudaDeviceGetDefaultMemPool(&pool, D.ordinal) == cudaSuccess) {
         uint64_t keep = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        // and back it with 2 GiB now: the first factorization's grouped TRSMs
-        // otherwise grow the pool from the driver on the executor's path (the
-        // first C3 factorization of a run took 385-815 ms instead of 366)
+        // and back it now: the grouped TRSMs' per-stream scratch otherwise grows
+        // the pool from the driver on the executor's path (the first C3
+        // factorization of a run took 385-815 ms instead of 366).  6 GiB: every
+        // stream of a device can hold a launch group of b = 1024 tiles (~42
+        // streams x 64 MiB); with 2 GiB, streams that met their first big TRSM
+        // group late still grew the pool mid-run (C3 reps of 390-580 ms among
+        // 356 ms ones, tools/r4k_var.sh).  The pool is per physical GPU, so
+        // logical devices sharing one reuse the same backing.
         void* warm = nullptr;
-        if (cudaMallocAsync(&warm, size_t(2) << 30, 0) == cudaSuccess) {
+        if (cudaMallocAsync(&warm, size_t(6) << 30, 0) == cudaSuccess ||
+            (cudaGetLastError(), cudaMallocAsync(&warm, size_t(2) << 30, 0) == cudaSuccess)) {
           cudaFreeAsync(warm, 0);
           cudaStreamSynchronize(0);
         }
