@@ -29,7 +29,11 @@ _lib = None
 def example_lib():
     global _lib
     if _lib is None:
-        _lib = ctypes.CDLL(os.path.join(PKG, "libsfx_user_daxpy.so"))
+        path = os.path.join(PKG, "libsfx_user_daxpy.so")
+        if not os.path.exists(path):  # built by __graft_entry__.build(); build it if a checkout lacks it
+            from paper_2308_15964_b200 import build as B
+            B._build_examples(B._nvcc(), False, False)
+        _lib = ctypes.CDLL(path)
     return _lib
 
 
