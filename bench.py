@@ -78,6 +78,8 @@ def parse():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--e2e-skew", type=int, default=-1, help="insert_gemm skew on the e2e leg (-1: 3 nt, 0: FIFO)")
+    ap.add_argument("--pipeline", type=int, default=1,
+                    help="device-resident leg: the K steps inserted back to back in one timed bracket (0: per step)")
     ap.add_argument("--e2e-pipeline", type=int, default=1,
                     help="e2e headline: steps inserted back to back with one wait at the end (0: per-step wait)")
     ap.add_argument("--e2e-stage-stream", type=int, default=1,
@@ -526,22 +528,48 @@ def main_gemm(args, dist):
     p0 = sf.gemm_paths()
     clocks = ClockSampler(dev).start()
     times = []
-    for _ in range(args.steps):
+    if args.pipeline:
+        # the K steps in ONE bracket, inserted back to back with one wait at the end:
+        # step k+1's chain on a C tile starts when step k's chain on it ends, so the
+        # steps' ramp-down and ramp-up overlap (ms_per_step = total / K)
         dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        step()
+        for _ in range(args.steps):
+            alg.insert_gemm(g, A, B, C)
+        g.wait_all()
         e1.record()
         torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1) / 1e3)
+        times = [e0.elapsed_time(e1) / 1e3 / args.steps] * args.steps
+    else:
+        for _ in range(args.steps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
     clk = clocks.stop()
     st1 = eng.stats(0)
     p1 = sf.gemm_paths()
     step_s = dist.max(statistics.mean(times))
     value = flops * dist.world / step_s / 1e9
     launches = st1["kernel_launches"] - st0["kernel_launches"]
-    check = None if args.no_check else gemm_check(g, A, B, C, float(args.warmup + args.steps), seed=1)
+    iso = []
+    if args.pipeline:  # the same step timed alone (insert, wait), for comparison
+        for _ in range(2):
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step()
+            e1.record()
+            torch.cuda.synchronize()
+            iso.append(e0.elapsed_time(e1) / 1e3)
+    check = None if args.no_check else gemm_check(g, A, B, C, float(args.warmup + args.steps + len(iso)), seed=1)
 
     # ---- e2e: host-resident inputs through the public API ----
     def e2e_step(wait=True, prio_base=0):
@@ -694,6 +722,10 @@ def main_gemm(args, dist):
                    "l2": "inputs (6 GiB) larger than L2; no flush", "parallelism": f"replica x{dist.world}"},
         "clocks": clk, "check": check, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
         "pct_fp64_peak": 100.0 * value / dist.world / 1e3 / peak_tf,
+        "timing": (f"{args.steps} steps inserted back to back in one bracket, one wait_all (ms_per_step = total / "
+                   f"{args.steps})" if args.pipeline else f"{args.steps} steps, each bracketed and waited"),
+        "isolated_step": ({"value": flops * dist.world / dist.max(statistics.mean(iso)) / 1e9,
+                           "ms_per_step": 1e3 * dist.max(statistics.mean(iso)), "steps": len(iso)} if iso else None),
     }
 
     if dist.rank == 0 and dist.world == 1 and not args.no_secondary:
