@@ -662,7 +662,7 @@ def main_gemm(args, dist):
         # the host now holds C = (warmup + steps + 1 + ke) A B (every e2e pass accumulates)
         samples = verify.sample_tiles(nt, 3, seed=2)
         rel, comp = verify.gemm_tile_errors(C.tiles, A.tiles, B.tiles, samples,
-                                            mult=float(args.warmup + args.steps + 1 + ke + kp))
+                                            mult=float(args.warmup + args.steps + len(iso) + 1 + ke + kp))
         e2e["check"] = {"tiles_checked": len(samples), "max_rel_err": rel, "max_componentwise_err": comp,
                         "pass": rel <= verify.GEMM_REL_TOL and comp <= verify.GEMM_COMPONENTWISE_TOL}
     eng.stop()
