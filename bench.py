@@ -722,6 +722,10 @@ def main_gemm(args, dist):
                    "l2": "inputs (6 GiB) larger than L2; no flush", "parallelism": f"replica x{dist.world}"},
         "clocks": clk, "check": check, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
         "pct_fp64_peak": 100.0 * value / dist.world / 1e3 / peak_tf,
+        "runtime_host_us_per_task": {k: (st1[k] - st0[k]) / 1e3 / max(1, st1["tasks_executed"] - st0["tasks_executed"])
+                                     for k in ("t_plan_ns", "t_issue_ns", "t_release_ns", "t_complete_ns")}
+        | {"stream_waits_per_task": (st1["stream_waits"] - st0["stream_waits"]) /
+           max(1, st1["tasks_executed"] - st0["tasks_executed"]), "host_cores": os.cpu_count()},
         "timing": (f"{args.steps} steps inserted back to back in one bracket, one wait_all (ms_per_step = total / "
                    f"{args.steps})" if args.pipeline else f"{args.steps} steps, each bracketed and waited"),
         "isolated_step": ({"value": flops * dist.world / dist.max(statistics.mean(iso)) / 1e9,
