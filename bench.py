@@ -41,7 +41,6 @@ Legs of the N = 1 JSON line:
 from __future__ import annotations
 
 import argparse
-import gc
 import json
 import os
 import statistics
@@ -525,6 +524,17 @@ def main_gemm(args, dist):
 
     for _ in range(args.warmup):
         step()
+    iso = []
+    if args.pipeline:  # the same step timed alone (insert, wait) after the warm-up, for comparison
+        for _ in range(2):
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step()
+            e1.record()
+            torch.cuda.synchronize()
+            iso.append(e0.elapsed_time(e1) / 1e3)
     st0 = eng.stats(0)
     p0 = sf.gemm_paths()
     clocks = ClockSampler(dev).start()
@@ -559,18 +569,6 @@ def main_gemm(args, dist):
     step_s = dist.max(statistics.mean(times))
     value = flops * dist.world / step_s / 1e9
     launches = st1["kernel_launches"] - st0["kernel_launches"]
-    iso = []
-    if args.pipeline:  # the same step timed alone (insert, wait), for comparison
-        gc.collect()  # (untimed) the burst of K steps' Python objects, not inside a timed step
-        for _ in range(2):
-            dist.barrier()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            step()
-            e1.record()
-            torch.cuda.synchronize()
-            iso.append(e0.elapsed_time(e1) / 1e3)
     check = None if args.no_check else gemm_check(g, A, B, C, float(args.warmup + args.steps + len(iso)), seed=1)
 
     # ---- e2e: host-resident inputs through the public API ----
