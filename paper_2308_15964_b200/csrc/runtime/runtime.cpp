@@ -696,7 +696,7 @@ int Runtime::submit_bound(uint32_t n, const sfx_task_desc* descs, const sfx_acce
     }
     Graph* g = graphs_[d.graph].get();
     g->inserted += 1;
-    tasks_by_tid_[t->tid] = t;
+    tasks_by_tid_.put(t->tid, t);
     if (--t->pending == 0) {  // drop the insertion guard (graph.py:161-163)
       t->state = SFX_STATE_READY;
       push_ready(t, -1);
@@ -1619,12 +1619,11 @@ int Runtime::extern_poll(uint64_t* tids, uint64_t cap, uint64_t* n, double timeo
 int Runtime::extern_done(uint64_t tid, int status, const char* msg) {
   std::unique_lock<std::mutex> lk(mu_);
   drain_locked();
-  auto it = tasks_by_tid_.find(tid);
-  if (it == tasks_by_tid_.end() || it->second->op != SFX_OP_EXTERN || !it->second->detached) {
+  Task* t = tasks_by_tid_.get(tid);
+  if (!t || t->op != SFX_OP_EXTERN || !t->detached) {
     last_error = "extern_done: not an external task handed out by sfx_extern_poll";
     return SFX_ERR_CONFIG;
   }
-  Task* t = it->second;
   if (status != 0) {
     poison(SFX_ERR_ENGINE_FAILED, msg ? msg : "external task failed");
     return SFX_OK;
@@ -2141,13 +2140,12 @@ int Runtime::wait_all(uint32_t gid, double timeout_s) {
 int Runtime::wait_task(uint64_t tid, double timeout_s) {
   std::unique_lock<std::mutex> lk(mu_);
   drain_locked();
-  auto it = tasks_by_tid_.find(tid);
-  if (it == tasks_by_tid_.end()) {
+  Task* t = tasks_by_tid_.get(tid);
+  if (!t) {
     if (tid && tid <= max_tid_ && retired_tasks_) return SFX_OK;  // retired: it finished
     last_error = "unknown task";
     return SFX_ERR_CONFIG;
   }
-  Task* t = it->second;
   auto done = [&] { return t->state == SFX_STATE_FINISHED || fail_code_ != 0; };
   if (timeout_s < 0)
     done_cv_.wait(lk, done);
@@ -2164,8 +2162,8 @@ int Runtime::wait_task(uint64_t tid, double timeout_s) {
 int Runtime::task_state(uint64_t tid, int32_t* st) {
   std::unique_lock<std::mutex> lk(mu_);
   drain_locked();
-  auto it = tasks_by_tid_.find(tid);
-  if (it == tasks_by_tid_.end()) {
+  Task* found = tasks_by_tid_.get(tid);
+  if (!found) {
     if (tid && tid <= max_tid_ && retired_tasks_) {  // retired by a history-free graph: it finished
       *st = SFX_STATE_FINISHED;
       return SFX_OK;
@@ -2173,7 +2171,7 @@ int Runtime::task_state(uint64_t tid, int32_t* st) {
     last_error = "unknown task";
     return SFX_ERR_CONFIG;
   }
-  *st = it->second->state;
+  *st = found->state;
   return SFX_OK;
 }
 

@@ -199,6 +199,41 @@ int register_user_op(const char* name, sfx_user_launch_fn fn, void* user, uint32
 // calls the launcher with the staged operands as views; SFX_ERR_USER on failure
 int run_user_op(const UserOp& u, const OpLaunch& op, int dev, void* stream, std::string& err);
 
+// Task lookup by tid (sfx_wait_task, sfx_task_state, extern_done, duplicate
+// check).  Tids are process-global increasing counters, so a paged direct table
+// (64 Ki tids per page, freed when its last task retires) replaces a hash map:
+// the map's rehash of ~10^6 entries stalled insertion for ~100 ms once it grew
+// past a bucket-count threshold (a C2 step after a 20-step burst).
+class TidMap {
+ public:
+  Task* get(uint64_t tid) const {
+    auto it = pages_.find(tid >> kBits);
+    return it == pages_.end() ? nullptr : it->second.slot[tid & kMask];
+  }
+  size_t count(uint64_t tid) const { return get(tid) ? 1 : 0; }
+  void put(uint64_t tid, Task* t) {
+    Page& p = pages_[tid >> kBits];
+    if (!p.slot) p.slot.reset(new Task*[size_t(1) << kBits]());
+    if (!p.slot[tid & kMask]) p.live += 1;
+    p.slot[tid & kMask] = t;
+  }
+  void erase(uint64_t tid) {
+    auto it = pages_.find(tid >> kBits);
+    if (it == pages_.end() || !it->second.slot[tid & kMask]) return;
+    it->second.slot[tid & kMask] = nullptr;
+    if (--it->second.live == 0) pages_.erase(it);
+  }
+
+ private:
+  static constexpr int kBits = 16;
+  static constexpr uint64_t kMask = (uint64_t(1) << kBits) - 1;
+  struct Page {
+    std::unique_ptr<Task*[]> slot;
+    size_t live = 0;
+  };
+  std::unordered_map<uint64_t, Page> pages_;
+};
+
 // One step of a planned task, issued outside the runtime lock.
 struct Action {
   enum Kind { WAIT, H2D, D2H, P2P, RECORD } kind;
@@ -458,7 +493,7 @@ class Runtime {
   uint64_t max_handle_bytes_ = 0;
   std::vector<std::unique_ptr<Handle>> handle_store_;
   std::unordered_map<uint32_t, std::unique_ptr<Graph>> graphs_;
-  std::unordered_map<uint64_t, Task*> tasks_by_tid_;
+  TidMap tasks_by_tid_;
   std::vector<std::unique_ptr<Task>> task_store_;  // every Task object ever allocated
   std::vector<Task*> task_free_;                   // retired, reusable
   std::vector<Handle*> retire_pending_;            // handles whose active slot moved (history-free)
