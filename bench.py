@@ -153,21 +153,31 @@ class ClockSampler:
         self.samples = []
         self._stop = threading.Event()
         self._th = None
+        self._proc = None
 
     def start(self):
+        # ONE long-running `nvidia-smi ... -lms 200` (the profiling recipe's clocks
+        # line), not a process per sample: spawning nvidia-smi every 0.2 s costs a
+        # driver/NVML initialisation each time on the host the runtime runs on
         ids = ",".join(str(i) for i in sorted(set(self.index)))
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", "-i", ids, "--query-gpu=" + self.FIELDS,
+                                           "--format=csv,noheader,nounits", "-lms", "200"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self._proc = None
+            return self
 
         def run():
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(["nvidia-smi", "-i", ids, "--query-gpu=" + self.FIELDS,
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    for line in out.splitlines():
+            try:
+                for line in self._proc.stdout:
+                    if self._stop.is_set():
+                        break
+                    line = line.strip()
+                    if line:
                         self.samples.append([x.strip() for x in line.split(",")])
-                except Exception:
-                    pass
-                self._stop.wait(0.2)
+            except Exception:
+                pass
 
         self._th = threading.Thread(target=run, daemon=True)
         self._th.start()
@@ -175,6 +185,13 @@ class ClockSampler:
 
     def stop(self):
         self._stop.set()
+        proc = getattr(self, "_proc", None)
+        if proc is not None:
+            proc.terminate()
+            try:
+                proc.wait(timeout=10)
+            except Exception:
+                proc.kill()
         if self._th:
             self._th.join(timeout=10)
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
